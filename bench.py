@@ -1,0 +1,437 @@
+#!/usr/bin/env python3
+"""Headline benchmark: 4K frames/s through Tangram's frame->canvas path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): per GPU one synthetic 3840x2160 RGB
+camera, 300 frames, moderate RoI density (generate_trace defaults with
+roi_proportion_mean=0.10, roi_max_dim=480, fps=30, seed 1000+camera), 4x4
+zone grid, 1024x1024 canvases.  A step is one pass of the whole path over the
+camera's 300 device-resident frames: K1 mask+cells -> K2-K4 planner -> scan
+-> K5 canvas gather (plus, at N>1, the NCCL allgather of patch descriptors).
+Inputs (7.5 GB per GPU) are far larger than L2, so no flush is needed.
+
+`value` is whole-job device throughput (frames/s, max-over-ranks time),
+`e2e` the same through the public API with pinned host frames copied in and
+descriptors copied out every step, `roofline` K1 against measured HBM
+bandwidth, `cpu_baseline` the CPU path on the box's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+W, H, C = 3840, 2160, 3
+FRAME_BYTES = W * H * C
+METRIC = "4K frames/sec (RoI->patch->stitched canvas)"
+WORKLOAD = ("BASELINE configs[1]: synthetic 3840x2160 RGB camera per GPU, 300 frames, moderate "
+            "RoI density (roi_proportion_mean=0.10, roi_max_dim=480), 4x4 zones, 1024x1024 canvases")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=300)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 6
+                          for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(sm)}
+
+
+# ================================================================== ours
+def run_ours(args):
+    rank, world, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    from paper_2404_09267_b200 import api as A
+    from paper_2404_09267_b200 import _native as N
+
+    n = args.frames
+    ctx = A.Context(local)
+    camera = rank
+    seed = 1000 + camera
+    t_us, rects = A.generate_trace(n_frames=n, fps=30.0, frame_width=W, frame_height=H,
+                                   roi_proportion_mean=0.10, roi_max_dim=480, seed=seed)
+    ring = A.FrameRing(ctx, W, H, n)
+    ring.synthesize(A.derive_seed(seed, "pixels"), rects)
+    zones = 16
+    max_canv = n * zones
+    pipe = A.Pipeline(ctx, W, H, max_frames=n, max_canvases=max_canv)
+    d_cur, d_prev = ring.tables()
+    d_ids, d_gen = ctx.malloc(8 * n), ctx.malloc(8 * n)
+    ctx.upload(d_ids, np.arange(n, dtype=np.uint64))
+    ctx.upload(d_gen, np.array(t_us, np.int64))
+    d_canv = ctx.malloc(pipe.canvas_bytes * max_canv)
+    stream = ctx.new_stream()
+    lib = N.lib()
+
+    # descriptor allgather buffers (N > 1): per-frame placements + counts
+    desc_bytes = n * zones * 32 + n * 4
+    if dist is not None:
+        import torch
+        send = torch.empty(desc_bytes, dtype=torch.uint8, device=f"cuda:{local}")
+        recv = torch.empty(desc_bytes * world, dtype=torch.uint8, device=f"cuda:{local}")
+        tstream = torch.cuda.ExternalStream(stream, device=f"cuda:{local}")
+
+    def step(evs=None):
+        if evs:
+            ctx.record(evs[0], stream)
+        A.check(lib.tg_pipeline_stage_mask(pipe.handle, n, d_cur, d_prev, stream))
+        if evs:
+            ctx.record(evs[1], stream)
+        A.check(lib.tg_pipeline_stage_plan(pipe.handle, n, d_ids, d_gen, 0, stream))
+        if evs:
+            ctx.record(evs[2], stream)
+        A.check(lib.tg_pipeline_stage_gather(pipe.handle, n, d_cur, d_canv, stream))
+        if evs:
+            ctx.record(evs[3], stream)
+        if dist is not None:
+            v = pipe.views
+            ctx.memcpy(send.data_ptr(), v.placements, n * zones * 32, 2, stream)
+            ctx.memcpy(send.data_ptr() + n * zones * 32, v.n_placements, n * 4, 2, stream)
+            with torch.cuda.stream(tstream):
+                dist.all_gather_into_tensor(recv, send)
+
+    for _ in range(args.warmup):
+        step()
+    ctx.stream_sync(stream)
+    res = pipe.results(n, stream)
+
+    K = args.steps
+    evs = [[ctx.event() for _ in range(4)] for _ in range(K)]
+    e0, e1 = ctx.event(), ctx.event()
+    clocks = Clocks(local)
+    if dist is not None:
+        torch.cuda.synchronize()
+        dist.barrier()
+    ctx.synchronize()
+    clocks.start()
+    ctx.record(e0, stream)
+    for k in range(K):
+        step(evs[k])
+    ctx.record(e1, stream)
+    ctx.stream_sync(stream)
+    if dist is not None:
+        torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = ctx.elapsed_ms(e0, e1)
+    k1 = [ctx.elapsed_ms(e[0], e[1]) for e in evs]
+    plan = [ctx.elapsed_ms(e[1], e[2]) for e in evs]
+    gat = [ctx.elapsed_ms(e[2], e[3]) for e in evs]
+    if dist is not None:
+        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_step = total_ms / K
+    frames_total = n * K * world
+    value = frames_total / (total_ms / 1e3)
+
+    # algorithmic bytes: 2*W*H*C per frame + admitted patch
+    # bytes + every canvas byte.
+    adm_bytes = 0
+    for f in range(n):
+        for j, p in enumerate(res["patch_list"][f]):
+            if res["admitted"][f, j]:
+                adm_bytes += p.rect.w * p.rect.h * C
+    ncanv = int(res["total_canvases"])
+    k1_bytes = n * 2 * FRAME_BYTES
+    b_run = k1_bytes + adm_bytes + ncanv * pipe.canvas_bytes
+    peak, peak_src = peaks()
+    k1_ms = statistics.mean(k1)
+    achieved = k1_bytes / (k1_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(tp):
+        try:
+            tj = json.load(open(tp))
+            traffic = tj["dram_bytes_per_frame"] * n
+        except Exception:
+            traffic = None
+
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": "frames/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (generate_trace rects, frozen pixel spec, device-resident)",
+        "config": {"workload": WORKLOAD, "frames_per_gpu": n, "width": W, "height": H,
+                   "zones": "4x4", "canvas": "1024x1024", "threshold": 25, "dilate_radius": 2,
+                   "l2": "inputs larger than L2 (7.5 GB/GPU), no flush",
+                   "parallelism": f"cameras sharded, {world} GPU(s)" +
+                                  (", NCCL allgather of descriptors" if world > 1 else "")},
+        "roofline": {"bound": "hbm", "kernel": "mask_cells_kernel (K1)",
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "algorithmic_bytes_per_launch": k1_bytes, "peak_source": peak_src,
+                     "launch_ms": round(k1_ms, 4)},
+        "path": {"B_run_bytes_per_step": b_run, "path_GBps": round(b_run / (ms_step / 1e3) / 1e9, 1),
+                 "path_frac": round(b_run / (ms_step / 1e3) / 1e9 / peak, 4),
+                 "stage_ms": {"k1_mask_cells": round(k1_ms, 4), "plan+scan": round(statistics.mean(plan), 4),
+                              "gather": round(statistics.mean(gat), 4)},
+                 "rois": int(res["n_rois"].sum()), "patches": int(res["n_patches"].sum()),
+                 "admitted": int(res["admitted"].sum()), "canvases": ncanv,
+                 "canvas_efficiency_mean": round(adm_bytes / max(1, ncanv * pipe.canvas_bytes), 4)},
+        "clocks": clk,
+        "gpu_launches": 4 * K,
+    }
+
+    if not args.no_e2e:
+        out["e2e"] = e2e(ctx, pipe, ring, n, d_ids, d_gen, d_canv, stream, args, world, dist)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(ring, t_us, n)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e(ctx, pipe, ring, n, d_ids, d_gen, d_canv, stream, args, world, dist):
+    """Same metric through the public API with host buffers: every step
+    copies the camera's frames from pinned host memory (chunked on a copy
+    stream, overlapped with compute) and reads back the patch/placement
+    descriptors the batcher consumes."""
+    from paper_2404_09267_b200 import api as A
+    from paper_2404_09267_b200 import _native as N
+    lib = N.lib()
+    slots = n + 1
+    host = ctx.malloc_host(FRAME_BYTES * slots)
+    ctx.memcpy(host, ring.base, FRAME_BYTES * slots, 1, stream)
+    ctx.stream_sync(stream)
+    chunk = 30
+    nch = (n + chunk - 1) // chunk
+    zones = pipe.zones
+    cstream = ctx.new_stream()
+    per_chunk = chunk * zones * 96 + chunk * 12
+    hdesc = ctx.malloc_host(nch * per_chunk)  # pinned, so D2H stays asynchronous
+    tabs = [ring.tables(c * chunk, min(chunk, n - c * chunk)) for c in range(nch)]
+    copied = [ctx.event() for _ in range(nch)]
+    step_done = ctx.event()
+    ctx.record(step_done, stream)
+    v = pipe.views
+
+    def one():
+        h2d = d2h = 0
+        # frames of this step may only be overwritten once the previous
+        # step's compute has read them
+        A.check(lib.tg_stream_wait_event(ctx.handle, cstream, step_done))
+        for c in range(nch):
+            f0, fc = c * chunk, min(chunk, n - c * chunk)
+            lo = 0 if c == 0 else f0 + 1  # slot 0 (background) travels with chunk 0
+            hi = f0 + fc + 1
+            nb = (hi - lo) * FRAME_BYTES
+            ctx.memcpy(ring.slots[lo], host + lo * FRAME_BYTES, nb, 0, cstream)
+            h2d += nb
+            ctx.record(copied[c], cstream)
+            A.check(lib.tg_stream_wait_event(ctx.handle, stream, copied[c]))
+            d_cur, d_prev = tabs[c]
+            first = 0 if c == 0 else 0xFFFFFFFFFFFFFFFF  # TG_CONTINUE_PATCH_IDS
+            A.check(lib.tg_pipeline_run(pipe.handle, fc, d_cur, d_prev, d_ids + 8 * f0,
+                                        d_gen + 8 * f0, first, d_canv, stream))
+            buf = hdesc + c * per_chunk
+            nbp = fc * zones * 32
+            ctx.memcpy(buf, v.placements, nbp, 1, stream)
+            ctx.memcpy(buf + nbp, v.n_placements, fc * 4, 1, stream)
+            ctx.memcpy(buf + nbp + fc * 4, v.n_canvases, fc * 4, 1, stream)
+            nbq = fc * zones * 64
+            ctx.memcpy(buf + nbp + fc * 8, v.patches, nbq, 1, stream)
+            ctx.memcpy(buf + nbp + fc * 8 + nbq, v.n_patches, fc * 4, 1, stream)
+            d2h += nbp + nbq + 12 * fc
+        ctx.record(step_done, stream)
+        return h2d, d2h
+
+    for _ in range(max(1, args.warmup)):
+        one()
+    ctx.stream_sync(stream)
+    e0, e1 = ctx.event(), ctx.event()
+    ctx.synchronize()
+    ctx.record(e0, cstream)
+    for _ in range(args.steps):
+        h2d, d2h = one()
+    ctx.record(e1, stream)
+    ctx.stream_sync(stream)
+    ms = ctx.elapsed_ms(e0, e1)
+    if dist is not None:
+        import torch
+        t = torch.tensor([ms], device=f"cuda:{ctx.device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ctx.free_host(host)
+    ctx.free_host(hdesc)
+    return {"value": round(n * args.steps * world / (ms / 1e3), 1), "unit": "frames/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "note": "pinned host frames -> device in 30-frame chunks overlapped with compute; "
+                    "patch + placement descriptors read back; PCIe-bound"}
+
+
+def cpu_baseline(ring, t_us, n, sample=None):
+    """The CPU path (reference partition/stitch_all from oracle/_ref when
+    built, else the oracle port) over a bounded sample of this workload."""
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    sample = sample or min(n, max(8, min(48, 2 * threads)))
+    frames = [ring.download_frame(i) for i in range(sample + 1)]
+    return cpu_measure(frames, t_us[:sample], threads)
+
+
+def cpu_measure(frames, t_us, threads, passes=None):
+    from oracle import oracle as O
+    lib = "ref" if O.have_ref() else "port"
+    sample = len(frames) - 1
+    params = dict(width=W, height=H, pitch=W * C, threshold=25, radius=2, zones_x=4, zones_y=4,
+                  canvas_w=1024, canvas_h=1024, bytes_per_pixel=1.5, slo_us=1_000_000, max_rois=1024,
+                  threads=threads)
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        O.process_frames(params, frames[1:], frames[:-1], list(range(sample)), t_us, lib=lib,
+                         want_canvases=True, canvas_cap=sample * 16)
+        times.append(time.perf_counter() - t0)
+        if (passes and len(times) >= passes) or (not passes and time.perf_counter() - t_start > 10.0) \
+                or len(times) >= 20:
+            break
+    best = statistics.median(times)
+    return {"value": round(sample / best, 2), "unit": "frames/s", "cores": threads,
+            "kind": "reference" if lib == "ref" else "port",
+            "sample": f"{sample} frames of the same 4K workload, {len(times)} passes, median; pixel "
+                      f"stages restated (absent from the reference), partition/stitch_all "
+                      f"{'= reference code (oracle/_ref)' if lib == 'ref' else '= oracle port'}; "
+                      "canvases materialized"}
+
+
+# ============================================================= reference
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    sample = min(args.frames, max(8, min(32, threads)))
+    cfg = O.gen_cfg(seed=1000, n_frames=args.frames, fps=30.0, frame_width=W, frame_height=H,
+                    roi_proportion_mean=0.10, roi_max_dim=480)
+    t_us, rects = O.generate_trace(cfg)
+    ps = O.derive_seed(1000, "pixels")
+    with ThreadPoolExecutor(threads) as ex:
+        frames = list(ex.map(lambda i: O.synth_frame(W, H, ps, i, rects[i] if i >= 0 else []),
+                             range(-1, sample)))
+    lib = "ref" if O.have_ref() else "port"
+    params = dict(width=W, height=H, pitch=W * C, threshold=25, radius=2, zones_x=4, zones_y=4,
+                  canvas_w=1024, canvas_h=1024, bytes_per_pixel=1.5, slo_us=1_000_000, max_rois=1024,
+                  threads=threads)
+
+    def step():
+        O.process_frames(params, frames[1:], frames[:-1], list(range(sample)), t_us[:sample],
+                         lib=lib, want_canvases=True, canvas_cap=sample * 16)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = sample * args.steps / dt
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (generate_trace rects, frozen pixel spec, host memory)",
+        "config": {"workload": WORKLOAD, "frames_per_step": sample, "width": W, "height": H},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 2), "unit": "frames/s", "cores": threads,
+                         "kind": "reference" if lib == "ref" else "port",
+                         "sample": f"{sample} frames of the workload per step; reference "
+                                   "partition()/stitch_all() compiled as-is (oracle/_ref), pixel "
+                                   "stages restated (absent from the reference)"},
+        "e2e": {"value": round(value, 2), "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

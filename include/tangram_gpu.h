@@ -1,0 +1,278 @@
+/*
+ * tangram_gpu.h -- C ABI of the B200-native Tangram frame->canvas path.
+ *
+ * The reference (/root/reference/proj/include/tangram) is a header-only C++20
+ * library with no FFI of its own; its public surface for this path is the
+ * C++ API of partition.hpp and stitch.hpp.  This header is
+ * the thin C layer underneath the C++ drop-in (include/tangram/[name].hpp), plus
+ * the batched device entry points that carry the data-parallel hot path:
+ *
+ *   frames -> [K1 mask+cells] -> [K2 RoI boxes, K3 partition, K4 stitch plan]
+ *          -> [scan] -> [K5 canvas gather]            (all stream-ordered)
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  "d_" pointers are device memory,
+ *     everything else is host memory.
+ *   - Every call returns a tg_status.  On failure tg_last_error() returns the
+ *     message; messages reuse the reference's exception texts so the C++
+ *     drop-in can rethrow the same std::invalid_argument / std::out_of_range.
+ *   - Stream-ordered calls take a `void* stream` (a cudaStream_t; NULL = the
+ *     context's own stream).  Device-side errors are latched in the context
+ *     and reported by the next synchronizing call.
+ *   - One context per device; a context is not thread-safe.
+ *   - There is no CPU fallback: without a CUDA device every compute call
+ *     returns TG_ERR_NO_DEVICE.
+ */
+#ifndef TANGRAM_GPU_H
+#define TANGRAM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TG_ABI_VERSION 1
+#define TG_CELL_SIZE 16   /* patch-grid cell edge in pixels (frozen spec) */
+#define TG_CONTINUE_PATCH_IDS (~(uint64_t)0)
+
+typedef enum {
+  TG_OK = 0,
+  TG_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  TG_ERR_OUT_OF_RANGE = 2,     /* reference: std::out_of_range    */
+  TG_ERR_CAPACITY = 3,         /* a fixed device capacity was exceeded */
+  TG_ERR_CUDA = 4,             /* CUDA runtime failure */
+  TG_ERR_NO_DEVICE = 5         /* no usable CUDA device: no fallback exists */
+} tg_status;
+
+/* ---- POD mirrors of the reference value types --------------------------- */
+/* tangram::Rect (geometry.hpp:28-38): bottom-left origin, y up; memory row
+ * r of a frame/canvas is reference y = r. */
+typedef struct { int32_t x, y, w, h; } tg_rect;
+
+/* tangram::FrameSpec (partition.hpp:40-46) */
+typedef struct {
+  uint64_t frame_id;
+  int32_t width, height;
+  int64_t generation_time_us;
+  int64_t slo_us;
+} tg_frame_spec;
+
+/* tangram::PartitionConfig (partition.hpp:49-52) */
+typedef struct { int32_t zones_x, zones_y; } tg_partition_config;
+
+/* tangram::PatchMeta (partition.hpp:56-64), 64 bytes */
+typedef struct {
+  uint64_t patch_id;
+  uint64_t source_frame_id;
+  tg_rect rect;
+  int64_t generation_time_us;
+  int64_t slo_us;
+  int64_t deadline_us;
+  int64_t size_bytes;
+} tg_patch_meta;
+
+/* tangram::CanvasSpec (stitch.hpp:32-40) */
+typedef struct {
+  int32_t width, height;
+  double vram_per_canvas_gb;
+} tg_canvas_spec;
+
+/* tangram::Placement (stitch.hpp:42-46), 32 bytes */
+typedef struct {
+  uint64_t patch_id;
+  int32_t canvas_index;
+  tg_rect position;
+  int32_t reserved;
+} tg_placement;
+
+/* One live guillotine free rect (CanvasState::free_rects element,
+ * stitch.hpp:48-52).  `seq` is its insertion order: sorting a canvas's
+ * rects by seq reproduces the reference's list order. */
+typedef struct {
+  tg_rect rect;
+  int32_t canvas_index;
+  int32_t seq;
+} tg_free_rect;
+
+typedef struct tg_ctx tg_ctx;
+typedef struct tg_pipeline tg_pipeline;
+typedef struct tg_graph tg_graph;
+
+/* ---- library / context --------------------------------------------------- */
+int tg_abi_version(void);
+const char* tg_last_error(void);
+tg_status tg_device_count(int32_t* count);
+tg_status tg_ctx_create(int32_t device, tg_ctx** out);
+void tg_ctx_destroy(tg_ctx* ctx);
+void* tg_ctx_stream(tg_ctx* ctx);
+tg_status tg_ctx_synchronize(tg_ctx* ctx); /* waits; reports latched device errors */
+tg_status tg_device_sm_count(tg_ctx* ctx, int32_t* sms);
+
+/* ---- memory / streams / events (plumbing for callers without a CUDA
+ *      runtime of their own) ----------------------------------------------- */
+tg_status tg_malloc_device(tg_ctx* ctx, size_t bytes, void** d_ptr);
+tg_status tg_free_device(tg_ctx* ctx, void* d_ptr);
+tg_status tg_malloc_host(tg_ctx* ctx, size_t bytes, void** h_ptr); /* pinned */
+tg_status tg_free_host(tg_ctx* ctx, void* h_ptr);
+/* kind: 0 host->device, 1 device->host, 2 device->device; async on stream */
+tg_status tg_memcpy_async(tg_ctx* ctx, void* dst, const void* src, size_t bytes, int32_t kind,
+                          void* stream);
+tg_status tg_memset_async(tg_ctx* ctx, void* d_ptr, int32_t value, size_t bytes, void* stream);
+tg_status tg_stream_create(tg_ctx* ctx, void** stream);
+tg_status tg_stream_destroy(tg_ctx* ctx, void* stream);
+tg_status tg_stream_synchronize(tg_ctx* ctx, void* stream);
+tg_status tg_event_create(tg_ctx* ctx, void** event);
+tg_status tg_event_destroy(tg_ctx* ctx, void* event);
+tg_status tg_event_record(tg_ctx* ctx, void* event, void* stream);
+tg_status tg_event_elapsed_ms(tg_ctx* ctx, void* start, void* stop, float* ms);
+tg_status tg_stream_wait_event(tg_ctx* ctx, void* stream, void* event);
+
+/* ---- drop-in rect-level API (host in, host out, blocking) ----------------
+ * Replaces, call for call:
+ *   make_zones  partition.hpp:69-88    (host arithmetic)
+ *   assign_rois partition.hpp:93-112   (device)
+ *   partition   partition.hpp:119-143  (device)
+ *   stitch_all  stitch.hpp:108-146     (device, bit-identical placements)   */
+tg_status tg_make_zones(const tg_frame_spec* frame, tg_partition_config cfg, tg_rect* zones,
+                        int32_t zones_cap);
+tg_status tg_assign_rois(tg_ctx* ctx, const tg_rect* rois, int32_t n_rois, const tg_rect* zones,
+                         int32_t n_zones, int32_t* zone_of);
+tg_status tg_partition(tg_ctx* ctx, const tg_frame_spec* frame, tg_partition_config cfg,
+                       const tg_rect* rois, int32_t n_rois, double bytes_per_pixel,
+                       uint64_t first_patch_id, tg_patch_meta* patches, int32_t patches_cap,
+                       int32_t* n_patches);
+/* placements[i] is queue[i]'s placement; free_rects receives every canvas's
+ * live free set (canvas-major, each canvas in reference list order). */
+tg_status tg_stitch_all(tg_ctx* ctx, const tg_patch_meta* queue, int32_t n,
+                        tg_canvas_spec spec, tg_placement* placements, int32_t* n_canvases,
+                        tg_free_rect* free_rects, int32_t free_cap, int32_t* n_free);
+
+/* ---- batched device rect-level API (stream-ordered, device buffers) ------
+ * Many independent queues stitched at once, one warp per queue.
+ * d_queue_offsets[q]..d_queue_offsets[q+1] index d_queue; outputs are
+ * indexed the same way; d_n_canvases[q] receives each queue's canvas count
+ * (-1 when the queue failed).  total_patches = d_queue_offsets[n_queues].
+ * d_free_ws must hold 2*total_patches+n_queues tg_free_rect; queue q's live
+ * free rects are d_free_ws[2*offsets[q]+q ..][0 .. d_n_free[q]) (unordered;
+ * sort each canvas by seq for the reference order).                        */
+tg_status tg_stitch_batch(tg_ctx* ctx, int32_t n_queues, int32_t total_patches,
+                          const int32_t* d_queue_offsets, const tg_patch_meta* d_queue,
+                          tg_canvas_spec spec, tg_placement* d_placements,
+                          int32_t* d_n_canvases, tg_free_rect* d_free_ws, int32_t* d_n_free,
+                          void* stream);
+
+/* ---- the hot path: frames -> canvases ------------------------------------ */
+typedef struct {
+  int32_t width, height;       /* frame size in pixels, width % 16 == 0 */
+  int32_t pitch;               /* bytes between rows, % 16 == 0, >= 3*width */
+  int32_t threshold;           /* fg if max_c |cur-prev| > threshold (default 25) */
+  int32_t dilate_radius;       /* square structuring element radius, 0..8 (default 2) */
+  tg_partition_config partition;
+  tg_canvas_spec canvas;
+  double bytes_per_pixel;      /* PatchMeta::size_bytes model (default 1.5) */
+  int64_t slo_us;
+  int32_t max_frames;          /* frames per run */
+  int32_t max_rois_per_frame;  /* RoI slots per frame (default 1024) */
+  int64_t max_canvases;        /* canvases the output buffer holds */
+  int32_t keep_mask;           /* 1: also write the dilated bit mask (debug/parity) */
+} tg_pipeline_params;
+
+tg_status tg_pipeline_params_default(int32_t width, int32_t height, tg_pipeline_params* out);
+tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_pipeline** out);
+void tg_pipeline_destroy(tg_pipeline* p);
+
+/* Runs every stage for n_frames frames, asynchronously on `stream`.
+ * d_cur / d_prev: DEVICE arrays of n_frames device pointers (frame i and its
+ * predecessor).  d_frame_ids / d_gen_us: device arrays of n_frames.  Patch
+ * ids are numbered from first_patch_id in frame order (sim.hpp:249-251);
+ * first_patch_id == TG_CONTINUE_PATCH_IDS continues where the previous run
+ * on this pipeline stopped (device-side, so chunked streams need no sync);
+ * canvases are numbered in frame order and written to
+ * d_canvases + k * canvas.width * canvas.height * 3 (uint8 HWC RGB, every
+ * byte written: patch pixels or zero). */
+tg_status tg_pipeline_run(tg_pipeline* p, int32_t n_frames, const uint8_t* const* d_cur,
+                          const uint8_t* const* d_prev, const uint64_t* d_frame_ids,
+                          const int64_t* d_gen_us, uint64_t first_patch_id,
+                          uint8_t* d_canvases, void* stream);
+
+/* The same stages one by one (parity tests, profiling). */
+tg_status tg_pipeline_stage_mask(tg_pipeline* p, int32_t n_frames, const uint8_t* const* d_cur,
+                                 const uint8_t* const* d_prev, void* stream);
+tg_status tg_pipeline_stage_plan(tg_pipeline* p, int32_t n_frames, const uint64_t* d_frame_ids,
+                                 const int64_t* d_gen_us, uint64_t first_patch_id, void* stream);
+tg_status tg_pipeline_stage_gather(tg_pipeline* p, int32_t n_frames,
+                                   const uint8_t* const* d_cur, uint8_t* d_canvases,
+                                   void* stream);
+
+/* Captures one tg_pipeline_run into a CUDA graph (same arguments) so a
+ * steady-state step is a single graph launch. */
+tg_status tg_pipeline_graph_create(tg_pipeline* p, int32_t n_frames, const uint8_t* const* d_cur,
+                                   const uint8_t* const* d_prev, const uint64_t* d_frame_ids,
+                                   const int64_t* d_gen_us, uint64_t first_patch_id,
+                                   uint8_t* d_canvases, void* stream, tg_graph** out);
+tg_status tg_graph_launch(tg_graph* g, void* stream);
+void tg_graph_destroy(tg_graph* g);
+
+/* Device-resident results of the last run (valid until the next run);
+ * these feed the batcher / descriptor allgather without a host round trip. */
+typedef struct {
+  int32_t* n_rois;          /* [max_frames] */
+  tg_rect* rois;            /* [max_frames * max_rois_per_frame] */
+  int32_t* n_patches;       /* [max_frames] (admitted or not) */
+  tg_patch_meta* patches;   /* [max_frames * zones] */
+  uint8_t* admitted;        /* [max_frames * zones] */
+  int32_t* n_placements;    /* [max_frames] == admitted patches */
+  tg_placement* placements; /* [max_frames * zones], canvas_index frame-local */
+  int32_t* n_canvases;      /* [max_frames] */
+  int64_t* canvas_base;     /* [max_frames + 1] global index of each frame's canvas 0 */
+  uint32_t* cells;          /* [max_frames * cells_y * cells_x] packed cell summaries */
+  uint32_t* mask;           /* [max_frames * height * ceil(width/32)] if keep_mask */
+  int32_t zones, cells_x, cells_y, mask_words;
+} tg_pipeline_views;
+tg_status tg_pipeline_device_views(tg_pipeline* p, tg_pipeline_views* out);
+
+/* Blocking copies of the last run's results to host (waits on `stream`,
+ * then reports latched device errors). */
+tg_status tg_pipeline_download(tg_pipeline* p, int32_t n_frames, void* stream,
+                               int32_t* n_rois, tg_rect* rois, int32_t* n_patches,
+                               tg_patch_meta* patches, uint8_t* admitted,
+                               int32_t* n_placements, tg_placement* placements,
+                               int32_t* n_canvases, int64_t* total_canvases);
+/* Free rects of frame f's canvases (canvas-major, reference list order). */
+tg_status tg_pipeline_free_rects(tg_pipeline* p, int32_t frame, tg_free_rect* out, int32_t cap,
+                                 int32_t* n_out);
+
+/* ---- synthetic workload (fixture source; not part of the timed path) -----
+ * trace.hpp:145-231 generate_trace, restated (std::mt19937_64 + the
+ * reference's hand-rolled distributions).  Writes t_us[n_frames],
+ * roi_counts[n_frames] and the RoIs back to back; returns TG_ERR_CAPACITY if
+ * roi_cap is too small. */
+typedef struct {
+  int32_t n_frames;
+  double fps;
+  int32_t frame_width, frame_height;
+  double roi_proportion_mean, roi_proportion_jitter;
+  double burst_probability, burst_multiplier;
+  int32_t roi_count_min, roi_count_max;
+  double roi_aspect_min, roi_aspect_max;
+  int32_t roi_max_dim;
+  uint64_t seed;
+} tg_workload_config;
+tg_status tg_workload_default(tg_workload_config* out);
+uint64_t tg_derive_seed(uint64_t master, const char* component);
+tg_status tg_generate_trace(const tg_workload_config* cfg, int64_t* t_us, int32_t* roi_counts,
+                            tg_rect* rois, int64_t roi_cap, int64_t* n_rois_total);
+/* Synthesizes frames on the device (frozen pixel spec).
+ * Frame i gets time index t0 + i (-1 = background only), its RoIs are
+ * d_rects[d_rect_offsets[i] .. d_rect_offsets[i+1]). */
+tg_status tg_synth_frames(tg_ctx* ctx, int32_t width, int32_t height, int32_t pitch,
+                          uint64_t pixel_seed, int32_t n_frames, int32_t t0,
+                          const tg_rect* d_rects, const int32_t* d_rect_offsets,
+                          uint8_t* const* d_frames, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TANGRAM_GPU_H */

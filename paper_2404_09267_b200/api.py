@@ -1,0 +1,588 @@
+"""Python mirror of the reference's hot-path API, executed on the B200.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/tangram/{geometry,partition,stitch}.hpp:
+
+* ``partition(frame, cfg, rois, bytes_per_pixel, first_patch_id=0)``
+  (partition.hpp:119-143) and ``stitch_all(queue, spec)`` (stitch.hpp:108-146)
+  run as CUDA kernels through the C ABI;
+* ``std::invalid_argument`` surfaces as :class:`InvalidArgument` (a
+  ``ValueError``) and ``std::out_of_range`` as :class:`OutOfRange` (an
+  ``IndexError``), with the reference's message texts;
+* value helpers (``area``, ``overlap_area``, ``canvas_efficiency``,
+  ``extract_canvas``, ``concat_stitches``, ``dump_layout``) are plain data
+  manipulation, as in the reference headers.
+
+The frame->canvas hot path itself is :class:`Pipeline` (device-resident
+frames in, device-resident canvases out).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _native as N
+
+
+# ---------------------------------------------------------------- errors
+class TangramError(RuntimeError):
+    pass
+
+
+class InvalidArgument(ValueError):
+    """Reference: std::invalid_argument."""
+
+
+class OutOfRange(IndexError):
+    """Reference: std::out_of_range."""
+
+
+class CapacityError(TangramError):
+    pass
+
+
+class CudaError(TangramError):
+    pass
+
+
+class NoDevice(TangramError):
+    pass
+
+
+_ERRS = {N.TG_ERR_INVALID_ARGUMENT: InvalidArgument, N.TG_ERR_OUT_OF_RANGE: OutOfRange,
+         N.TG_ERR_CAPACITY: CapacityError, N.TG_ERR_CUDA: CudaError, N.TG_ERR_NO_DEVICE: NoDevice}
+
+
+def check(status: int) -> None:
+    if status != N.TG_OK:
+        msg = N.lib().tg_last_error().decode()
+        raise _ERRS.get(status, TangramError)(msg)
+
+
+# ------------------------------------------------------------ value types
+@dataclass(frozen=True)
+class Rect:
+    """geometry.hpp:28-38 -- bottom-left origin; memory row r is y = r."""
+    x: int = 0
+    y: int = 0
+    w: int = 0
+    h: int = 0
+
+    def right(self) -> int:
+        return self.x + self.w
+
+    def top(self) -> int:
+        return self.y + self.h
+
+
+def area(r: Rect) -> int:
+    return r.w * r.h
+
+
+def overlap_area(a: Rect, b: Rect) -> int:
+    ow = min(a.right(), b.right()) - max(a.x, b.x)
+    oh = min(a.top(), b.top()) - max(a.y, b.y)
+    return ow * oh if ow > 0 and oh > 0 else 0
+
+
+def contains(outer: Rect, inner: Rect) -> bool:
+    return (inner.x >= outer.x and inner.y >= outer.y and inner.right() <= outer.right()
+            and inner.top() <= outer.top())
+
+
+def enclosing_rect(rects: Sequence[Rect]) -> Rect:
+    if not rects:
+        raise InvalidArgument("empty rect set")
+    x0 = min(r.x for r in rects)
+    y0 = min(r.y for r in rects)
+    x1 = max(r.right() for r in rects)
+    y1 = max(r.top() for r in rects)
+    return Rect(x0, y0, x1 - x0, y1 - y0)
+
+
+@dataclass
+class FrameSpec:
+    frame_id: int = 0
+    width: int = 0
+    height: int = 0
+    generation_time_us: int = 0
+    slo_us: int = 0
+
+
+@dataclass
+class PartitionConfig:
+    zones_x: int = 4
+    zones_y: int = 4
+
+
+@dataclass
+class PatchMeta:
+    patch_id: int = 0
+    source_frame_id: int = 0
+    rect: Rect = field(default_factory=Rect)
+    generation_time_us: int = 0
+    slo_us: int = 0
+    deadline_us: int = 0
+    size_bytes: int = 0
+
+
+@dataclass
+class CanvasSpec:
+    width: int = 1024
+    height: int = 1024
+    vram_per_canvas_gb: float = 1.0
+
+    def surface_area(self) -> int:
+        return self.width * self.height
+
+
+@dataclass
+class Placement:
+    patch_id: int = 0
+    canvas_index: int = 0
+    position: Rect = field(default_factory=Rect)
+
+
+@dataclass
+class CanvasState:
+    placements: list = field(default_factory=list)
+    free_rects: list = field(default_factory=list)
+    used_area: int = 0
+
+
+@dataclass
+class StitchResult:
+    spec: CanvasSpec = field(default_factory=CanvasSpec)
+    canvases: list = field(default_factory=list)
+    placement_index: dict = field(default_factory=dict)
+
+    def canvas_count(self) -> int:
+        return len(self.canvases)
+
+    def empty(self) -> bool:
+        return not self.canvases
+
+
+def _rect(r) -> Rect:
+    return r if isinstance(r, Rect) else Rect(*r)
+
+
+def _c_rect(r: Rect) -> N.tg_rect:
+    return N.tg_rect(r.x, r.y, r.w, r.h)
+
+
+def _py_rect(r: N.tg_rect) -> Rect:
+    return Rect(r.x, r.y, r.w, r.h)
+
+
+def _c_patch(p: PatchMeta) -> N.tg_patch_meta:
+    return N.tg_patch_meta(p.patch_id, p.source_frame_id, _c_rect(p.rect), p.generation_time_us,
+                           p.slo_us, p.deadline_us, p.size_bytes)
+
+
+def _py_patch(p: N.tg_patch_meta) -> PatchMeta:
+    return PatchMeta(p.patch_id, p.source_frame_id, _py_rect(p.rect), p.generation_time_us,
+                     p.slo_us, p.deadline_us, p.size_bytes)
+
+
+# ---------------------------------------------------------------- context
+class Context:
+    """One CUDA device + stream (tg_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = N.lib()
+        h = C.c_void_p()
+        check(self._lib.tg_ctx_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def close(self) -> None:
+        if self.handle:
+            self._lib.tg_ctx_destroy(self.handle)
+            self.handle = None
+
+    @property
+    def stream(self) -> int:
+        return self._lib.tg_ctx_stream(self.handle)
+
+    def synchronize(self) -> None:
+        check(self._lib.tg_ctx_synchronize(self.handle))
+
+    def sm_count(self) -> int:
+        n = C.c_int32()
+        check(self._lib.tg_device_sm_count(self.handle, C.byref(n)))
+        return n.value
+
+    # plumbing
+    def malloc(self, nbytes: int) -> int:
+        p = C.c_void_p()
+        check(self._lib.tg_malloc_device(self.handle, max(1, nbytes), C.byref(p)))
+        return p.value
+
+    def free(self, ptr: int) -> None:
+        check(self._lib.tg_free_device(self.handle, ptr))
+
+    def malloc_host(self, nbytes: int) -> int:
+        p = C.c_void_p()
+        check(self._lib.tg_malloc_host(self.handle, max(1, nbytes), C.byref(p)))
+        return p.value
+
+    def free_host(self, ptr: int) -> None:
+        check(self._lib.tg_free_host(self.handle, ptr))
+
+    def memcpy(self, dst: int, src: int, nbytes: int, kind: int, stream=None) -> None:
+        check(self._lib.tg_memcpy_async(self.handle, dst, src, nbytes, kind, stream))
+
+    def upload(self, dptr: int, arr: np.ndarray, stream=None) -> None:
+        arr = np.ascontiguousarray(arr)
+        self.memcpy(dptr, arr.ctypes.data, arr.nbytes, 0, stream)
+        self.stream_sync(stream)
+
+    def download(self, dptr: int, shape, dtype, stream=None) -> np.ndarray:
+        out = np.empty(shape, dtype=dtype)
+        self.memcpy(out.ctypes.data, dptr, out.nbytes, 1, stream)
+        self.stream_sync(stream)
+        return out
+
+    def memset(self, dptr: int, value: int, nbytes: int, stream=None) -> None:
+        check(self._lib.tg_memset_async(self.handle, dptr, value, nbytes, stream))
+
+    def stream_sync(self, stream=None) -> None:
+        check(self._lib.tg_stream_synchronize(self.handle, stream))
+
+    def new_stream(self) -> int:
+        s = C.c_void_p()
+        check(self._lib.tg_stream_create(self.handle, C.byref(s)))
+        return s.value
+
+    def event(self) -> int:
+        e = C.c_void_p()
+        check(self._lib.tg_event_create(self.handle, C.byref(e)))
+        return e.value
+
+    def record(self, ev: int, stream=None) -> None:
+        check(self._lib.tg_event_record(self.handle, ev, stream))
+
+    def elapsed_ms(self, start: int, stop: int) -> float:
+        ms = C.c_float()
+        check(self._lib.tg_event_elapsed_ms(self.handle, start, stop, C.byref(ms)))
+        return ms.value
+
+
+_DEFAULT: Context | None = None
+
+
+def default_context() -> Context:
+    global _DEFAULT
+    if _DEFAULT is None:
+        _DEFAULT = Context(0)
+    return _DEFAULT
+
+
+# ------------------------------------------------------ rect-level drop-in
+def make_zones(frame: FrameSpec, cfg: PartitionConfig) -> list[Rect]:
+    """partition.hpp:69-88."""
+    n = max(1, cfg.zones_x * cfg.zones_y)
+    out = (N.tg_rect * n)()
+    fs = N.tg_frame_spec(frame.frame_id, frame.width, frame.height, frame.generation_time_us,
+                         frame.slo_us)
+    check(N.lib().tg_make_zones(C.byref(fs), N.tg_partition_config(cfg.zones_x, cfg.zones_y),
+                                out, n))
+    return [_py_rect(r) for r in out]
+
+
+def assign_rois(rois: Sequence[Rect], zones: Sequence[Rect], ctx: Context | None = None):
+    """partition.hpp:93-112: per-zone lists of RoI indices."""
+    ctx = ctx or default_context()
+    rois = [_rect(r) for r in rois]
+    n, nz = len(rois), len(zones)
+    rarr = (N.tg_rect * max(1, n))(*[_c_rect(r) for r in rois])
+    zarr = (N.tg_rect * max(1, nz))(*[_c_rect(_rect(z)) for z in zones])
+    zone_of = (C.c_int32 * max(1, n))()
+    check(N.lib().tg_assign_rois(ctx.handle, rarr, n, zarr, nz, zone_of))
+    lists = [[] for _ in range(nz)]
+    for i in range(n):
+        lists[zone_of[i]].append(i)
+    return lists
+
+
+def partition(frame: FrameSpec, cfg: PartitionConfig, rois: Iterable, bytes_per_pixel: float,
+              first_patch_id: int = 0, ctx: Context | None = None) -> list[PatchMeta]:
+    """partition.hpp:119-143, on the device."""
+    ctx = ctx or default_context()
+    rois = [_rect(r) for r in rois]
+    n = len(rois)
+    rarr = (N.tg_rect * max(1, n))(*[_c_rect(r) for r in rois])
+    cap = max(1, cfg.zones_x * cfg.zones_y)
+    out = (N.tg_patch_meta * cap)()
+    got = C.c_int32()
+    fs = N.tg_frame_spec(frame.frame_id, frame.width, frame.height, frame.generation_time_us,
+                         frame.slo_us)
+    check(N.lib().tg_partition(ctx.handle, C.byref(fs),
+                               N.tg_partition_config(cfg.zones_x, cfg.zones_y), rarr, n,
+                               float(bytes_per_pixel), first_patch_id, out, cap, C.byref(got)))
+    return [_py_patch(out[i]) for i in range(got.value)]
+
+
+def stitch_all(queue: Sequence[PatchMeta], spec: CanvasSpec,
+               ctx: Context | None = None) -> StitchResult:
+    """stitch.hpp:108-146, on the device, placements bit-identical."""
+    ctx = ctx or default_context()
+    n = len(queue)
+    q = (N.tg_patch_meta * max(1, n))(*[_c_patch(p) for p in queue])
+    pl = (N.tg_placement * max(1, n))()
+    cap = 2 * n + 1
+    fr = (N.tg_free_rect * cap)()
+    nc, nf = C.c_int32(), C.c_int32()
+    check(N.lib().tg_stitch_all(ctx.handle, q, n,
+                                N.tg_canvas_spec(spec.width, spec.height, spec.vram_per_canvas_gb),
+                                pl, C.byref(nc), fr, cap, C.byref(nf)))
+    res = StitchResult(spec=spec, canvases=[CanvasState() for _ in range(nc.value)])
+    for i in range(n):
+        p = Placement(pl[i].patch_id, pl[i].canvas_index, _py_rect(pl[i].position))
+        cs = res.canvases[p.canvas_index]
+        cs.placements.append(p)
+        cs.used_area += area(p.position)
+        res.placement_index[p.patch_id] = p
+    for i in range(nf.value):
+        res.canvases[fr[i].canvas_index].free_rects.append(_py_rect(fr[i].rect))
+    return res
+
+
+def canvas_efficiency(result: StitchResult) -> list[float]:
+    """stitch.hpp:149-157."""
+    s = float(result.spec.surface_area())
+    return [c.used_area / s for c in result.canvases]
+
+
+def dump_layout(result: StitchResult) -> str:
+    """stitch.hpp:160-176."""
+    out = []
+    eff = canvas_efficiency(result)
+    for ci, c in enumerate(result.canvases):
+        out.append(f"canvas {ci} ({result.spec.width}x{result.spec.height}) "
+                   f"efficiency={eff[ci]:.4f}\n")
+        for p in c.placements:
+            out.append(f"  patch {p.patch_id} at ({p.position.x},{p.position.y}) "
+                       f"{p.position.w}x{p.position.h}\n")
+    return "".join(out)
+
+
+def extract_canvas(result: StitchResult, canvas_index: int) -> StitchResult:
+    """stitch.hpp:179-190."""
+    if canvas_index < 0 or canvas_index >= result.canvas_count():
+        raise OutOfRange("canvas index out of range")
+    src = result.canvases[canvas_index]
+    c = CanvasState([Placement(p.patch_id, 0, p.position) for p in src.placements],
+                    list(src.free_rects), src.used_area)
+    return StitchResult(result.spec, [c], {p.patch_id: p for p in c.placements})
+
+
+def concat_stitches(parts: Sequence[StitchResult]) -> StitchResult:
+    """stitch.hpp:193-208."""
+    out = StitchResult()
+    if parts:
+        out.spec = parts[0].spec
+    for part in parts:
+        base = out.canvas_count()
+        for c in part.canvases:
+            cc = CanvasState([Placement(p.patch_id, p.canvas_index + base, p.position)
+                              for p in c.placements], list(c.free_rects), c.used_area)
+            for p in cc.placements:
+                out.placement_index[p.patch_id] = p
+            out.canvases.append(cc)
+    return out
+
+
+# --------------------------------------------------------- synthetic input
+def derive_seed(master: int, component: str) -> int:
+    return N.lib().tg_derive_seed(master, component.encode())
+
+
+def generate_trace(n_frames=150, fps=15.0, frame_width=1920, frame_height=1080,
+                   roi_proportion_mean=0.10, roi_proportion_jitter=0.5, burst_probability=0.05,
+                   burst_multiplier=3.0, roi_count_min=2, roi_count_max=12, roi_aspect_min=0.5,
+                   roi_aspect_max=2.0, roi_max_dim=480, seed=1):
+    """trace.hpp:184-231.  Returns (t_us list, per-frame lists of Rect)."""
+    cfg = N.tg_workload_config(n_frames, fps, frame_width, frame_height, roi_proportion_mean,
+                               roi_proportion_jitter, burst_probability, burst_multiplier,
+                               roi_count_min, roi_count_max, roi_aspect_min, roi_aspect_max,
+                               roi_max_dim, seed)
+    n = max(1, n_frames)
+    cap = max(1, n_frames * max(1, roi_count_max))
+    t = (C.c_int64 * n)()
+    cnt = (C.c_int32 * n)()
+    rois = (N.tg_rect * cap)()
+    tot = C.c_int64()
+    check(N.lib().tg_generate_trace(C.byref(cfg), t, cnt, rois, cap, C.byref(tot)))
+    frames, k = [], 0
+    for i in range(n_frames):
+        frames.append([_py_rect(rois[k + j]) for j in range(cnt[i])])
+        k += cnt[i]
+    return [t[i] for i in range(n_frames)], frames
+
+
+class FrameRing:
+    """Device-resident frames of one camera: slot 0 is the background-only
+    frame (t = -1), slot i+1 is frame i.  Frame i's predecessor is slot i."""
+
+    def __init__(self, ctx: Context, width: int, height: int, n_frames: int, pitch=None):
+        self.ctx, self.W, self.H, self.n = ctx, width, height, n_frames
+        self.pitch = pitch or 3 * width
+        self.frame_bytes = self.pitch * height
+        self.base = ctx.malloc(self.frame_bytes * (n_frames + 1))
+        self.slots = [self.base + i * self.frame_bytes for i in range(n_frames + 1)]
+        self._tables = []
+
+    def close(self):
+        for t in self._tables:
+            self.ctx.free(t)
+        self._tables = []
+        if self.base:
+            self.ctx.free(self.base)
+            self.base = None
+
+    def synthesize(self, pixel_seed: int, rects_per_frame: Sequence[Sequence[Rect]]):
+        """Writes the background frame and frames 0..n-1 on the device."""
+        lib, ctx = N.lib(), self.ctx
+        flat = [r for fr in rects_per_frame for r in fr]
+        offs = np.zeros(self.n + 2, np.int32)
+        offs[2:] = np.cumsum([len(fr) for fr in rects_per_frame])
+        d_rects = ctx.malloc(16 * max(1, len(flat)))
+        d_offs = ctx.malloc(4 * len(offs))
+        d_ptrs = ctx.malloc(8 * (self.n + 1))
+        if flat:
+            ctx.upload(d_rects, np.array([(r.x, r.y, r.w, r.h) for r in flat], np.int32))
+        ctx.upload(d_offs, offs)
+        ctx.upload(d_ptrs, np.array(self.slots, np.uint64))
+        # background (t=-1) uses offsets[0..1] = empty
+        check(lib.tg_synth_frames(ctx.handle, self.W, self.H, self.pitch, pixel_seed, 1, -1,
+                                  d_rects, d_offs, d_ptrs, None))
+        check(lib.tg_synth_frames(ctx.handle, self.W, self.H, self.pitch, pixel_seed, self.n, 0,
+                                  d_rects, d_offs + 4, d_ptrs + 8, None))
+        ctx.stream_sync()
+        for p in (d_rects, d_offs, d_ptrs):
+            ctx.free(p)
+
+    def upload_frame(self, slot: int, arr: np.ndarray):
+        assert arr.nbytes == self.frame_bytes
+        self.ctx.upload(self.slots[slot], arr)
+
+    def download_frame(self, slot: int) -> np.ndarray:
+        return self.ctx.download(self.slots[slot], (self.H, self.pitch), np.uint8)
+
+    def tables(self, first: int = 0, count: int | None = None):
+        """Device pointer tables (cur, prev) for frames first..first+count-1."""
+        count = self.n - first if count is None else count
+        cur = np.array(self.slots[first + 1:first + 1 + count], np.uint64)
+        prev = np.array(self.slots[first:first + count], np.uint64)
+        d_cur, d_prev = self.ctx.malloc(8 * count), self.ctx.malloc(8 * count)
+        self.ctx.upload(d_cur, cur)
+        self.ctx.upload(d_prev, prev)
+        self._tables += [d_cur, d_prev]
+        return d_cur, d_prev
+
+
+class Pipeline:
+    """frames -> masks -> cells -> RoIs -> patches -> placements -> canvases."""
+
+    def __init__(self, ctx: Context, width: int, height: int, **overrides):
+        self.ctx = ctx
+        lib = N.lib()
+        p = N.tg_pipeline_params()
+        check(lib.tg_pipeline_params_default(width, height, C.byref(p)))
+        for k, v in overrides.items():
+            if k == "zones":
+                p.partition = N.tg_partition_config(*v)
+            elif k == "canvas":
+                p.canvas = N.tg_canvas_spec(v[0], v[1], 1.0)
+            else:
+                setattr(p, k, v)
+        self.params = p
+        h = C.c_void_p()
+        check(lib.tg_pipeline_create(ctx.handle, C.byref(p), C.byref(h)))
+        self.handle = h
+        v = N.tg_pipeline_views()
+        check(lib.tg_pipeline_device_views(h, C.byref(v)))
+        self.views = v
+        self.zones = v.zones
+
+    def close(self):
+        if self.handle:
+            N.lib().tg_pipeline_destroy(self.handle)
+            self.handle = None
+
+    @property
+    def canvas_bytes(self) -> int:
+        return self.params.canvas.width * self.params.canvas.height * 3
+
+    def run(self, n_frames, d_cur, d_prev, d_frame_ids, d_gen_us, first_patch_id, d_canvases,
+            stream=None):
+        check(N.lib().tg_pipeline_run(self.handle, n_frames, d_cur, d_prev, d_frame_ids, d_gen_us,
+                                      first_patch_id, d_canvases, stream))
+
+    def graph(self, n_frames, d_cur, d_prev, d_frame_ids, d_gen_us, first_patch_id, d_canvases,
+              stream=None) -> "Graph":
+        g = C.c_void_p()
+        check(N.lib().tg_pipeline_graph_create(self.handle, n_frames, d_cur, d_prev, d_frame_ids,
+                                               d_gen_us, first_patch_id, d_canvases, stream,
+                                               C.byref(g)))
+        return Graph(g)
+
+    def results(self, n_frames: int, stream=None) -> dict:
+        """Blocking download of the last run's per-frame results."""
+        F, Z, R = n_frames, self.zones, self.params.max_rois_per_frame
+        out = dict(
+            n_rois=np.zeros(F, np.int32), rois=np.zeros((F, R, 4), np.int32),
+            n_patches=np.zeros(F, np.int32), patches=(N.tg_patch_meta * max(1, F * Z))(),
+            admitted=np.zeros((F, Z), np.uint8), n_placements=np.zeros(F, np.int32),
+            placements=(N.tg_placement * max(1, F * Z))(), n_canvases=np.zeros(F, np.int32))
+        total = C.c_int64()
+        check(N.lib().tg_pipeline_download(
+            self.handle, F, stream, out["n_rois"].ctypes.data, out["rois"].ctypes.data,
+            out["n_patches"].ctypes.data, C.cast(out["patches"], C.c_void_p),
+            out["admitted"].ctypes.data, out["n_placements"].ctypes.data,
+            C.cast(out["placements"], C.c_void_p), out["n_canvases"].ctypes.data, C.byref(total)))
+        out["total_canvases"] = total.value
+        out["patch_list"] = [[_py_patch(out["patches"][f * Z + j]) for j in range(out["n_patches"][f])]
+                             for f in range(F)]
+        out["placement_list"] = [
+            [(pl.patch_id, pl.canvas_index, pl.position.x, pl.position.y, pl.position.w,
+              pl.position.h) for pl in (out["placements"][f * Z + k]
+                                        for k in range(out["n_placements"][f]))]
+            for f in range(F)]
+        return out
+
+    def free_rects(self, frame: int):
+        cap = 3 * self.zones + 4
+        arr = (N.tg_free_rect * cap)()
+        n = C.c_int32()
+        check(N.lib().tg_pipeline_free_rects(self.handle, frame, arr, cap, C.byref(n)))
+        return [(arr[i].canvas_index, arr[i].rect.x, arr[i].rect.y, arr[i].rect.w, arr[i].rect.h)
+                for i in range(n.value)]
+
+    def cells(self, n_frames: int) -> np.ndarray:
+        v = self.views
+        return self.ctx.download(v.cells, (n_frames, v.cells_y, v.cells_x), np.uint32)
+
+    def mask(self, n_frames: int) -> np.ndarray:
+        v = self.views
+        if not v.mask:
+            raise TangramError("pipeline was created without keep_mask")
+        return self.ctx.download(v.mask, (n_frames, self.params.height, v.mask_words), np.uint32)
+
+
+class Graph:
+    def __init__(self, handle):
+        self.handle = handle
+
+    def launch(self, stream=None):
+        check(N.lib().tg_graph_launch(self.handle, stream))
+
+    def close(self):
+        if self.handle:
+            N.lib().tg_graph_destroy(self.handle)
+            self.handle = None

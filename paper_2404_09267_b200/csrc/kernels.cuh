@@ -1,0 +1,109 @@
+// kernels.cuh -- launch descriptors shared by the kernels and the C ABI.
+#pragma once
+
+#include "common.cuh"
+
+namespace tg {
+
+// ---- K1 (k_mask.cu) --------------------------------------------------------
+cudaError_t launch_mask_cells(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
+                              int n_frames, int W, int H, int pitch, int threshold, int radius,
+                              uint32_t* d_cells, uint32_t* d_active, uint32_t* d_mask, int sms,
+                              cudaStream_t stream);
+
+// ---- K2-K4 per-frame planner + scan (k_plan.cu) ----------------------------
+struct PlanArgs {
+  int n_frames, W, H, X, Y, M, N;
+  int cells_x, cells_y, act_words, max_rois, job_cap;
+  double bpp;
+  int64_t slo_us;
+  const uint32_t* cells;
+  const uint32_t* active;
+  const uint64_t* frame_ids;
+  const int64_t* gen_us;
+  int32_t* n_rois;
+  tg_rect* rois;
+  int32_t* n_patches;
+  tg_patch_meta* patches;
+  uint8_t* admitted;
+  int32_t* n_placements;
+  tg_placement* placements;
+  int32_t* n_canvases;
+  Job* jobs;
+  uint32_t* canvas_jobs;  // [F][Z] start | count << 16
+  DevError* err;
+};
+
+struct ScanArgs {
+  int n_frames, zones;
+  uint64_t first_id;
+  int64_t max_canvases;
+  int nbands;
+  const int32_t* n_patches;
+  const int32_t* n_placements;
+  const int32_t* n_canvases;
+  tg_patch_meta* patches;
+  tg_placement* placements;
+  int64_t* canvas_base;
+  uint32_t* canvas_map;   // [max_canvases] frame << 6 | local canvas
+  int32_t* gather_units;  // out: min(total, cap) * nbands
+  uint64_t* id_state;     // next patch id after this run; read when first_id == ~0
+  DevError* err;
+};
+
+struct PartitionBatchArgs {
+  int n_frames, X, Y;
+  double bpp;
+  const tg_frame_spec* frames;
+  const int32_t* roi_offsets;  // [n+1]
+  const tg_rect* rois;
+  const uint64_t* first_ids;   // [n]
+  tg_patch_meta* patches;      // [n * X*Y]
+  int32_t* n_patches;
+  int32_t* zone_of;            // optional [total rois]
+  DevError* err;
+};
+
+struct StitchBatchArgs {
+  int n_queues, M, N;
+  const int32_t* offsets;
+  const tg_patch_meta* queue;
+  tg_placement* placements;
+  int32_t* n_canvases;
+  FreeRect* free_ws;   // [2*total + n_queues]
+  int32_t* n_free;     // optional [n_queues]
+  int32_t* dims_ws;    // [5*total] scratch: w, h, StitchOut{canvas, x, y}
+  uint64_t* ids_ws;    // [total] scratch patch ids
+  DevError* err;
+};
+
+size_t plan_smem_bytes(int cells_x, int cells_y, int max_rois);
+cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
+cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream);
+cudaError_t launch_partition_batch(const PartitionBatchArgs& a, cudaStream_t stream);
+cudaError_t launch_stitch_batch(const StitchBatchArgs& a, cudaStream_t stream);
+
+// ---- K5 (k_gather.cu) -------------------------------------------------------
+struct GatherArgs {
+  const uint8_t* const* frames;
+  int pitch, M, N, zones, job_cap, nbands;
+  const Job* jobs;
+  const uint32_t* canvas_jobs;
+  const uint32_t* canvas_map;
+  const int32_t* units;
+  uint8_t* out;
+};
+cudaError_t launch_gather(const GatherArgs& a, int sms, cudaStream_t stream);
+int gather_bands(int N);
+
+// ---- synthetic frames (k_synth.cu) -----------------------------------------
+struct SynthArgs {
+  int W, H, pitch, t0;
+  uint64_t seed;
+  const tg_rect* rects;
+  const int32_t* offsets;
+  uint8_t* const* frames;
+};
+cudaError_t launch_synth(const SynthArgs& a, int n_frames, cudaStream_t stream);
+
+}  // namespace tg

@@ -1,0 +1,213 @@
+// rect_core.cuh -- device restatement of the reference's rect-level core:
+// Alg. 1 partition (partition.hpp:69-143) and Alg. 2's patch-stitching
+// solver (stitch.hpp:66-146), shared by the fused per-frame planner and the
+// drop-in / batched entry points.
+#pragma once
+
+#include <climits>
+
+#include "common.cuh"
+
+namespace tg {
+
+// make_zones (partition.hpp:69-88): row-major from the bottom-left, the last
+// column/row absorbs the remainder.
+__device__ __forceinline__ tg_rect zone_rect(int z, int W, int H, int X, int Y) {
+  const int zw = W / X, zh = H / Y;
+  const int row = z / X, col = z - row * X;
+  tg_rect r;
+  r.x = col * zw;
+  r.y = row * zh;
+  r.w = (col == X - 1) ? W - r.x : zw;
+  r.h = (row == Y - 1) ? H - r.y : zh;
+  return r;
+}
+
+// overlap_area (geometry.hpp:44-49), int64.
+__device__ __forceinline__ long long overlap_area(const tg_rect& a, const tg_rect& b) {
+  const int ow = min(a.x + a.w, b.x + b.w) - max(a.x, b.x);
+  const int oh = min(a.y + a.h, b.y + b.h) - max(a.y, b.y);
+  if (ow <= 0 || oh <= 0) return 0;
+  return static_cast<long long>(ow) * static_cast<long long>(oh);
+}
+
+// assign_rois (partition.hpp:93-112): zone of maximum overlap, strict '>'
+// so ties keep the lowest zone index; -1 if the RoI misses the frame.
+__device__ __forceinline__ int best_zone(const tg_rect& r, int W, int H, int X, int Y) {
+  long long best = 0;
+  int bz = -1;
+  const int nz = X * Y;
+  for (int z = 0; z < nz; ++z) {
+    const long long s = overlap_area(r, zone_rect(z, W, H, X, Y));
+    if (s > best) {
+      best = s;
+      bz = z;
+    }
+  }
+  return bz;
+}
+
+// Per-zone enclosing-rect accumulators in shared memory.
+struct ZoneAcc {
+  int x0[kMaxZones], y0[kMaxZones], x1[kMaxZones], y1[kMaxZones], cnt[kMaxZones];
+};
+
+__device__ __forceinline__ void zone_acc_init(ZoneAcc& z, int nz, int tid, int nthreads) {
+  for (int i = tid; i < nz; i += nthreads) {
+    z.x0[i] = INT_MAX;
+    z.y0[i] = INT_MAX;
+    z.x1[i] = INT_MIN;
+    z.y1[i] = INT_MIN;
+    z.cnt[i] = 0;
+  }
+}
+
+// Block-cooperative assignment of n RoIs into the zone accumulators.
+// Returns nothing; an RoI outside the frame latches kErrRoiOutside.
+__device__ __forceinline__ void partition_accumulate(const tg_rect* rois, int n, int W, int H,
+                                                     int X, int Y, ZoneAcc& z, DevError* err,
+                                                     int frame, int* zone_of, int tid,
+                                                     int nthreads) {
+  for (int i = tid; i < n; i += nthreads) {
+    const tg_rect r = rois[i];
+    const int bz = best_zone(r, W, H, X, Y);
+    if (zone_of) zone_of[i] = bz;
+    if (bz < 0) {
+      // With zone_of the caller reports the FIRST bad index itself (the
+      // reference throws at the lowest one, partition.hpp:106-108).
+      if (!zone_of) raise_error(err, TG_ERR_INVALID_ARGUMENT, kErrRoiOutside, i, frame);
+      continue;
+    }
+    atomicMin(&z.x0[bz], r.x);
+    atomicMin(&z.y0[bz], r.y);
+    atomicMax(&z.x1[bz], r.x + r.w);
+    atomicMax(&z.y1[bz], r.y + r.h);
+    atomicAdd(&z.cnt[bz], 1);
+  }
+}
+
+// One warp: one patch per non-empty zone in zone order (partition.hpp:
+// 125-141).  patch_id = first_id + rank; returns the patch count.
+__device__ __forceinline__ int partition_emit(const ZoneAcc& z, int nz, uint64_t frame_id,
+                                              int64_t gen_us, int64_t slo_us, double bpp,
+                                              uint64_t first_id, tg_patch_meta* out, int lane) {
+  int base = 0;
+  for (int zb = 0; zb < nz; zb += 32) {
+    const int zi = zb + lane;
+    const bool ne = zi < nz && z.cnt[zi] > 0;
+    const unsigned m = __ballot_sync(0xffffffffu, ne);
+    if (ne) {
+      const int rank = base + __popc(m & ((1u << lane) - 1u));
+      tg_patch_meta p;
+      p.patch_id = first_id + static_cast<uint64_t>(rank);
+      p.source_frame_id = frame_id;
+      p.rect.x = z.x0[zi];
+      p.rect.y = z.y0[zi];
+      p.rect.w = z.x1[zi] - z.x0[zi];
+      p.rect.h = z.y1[zi] - z.y0[zi];
+      p.generation_time_us = gen_us;
+      p.slo_us = slo_us;
+      p.deadline_us = gen_us + slo_us;
+      p.size_bytes = static_cast<int64_t>(
+          ceil(static_cast<double>(static_cast<long long>(p.rect.w) * p.rect.h) * bpp));
+      out[rank] = p;
+    }
+    base += __popc(m);
+  }
+  return base;
+}
+
+// ---- Alg. 2 patch-stitching solver, one warp ------------------------------
+// Best-short-side fit over every live free rect of every open canvas;
+// ties by lower canvas, then lower y, then lower x (candidate_better,
+// stitch.hpp:72-81) -- a total order because a canvas's free rects are
+// disjoint, so one 64-bit key min finds the reference's choice.  The free
+// set is kept unordered (swap-remove); each rect carries its insertion seq
+// so the reference's list order can be rebuilt.  Guillotine split per
+// stitch.hpp:86-99.  Returns the canvas count, or -1 after latching an
+// error (oversize patch / free capacity).
+struct StitchOut {
+  int canvas;
+  int x, y;
+};
+
+__device__ __forceinline__ int bssf_stitch(const int* pw, const int* ph, const uint64_t* pid,
+                                           int n, int M, int N, FreeRect* fl, int cap,
+                                           StitchOut* out, int* n_free_out, DevError* err,
+                                           int queue, int lane) {
+  int nfree = 0, nc = 0, seq = 0;
+  for (int i = 0; i < n; ++i) {
+    const int w = pw[i], h = ph[i];
+    if (w > M || h > N) {
+      if (lane == 0)
+        raise_error(err, TG_ERR_INVALID_ARGUMENT, kErrPatchOversize,
+                    static_cast<long long>(pid ? pid[i] : static_cast<uint64_t>(i)), w, h, queue);
+      return -1;
+    }
+    unsigned long long best = ~0ull;
+    int bi = -1;
+    for (int k = lane; k < nfree; k += 32) {
+      const FreeRect c = fl[k];
+      if (c.w < w || c.h < h) continue;
+      const unsigned s = static_cast<unsigned>(min(c.w - w, c.h - h));
+      const unsigned long long key = (static_cast<unsigned long long>(s) << 48) |
+                                     (static_cast<unsigned long long>(c.canvas) << 32) |
+                                     (static_cast<unsigned long long>(c.y) << 16) |
+                                     static_cast<unsigned long long>(c.x);
+      if (key < best) {
+        best = key;
+        bi = k;
+      }
+    }
+    const unsigned long long gmin = warp_min_u64(best);
+    FreeRect chosen;
+    if (gmin == ~0ull) {  // nothing fits: open a blank canvas (stitch.hpp:129-135)
+      chosen = FreeRect{0, 0, M, N, nc, -1};
+      ++nc;
+    } else {
+      const unsigned owner = __ballot_sync(0xffffffffu, best == gmin && bi >= 0);
+      const int src = __ffs(owner) - 1;
+      bi = __shfl_sync(0xffffffffu, bi, src);
+      chosen = fl[bi];
+    }
+    __syncwarp();
+    const int lw = chosen.w - w, lh = chosen.h - h;
+    FreeRect a, b;
+    if (lw <= lh) {
+      a = FreeRect{chosen.x + w, chosen.y, lw, chosen.h, chosen.canvas, 0};
+      b = FreeRect{chosen.x, chosen.y + h, w, lh, chosen.canvas, 0};
+    } else {
+      a = FreeRect{chosen.x + w, chosen.y, lw, h, chosen.canvas, 0};
+      b = FreeRect{chosen.x, chosen.y + h, chosen.w, lh, chosen.canvas, 0};
+    }
+    const bool keep_a = a.w > 0 && a.h > 0, keep_b = b.w > 0 && b.h > 0;
+    int nf = nfree;
+    if (gmin != ~0ull) --nf;  // swap-remove the chosen rect
+    const int need = nf + (keep_a ? 1 : 0) + (keep_b ? 1 : 0);
+    if (need > cap) {
+      if (lane == 0) raise_error(err, TG_ERR_CAPACITY, kErrFreeCapacity, queue, cap);
+      return -1;
+    }
+    if (lane == 0) {
+      if (gmin != ~0ull) fl[bi] = fl[nfree - 1];
+      if (keep_a) {
+        a.seq = seq++;
+        fl[nf++] = a;
+      }
+      if (keep_b) {
+        b.seq = seq++;
+        fl[nf++] = b;
+      }
+      out[i] = StitchOut{chosen.canvas, chosen.x, chosen.y};
+    } else {
+      seq += (keep_a ? 1 : 0) + (keep_b ? 1 : 0);
+      nf += (keep_a ? 1 : 0) + (keep_b ? 1 : 0);
+    }
+    nfree = nf;
+    __syncwarp();
+  }
+  if (n_free_out) *n_free_out = nfree;
+  return nc;
+}
+
+}  // namespace tg

@@ -1,0 +1,399 @@
+"""Parity of the B200 kernels with the oracle -- the gate for every claim.
+
+Bit-exact everywhere (integer/byte work): masks, cell grids, RoI lists,
+patch lists, admission, placements, free-rect lists (in the reference's list
+order) and every canvas byte.  Rect-level outputs are additionally checked
+against golden vectors produced by the reference itself.
+"""
+import hashlib
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2404_09267_b200 import api as A
+from tests._helpers import GpuRun, oracle_patch_tuples, oracle_params, patch_tuples
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def tup(x):
+    return [tuple(v) if isinstance(v, list) else v for v in x]
+
+
+# ============================================================ drop-in API
+def test_partition_dropin_golden(ctx, golden):
+    for k in golden["rect"]["partition_kats"]:
+        fid, w, h, gen, slo = k["frame"]
+        got = A.partition(A.FrameSpec(fid, w, h, gen, slo), A.PartitionConfig(*k["grid"]),
+                          [tuple(r) for r in k["rois"]], k["bpp"], k["first"], ctx=ctx)
+        want = [(p["patch_id"], p["source_frame_id"], *p["rect"], p["generation_time_us"],
+                 p["slo_us"], p["deadline_us"], p["size_bytes"]) for p in k["patches"]]
+        assert patch_tuples([got])[0] == want
+
+
+def test_partition_dropin_errors(ctx, golden):
+    errs = golden["rect"]["partition_errors"]
+    with pytest.raises(A.InvalidArgument) as e:
+        A.partition(A.FrameSpec(0, 100, 100, 0, 1), A.PartitionConfig(2, 2),
+                    [(10, 10, 5, 5), (200, 200, 10, 10), (300, 300, 1, 1)], 1.5, ctx=ctx)
+    assert str(e.value) == errs["outside"].replace("index 0", "index 1")
+    with pytest.raises(A.InvalidArgument) as e:
+        A.partition(A.FrameSpec(0, 3, 3, 0, 1), A.PartitionConfig(4, 4), [], 1.5, ctx=ctx)
+    assert str(e.value) == errs["finer"]
+    # the context is usable after an error
+    assert len(A.partition(A.FrameSpec(0, 100, 100, 0, 1), A.PartitionConfig(2, 2),
+                           [(1, 1, 3, 3)], 1.5, ctx=ctx)) == 1
+
+
+def test_assign_rois_dropin(ctx):
+    zones = A.make_zones(A.FrameSpec(0, 100, 100, 0, 1), A.PartitionConfig(2, 2))
+    assert A.assign_rois([(30, 10, 30, 20)], zones, ctx=ctx)[0] == [0]
+    assert A.assign_rois([(40, 10, 20, 10)], zones, ctx=ctx)[0] == [0]     # tie -> lowest zone
+    assert A.assign_rois([(40, 40, 20, 20)], zones, ctx=ctx)[0] == [0]
+    with pytest.raises(A.InvalidArgument, match=r"roi outside frame \(roi index 0\)"):
+        A.assign_rois([(200, 200, 10, 10)], zones, ctx=ctx)
+
+
+def test_partition_dropin_random_vs_reference_port(ctx):
+    rng = O.Rng(O.derive_seed(5, "partition-gpu"))
+    for it in range(300):
+        W, H = rng.uniform_int(8, 4000), rng.uniform_int(8, 2200)
+        zx, zy = rng.uniform_int(1, min(8, W)), rng.uniform_int(1, min(8, H))
+        n = rng.uniform_int(0, 40)
+        rois = []
+        for _ in range(n):
+            w, h = rng.uniform_int(1, W), rng.uniform_int(1, H)
+            rois.append((rng.uniform_int(0, W - w), rng.uniform_int(0, H - h), w, h))
+        bpp = [1.5, 1.0, 0.37, 3.0][it % 4]
+        got = A.partition(A.FrameSpec(it, W, H, 1000 * it, 5000), A.PartitionConfig(zx, zy), rois,
+                          bpp, 17 * it, ctx=ctx)
+        want = O.partition(it, W, H, 1000 * it, 5000, zx, zy, rois, bpp, 17 * it)
+        assert patch_tuples([got])[0] == oracle_patch_tuples([want])[0]
+
+
+def _stitch_tuples(res):
+    pl = sorted([(p.patch_id, p.canvas_index, p.position.x, p.position.y, p.position.w,
+                  p.position.h) for c in res.canvases for p in c.placements])
+    fr = [(ci, r.x, r.y, r.w, r.h) for ci, c in enumerate(res.canvases) for r in c.free_rects]
+    return pl, res.canvas_count(), fr
+
+
+def test_stitch_dropin_golden(ctx, golden):
+    for k in golden["rect"]["stitch_kats"] + [dict(s, canvas=(1024, 1024))
+                                             for s in golden["rect"]["c01_sets"]]:
+        q = [A.PatchMeta(pid, 0, A.Rect(0, 0, w, h)) for pid, w, h in k["queue"]]
+        res = A.stitch_all(q, A.CanvasSpec(*k["canvas"]), ctx=ctx)
+        pl, nc, fr = _stitch_tuples(res)
+        assert pl == sorted(tup(k["placements"]))
+        assert nc == k["n_canvases"]
+        assert fr == tup(k["free"])  # reference list order, canvas by canvas
+    with pytest.raises(A.InvalidArgument) as e:
+        A.stitch_all([A.PatchMeta(0, 0, A.Rect(0, 0, 101, 10))], A.CanvasSpec(100, 100), ctx=ctx)
+    assert str(e.value) == golden["rect"]["stitch_error"]
+    assert A.stitch_all([], A.CanvasSpec(100, 100), ctx=ctx).empty()
+
+
+def test_stitch_dropin_kat_values(ctx):
+    # stitch_test.cpp:42-104
+    q = [A.PatchMeta(i, 0, A.Rect(0, 0, w, h)) for i, (w, h) in enumerate([(60, 60), (40, 40)])]
+    r = A.stitch_all(q, A.CanvasSpec(100, 100), ctx=ctx)
+    assert r.canvas_count() == 1 and r.placement_index[1].position == A.Rect(60, 0, 40, 40)
+    q = [A.PatchMeta(i, 0, A.Rect(0, 0, w, h)) for i, (w, h) in enumerate([(60, 60), (50, 50)])]
+    r = A.stitch_all(q, A.CanvasSpec(100, 100), ctx=ctx)
+    assert r.canvases[0].free_rects == [A.Rect(60, 0, 40, 100), A.Rect(0, 60, 60, 40)]
+    assert A.canvas_efficiency(r) == [0.36, 0.25]
+
+
+def test_stitch_batch_c01_acceptance(ctx):
+    """Acceptance C01 (acceptance_test.cpp:48-101): all 10,000 seeded sets,
+    stitched in one batched launch (one warp per queue), every placement and
+    free list equal to the oracle's."""
+    from paper_2404_09267_b200 import _native as N
+    rng = O.Rng(O.derive_seed(2026, "packing"))
+    queues = []
+    for _ in range(10_000):
+        n = rng.uniform_int(1, 24)
+        queues.append([(i, rng.uniform_int(16, 1024), rng.uniform_int(16, 1024)) for i in range(n)])
+    offs = np.zeros(len(queues) + 1, np.int32)
+    offs[1:] = np.cumsum([len(q) for q in queues])
+    total = int(offs[-1])
+    # tg_patch_meta as 8 int64 words: id, frame, (x|y<<32), (w|h<<32), gen, slo, ddl, bytes
+    meta = np.zeros((total, 8), np.int64)
+    k = 0
+    for q in queues:
+        for pid, w, h in q:
+            meta[k, 0] = pid
+            meta[k, 3] = h << 32 | w
+            k += 1
+    d_off, d_q = ctx.malloc(offs.nbytes), ctx.malloc(meta.nbytes)
+    d_pl, d_nc = ctx.malloc(32 * total), ctx.malloc(4 * len(queues))
+    d_fr, d_nf = ctx.malloc(24 * (2 * total + len(queues))), ctx.malloc(4 * len(queues))
+    ctx.upload(d_off, offs)
+    ctx.upload(d_q, meta)
+    A.check(N.lib().tg_stitch_batch(ctx.handle, len(queues), total, d_off, d_q,
+                                    N.tg_canvas_spec(1024, 1024, 1.0), d_pl, d_nc, d_fr, d_nf, None))
+    ctx.stream_sync()
+    pl = ctx.download(d_pl, (total, 8), np.int32)
+    nc = ctx.download(d_nc, (len(queues),), np.int32)
+    nf = ctx.download(d_nf, (len(queues),), np.int32)
+    fr = ctx.download(d_fr, (2 * total + len(queues), 6), np.int32)
+    for qi, q in enumerate(queues):
+        want_pl, want_nc, want_fr = O.stitch_all(q, 1024, 1024)
+        o = offs[qi]
+        got_pl = [(int(pl[o + i, 0]), int(pl[o + i, 2]), int(pl[o + i, 3]), int(pl[o + i, 4]),
+                   int(pl[o + i, 5]), int(pl[o + i, 6])) for i in range(len(q))]
+        assert got_pl == want_pl, qi
+        assert nc[qi] == want_nc
+        base = 2 * o + qi
+        f = fr[base:base + nf[qi]]
+        got_fr = [(int(c), int(x), int(y), int(w), int(h))
+                  for x, y, w, h, c, s in sorted(f.tolist(), key=lambda r: (r[4], r[5]))]
+        assert got_fr == want_fr, qi
+    for p in (d_off, d_q, d_pl, d_nc, d_fr, d_nf):
+        ctx.free(p)
+
+
+# ========================================================== pixel pipeline
+def test_synth_matches_oracle(ctx):
+    for (W, H, n, seed) in [(96, 64, 3, 5), (1920, 1080, 2, 1000), (208, 100, 2, 11)]:
+        run = GpuRun(ctx, W, H, n, seed=seed, trace_kw=dict(roi_max_dim=min(480, W, H)))
+        frames = run.host_frames()
+        ps = O.derive_seed(seed, "pixels")
+        assert sha(frames[0]) == sha(O.synth_frame(W, H, ps, -1, []))
+        for i in range(n):
+            rects = [(r.x, r.y, r.w, r.h) for r in run.rects[i]]
+            assert sha(frames[i + 1]) == sha(O.synth_frame(W, H, ps, i, rects)), (W, H, i)
+        run.close()
+
+
+def _compare_full(run, gpu, orc, check_canvases=True):
+    n = run.n
+    # masks + cells
+    gm = run.pipe.mask(n)
+    frames = run.host_frames()
+    for i in range(n):
+        om = O.mask(frames[i + 1], frames[i], run.W, run.H, run.threshold, run.radius)
+        assert np.array_equal(gm[i], om), f"mask frame {i}"
+    assert np.array_equal(run.pipe.cells(n), orc["cells"]), "cells"
+    # RoIs in raster order of their first cell
+    assert np.array_equal(gpu["n_rois"], orc["n_rois"])
+    for i in range(n):
+        assert np.array_equal(gpu["rois"][i, :gpu["n_rois"][i]], orc["rois"][i, :orc["n_rois"][i]]), i
+    # patches, admission, placements
+    assert patch_tuples(gpu["patch_list"]) == oracle_patch_tuples(orc["patch_list"])
+    assert np.array_equal(gpu["admitted"][:, :], orc["admitted"])
+    assert gpu["placement_list"] == orc["placement_list"]
+    assert np.array_equal(gpu["n_canvases"], orc["n_canvases"])
+    assert gpu["total_canvases"] == orc["total_canvases"]
+    # free rects in reference list order
+    zn = run.zones[0] * run.zones[1]
+    for i in range(n):
+        adm = [p for j, p in enumerate(orc["patch_list"][i]) if orc["admitted"][i, j]]
+        if not adm:
+            assert run.pipe.free_rects(i) == []
+            continue
+        _, _, want = O.stitch_all([(p["patch_id"], p["rect"][2], p["rect"][3]) for p in adm],
+                                  *run.canvas)
+        assert run.pipe.free_rects(i) == want, i
+    assert zn > 0
+    if check_canvases:
+        got = run.canvases()
+        want = orc["canvases"][:orc["total_canvases"]]
+        assert got.shape == want.shape
+        for k in range(got.shape[0]):
+            assert np.array_equal(got[k], want[k]), f"canvas {k}"
+
+
+def test_pipeline_cfg1_bit_exact(ctx):
+    """BASELINE config 1: one 1920x1080 camera, 30 frames, 4x4 grid, 1024^2
+    canvases -- every intermediate and every canvas byte."""
+    run = GpuRun(ctx, 1920, 1080, 30, seed=1000)
+    gpu = run.run()
+    orc = run.oracle()
+    _compare_full(run, gpu, orc)
+    assert gpu["total_canvases"] > 0
+    run.close()
+
+
+def test_pipeline_cfg1_reference_rect_stages(ctx):
+    """Same run, with the rect stages of the oracle path executed by the
+    reference's own partition()/stitch_all() (oracle/_ref)."""
+    if not O.have_ref():
+        pytest.skip("oracle/_ref absent")
+    run = GpuRun(ctx, 1920, 1080, 12, seed=1001)
+    gpu = run.run()
+    orc = run.oracle(lib="ref")
+    assert patch_tuples(gpu["patch_list"]) == oracle_patch_tuples(orc["patch_list"])
+    assert gpu["placement_list"] == orc["placement_list"]
+    assert np.array_equal(run.canvases(), orc["canvases"][:orc["total_canvases"]])
+    run.close()
+
+
+def test_pipeline_cfg2_4k_bit_exact(ctx):
+    """BASELINE config 2 geometry (3840x2160, moderate density), first 20
+    frames, every byte."""
+    run = GpuRun(ctx, 3840, 2160, 20, seed=1000)
+    gpu = run.run()
+    orc = run.oracle()
+    _compare_full(run, gpu, orc)
+    run.close()
+
+
+@pytest.mark.slow
+def test_pipeline_cfg2_full_300_frames(ctx):
+    """All 300 frames of config 2: rect stages for every frame against the
+    oracle's partition/stitch on the GPU's own RoIs, sampled frames fully
+    against the oracle pixel path, and size-independent canvas properties
+    for every canvas (exact tiling: placed bytes non-zero, free bytes zero)."""
+    run = GpuRun(ctx, 3840, 2160, 300, seed=1000, keep_mask=False)
+    gpu = run.run()
+    first = 0
+    for i in range(300):
+        rois = [tuple(r) for r in gpu["rois"][i, :gpu["n_rois"][i]].tolist()]
+        want = O.partition(i, 3840, 2160, run.t_us[i], 1_000_000, 4, 4, rois, 1.5, first)
+        first += len(want)
+        assert patch_tuples([gpu["patch_list"][i]])[0] == oracle_patch_tuples([want])[0]
+        adm = [p for p in want if p["rect"][2] <= 1024 and p["rect"][3] <= 1024]
+        if adm:
+            pl, nc, _ = O.stitch_all([(p["patch_id"], p["rect"][2], p["rect"][3]) for p in adm],
+                                     1024, 1024)
+            assert gpu["placement_list"][i] == pl and gpu["n_canvases"][i] == nc
+    # sampled frames through the whole oracle pixel path
+    frames = {}
+    idx = list(range(0, 300, 37))
+    for i in idx:
+        frames[i] = run.ring.download_frame(i)
+        frames[i + 1] = run.ring.download_frame(i + 1)
+    params = oracle_params(3840, 2160)
+    orc = O.process_frames(params, [frames[i + 1] for i in idx], [frames[i] for i in idx], idx,
+                           [run.t_us[i] for i in idx], 0, want_cells=True)
+    cells = run.pipe.cells(300)
+    base = np.concatenate([[0], np.cumsum(gpu["n_canvases"])])
+    canv = run.canvases()
+    ob = np.concatenate([[0], np.cumsum(orc["n_canvases"])])
+    for j, i in enumerate(idx):
+        assert np.array_equal(cells[i], orc["cells"][j])
+        assert np.array_equal(gpu["rois"][i, :gpu["n_rois"][i]], orc["rois"][j, :orc["n_rois"][j]])
+        for c in range(gpu["n_canvases"][i]):
+            assert np.array_equal(canv[base[i] + c], orc["canvases"][ob[j] + c])
+    # exact tiling on every canvas: synthetic pixels are never 0, so the
+    # non-zero pattern must equal the union of placements.
+    for i in range(300):
+        for c in range(gpu["n_canvases"][i]):
+            occ = np.zeros((1024, 1024), bool)
+            for (_, ci, x, y, w, h) in gpu["placement_list"][i]:
+                if ci == c:
+                    assert not occ[y:y + h, x:x + w].any()
+                    occ[y:y + h, x:x + w] = True
+            nz = canv[base[i] + c].reshape(1024, 1024, 3).any(axis=2)
+            assert np.array_equal(nz, occ), (i, c)
+    run.close()
+
+
+def test_round_trip_fixture(ctx):
+    """Cell-aligned separated rects, static background, r=0: the GPU RoIs
+    equal the rects, so the patches equal the reference's partition() of
+    those rects and the placements its stitch_all()."""
+    rects = [[(16, 16, 64, 32), (128, 0, 48, 48), (256, 96, 160, 128), (32, 160, 16, 80),
+              (480, 208, 32, 48)]]
+    W, H = 512, 256
+    run = GpuRun(ctx, W, H, 1, seed=9, radius=0, rects=rects)
+    gpu = run.run()
+    got = sorted(tuple(r) for r in gpu["rois"][0, :gpu["n_rois"][0]].tolist())
+    assert got == sorted(rects[0])
+    lib = "ref" if O.have_ref() else "port"
+    want = O.partition(0, W, H, 0, 1_000_000, 4, 4, rects[0], 1.5, 0, lib=lib)
+    assert patch_tuples(gpu["patch_list"])[0] == oracle_patch_tuples([want])[0]
+    pl, nc, _ = O.stitch_all([(p["patch_id"], p["rect"][2], p["rect"][3]) for p in want], 1024, 1024,
+                             lib=lib)
+    assert gpu["placement_list"][0] == pl
+    run.close()
+
+
+@pytest.mark.parametrize("case", [
+    dict(W=208, H=100, n=4, radius=2),                 # W % 32 == 16, H % 16 != 0
+    dict(W=96, H=64, n=6, radius=3),
+    dict(W=640, H=360, n=5, radius=0),
+    dict(W=640, H=360, n=5, radius=8),
+    dict(W=640, H=360, n=5, threshold=0),              # every noisy byte is foreground
+    dict(W=640, H=360, n=5, threshold=200),            # the T >= 128 SWAR path
+    dict(W=1280, H=720, n=4, zones=(1, 1)),
+    dict(W=1280, H=720, n=4, zones=(8, 8)),
+    dict(W=1280, H=720, n=4, zones=(3, 5), canvas=(300, 200)),
+    dict(W=640, H=352, n=3, pitch=640 * 3 + 64),       # padded rows
+    dict(W=1920, H=1080, n=6, trace_kw=dict(roi_proportion_mean=0.59, roi_max_dim=1080,
+                                            roi_count_max=30)),  # dense, oversize patches
+])
+def test_pipeline_edge_cases(ctx, case):
+    case = dict(case)
+    W, H, n = case.pop("W"), case.pop("H"), case.pop("n")
+    tk = case.pop("trace_kw", dict(roi_max_dim=min(480, W, H)))
+    run = GpuRun(ctx, W, H, n, seed=7, trace_kw=tk, **case)
+    gpu = run.run()
+    orc = run.oracle()
+    _compare_full(run, gpu, orc)
+    run.close()
+
+
+def test_pipeline_empty_and_full_motion(ctx):
+    # no RoIs at all: no patches, no canvases
+    run = GpuRun(ctx, 640, 480, 3, rects=[[], [], []])
+    gpu = run.run()
+    # frame 0 differs from the background only by noise -> nothing
+    assert gpu["n_rois"].tolist() == [0, 0, 0] and gpu["total_canvases"] == 0
+    run.close()
+    # the whole frame moves: one giant RoI, a patch larger than the canvas
+    # is rejected (sim.hpp:262) and never stitched.
+    run = GpuRun(ctx, 1280, 1280, 2, rects=[[(0, 0, 1280, 1280)], [(0, 0, 1280, 1280)]])
+    gpu = run.run()
+    assert gpu["n_rois"].tolist() == [1, 1]
+    assert gpu["admitted"][:, 0].tolist() == [0, 0] and gpu["total_canvases"] == 0
+    _compare_full(run, gpu, run.oracle())
+    run.close()
+
+
+def test_pipeline_capacity_errors(ctx):
+    run = GpuRun(ctx, 640, 480, 4, max_rois=2, trace_kw=dict(roi_count_min=8, roi_count_max=12,
+                                                            roi_max_dim=60))
+    with pytest.raises(A.CapacityError, match="roi capacity"):
+        run.run()
+    run.close()
+    run = GpuRun(ctx, 1920, 1080, 8, max_canvases=1)
+    with pytest.raises(A.CapacityError, match="canvas capacity"):
+        run.run()
+    run.close()
+
+
+def test_pipeline_graph_replay_and_patch_id_base(ctx):
+    run = GpuRun(ctx, 1920, 1080, 8, seed=3, first_patch_id=1000)
+    gpu = run.run()
+    first = run.canvases()
+    run.ctx.memset(run.d_canvases, 0, run.canvas_bytes * run.max_canvases)
+    g = run.pipe.graph(run.n, run.d_cur, run.d_prev, run.d_ids, run.d_gen, 1000, run.d_canvases)
+    g.launch()
+    g.launch()
+    again = run.pipe.results(run.n)
+    assert again["placement_list"] == gpu["placement_list"]
+    assert np.array_equal(run.canvases(), first)
+    assert gpu["patch_list"][0][0].patch_id == 1000
+    g.close()
+    run.close()
+
+
+def test_cpp_dropin_binary():
+    """The C++ drop-in headers (include/tangram/*.hpp) compile against the
+    reference's own test expectations and run on the GPU."""
+    exe = os.path.join(ROOT, "tests", "cpp", "dropin_test")
+    subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")])
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "ALL PASS" in out.stdout
