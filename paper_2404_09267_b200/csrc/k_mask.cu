@@ -18,6 +18,7 @@
 // ballot-built activity bitmask.  HBM traffic is the frames themselves; the
 // outputs are ~0.5% of it.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_cells_kernel(const MaskArg
         }
       }
     }
-    out_next = out_hi + 1;
+    out_next = max(out_next, out_hi + 1);  // stages of pure look-behind halo output nothing
     ++g;
     cursor_next(cc, a);
   }
@@ -328,7 +329,8 @@ cudaError_t launch_mask_cells(const uint8_t* const* d_cur, const uint8_t* const*
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(mp.smem));
   if (e != cudaSuccess) return e;
-  const int grid = std::min(a.total_items, sms);
+  int grid = std::min(a.total_items, sms);
+  if (const char* g = std::getenv("TG_K1_GRID")) grid = std::max(1, std::min(a.total_items, std::atoi(g)));
   mask_cells_kernel<<<grid, kK1Threads, mp.smem, stream>>>(a);
   return cudaGetLastError();
 }

@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     }
     na += __popc(m);
   }
+  for (int j = np + lane; j < nz; j += 32) a.admitted[static_cast<size_t>(f) * nz + j] = 0;
   __syncwarp();
 
   // ---- K4: stitch plan (Alg. 2 solver) ---------------------------------
