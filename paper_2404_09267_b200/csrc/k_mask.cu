@@ -2,21 +2,26 @@
 // patch-grid occupancy (frozen spec DESIGN.md §3).
 //
 // The reference has no pixel stage (RoIs are inputs, trace.hpp:39-45); this
-// kernel produces them.  One persistent CTA per SM streams work items
-// (frame, 128-row segment) in frame-fastest order, so frame t's rows are
-// read as `cur` by item (t, s) and as `prev` by item (t+1, s) at about the
-// same time and the second read is served from L2.
+// kernel produces them.  Persistent, one CTA per SM, warp-specialized:
 //
-// Per item the rows [s0-r, s1+r) of cur and prev stream through a 4-stage
-// ring of shared-memory slots filled by cp.async.bulk (TMA bulk engine,
-// mbarrier completion).  Each thread turns 96 bytes (32 RGB pixels) into
-// one 32-bit raw-foreground word with packed SIMD byte ops, words go to a
-// 32-row smem ring, and once r rows of look-ahead exist each output row is
-// dilated (vertical OR over 2r+1 ring rows, horizontal funnel-shift OR) and
-// folded into per-cell occupancy (popc) and bbox bit-masks held in
-// registers.  A finished cell row is written as packed u32 summaries plus a
-// ballot-built activity bitmask.  HBM traffic is the frames themselves; the
-// outputs are ~0.5% of it.
+//  * 1 producer warp streams the rows of each work item -- (frame, segment of
+//    up to 128 rows) plus r halo rows -- cur and prev side by side into a
+//    ring of shared-memory slots with cp.async.bulk (the TMA bulk-copy
+//    engine), full/empty mbarriers, no __syncthreads.  Items are walked in
+//    frame-fastest order, so frame t's rows are read as `cur` by item (t, s)
+//    and as `prev` by item (t+1, s) at about the same time and the second
+//    read is an L2 hit.
+//  * 8 consumer warps take stages round-robin; a lane turns 96 bytes (32 RGB
+//    pixels) of cur/prev into one 32-bit raw-foreground word with packed
+//    SIMD byte ops (VABSDIFF4 + SWAR compare + PRMT planar regroup) and
+//    stores it in the item's bitmap in shared memory.
+//  * When an item's bitmap is complete the consumers dilate it (vertical OR
+//    over 2r+1 rows, horizontal funnel shifts with neighbour words taken from
+//    adjacent lanes by shuffles) one 16-row cell band at a time and fold it
+//    into per-cell popcounts and bbox bit-masks, written as packed u32 cell
+//    summaries plus an activity bitmask.  Meanwhile the producer is already
+//    prefetching the next item.
+// HBM traffic is the frames themselves; the outputs are ~0.5% of it.
 #include <algorithm>
 #include <cstdlib>
 
@@ -24,11 +29,17 @@
 
 namespace tg {
 
-constexpr int kK1Threads = 256;
-constexpr int kK1Ring = 32;            // fg0 rows held (>= 2*rows_per_stage + 2*radius)
-constexpr int kK1MaxWords = kK1Threads; // one output word per thread: width <= 8192
-constexpr int kK1SegRows = 128;        // rows per work item (multiple of kCell)
-constexpr int kK1StageTarget = 48 * 1024;
+// One consumer warp per smem slot (NS <= 8): a slot's consecutive phases are
+// always waited on by the same warp, so mbarrier parity waits can never run
+// two phases ahead.
+constexpr int kK1MaxSlots = 8;
+constexpr int kK1MaxThreads = (kK1MaxSlots + 1) * 32;
+constexpr int kK1MaxSeg = 128;          // rows per work item (multiple of kCell)
+constexpr int kK1SlotTarget = 24 * 1024;
+constexpr int kK1SmemBudget = 227 * 1024;
+constexpr int kK1GroupWords = 30;       // output words per warp task (lanes 1..30)
+constexpr int kK1MaxBands = kK1MaxSeg / kCell;
+constexpr int kK1MaxActWords = 16;      // act words per cell row held in smem (W <= 8192)
 
 struct MaskArgs {
   const uint8_t* const* cur;
@@ -37,34 +48,28 @@ struct MaskArgs {
   int nwords;          // ceil(W/32)
   int cells_x, cells_y, act_words;
   int rows_per_stage;  // RP
-  int nstages;         // smem slots
+  int nstages;         // NS smem slots
+  int seg_rows;        // SEG
   int nseg, total_items;
   uint32_t* cells;     // [F][cells_y][cells_x]
   uint32_t* active;    // [F][cells_y][act_words]
   uint32_t* mask_out;  // optional [F][H][nwords]
 };
 
-struct ItemCursor {
-  int item, st, nst, f, s0, s1, ya, yb;
+struct Item {
+  int f, s0, s1, ya, yb, nst;
 };
 
-__device__ __forceinline__ void cursor_load(ItemCursor& c, const MaskArgs& a) {
-  if (c.item >= a.total_items) return;
-  c.f = c.item % a.n_frames;
-  const int seg = c.item / a.n_frames;
-  c.s0 = seg * kK1SegRows;
-  c.s1 = min(a.H, c.s0 + kK1SegRows);
-  c.ya = max(0, c.s0 - a.radius);
-  c.yb = min(a.H, c.s1 + a.radius);
-  c.nst = ceil_div(c.yb - c.ya, a.rows_per_stage);
-  c.st = 0;
-}
-
-__device__ __forceinline__ void cursor_next(ItemCursor& c, const MaskArgs& a) {
-  if (++c.st >= c.nst) {
-    c.item += gridDim.x;
-    cursor_load(c, a);
-  }
+__device__ __forceinline__ Item load_item(const MaskArgs& a, int item) {
+  Item it;
+  it.f = item % a.n_frames;
+  const int seg = item / a.n_frames;
+  it.s0 = seg * a.seg_rows;
+  it.s1 = min(a.H, it.s0 + a.seg_rows);
+  it.ya = max(0, it.s0 - a.radius);
+  it.yb = min(a.H, it.s1 + a.radius);
+  it.nst = ceil_div(it.yb - it.ya, a.rows_per_stage);
+  return it;
 }
 
 // Per-byte "d > T" flag in bit 7 of each byte, SWAR without cross-byte
@@ -95,7 +100,7 @@ __device__ __forceinline__ uint32_t fg4(uint32_t a0, uint32_t a1, uint32_t a2, u
 // 32 pixels (96 bytes, or 48 for a trailing half word) -> 32 raw fg bits.
 template <bool kLow>
 __device__ __forceinline__ uint32_t fg_word(const uint8_t* cs, const uint8_t* ps, int nbytes,
-                                            uint32_t t4) {
+                                            uint32_t t1) {
   uint32_t bits = 0;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -103,22 +108,13 @@ __device__ __forceinline__ uint32_t fg_word(const uint8_t* cs, const uint8_t* ps
     const uint4 c0 = lds128(cs + 48 * h), c1 = lds128(cs + 48 * h + 16), c2 = lds128(cs + 48 * h + 32);
     const uint4 p0 = lds128(ps + 48 * h), p1 = lds128(ps + 48 * h + 16), p2 = lds128(ps + 48 * h + 32);
     uint32_t v = 0;
-    v |= fg4<kLow>(c0.x, c0.y, c0.z, p0.x, p0.y, p0.z, t4);
-    v |= fg4<kLow>(c0.w, c1.x, c1.y, p0.w, p1.x, p1.y, t4) << 4;
-    v |= fg4<kLow>(c1.z, c1.w, c2.x, p1.z, p1.w, p2.x, t4) << 8;
-    v |= fg4<kLow>(c2.y, c2.z, c2.w, p2.y, p2.z, p2.w, t4) << 12;
+    v |= fg4<kLow>(c0.x, c0.y, c0.z, p0.x, p0.y, p0.z, t1);
+    v |= fg4<kLow>(c0.w, c1.x, c1.y, p0.w, p1.x, p1.y, t1) << 4;
+    v |= fg4<kLow>(c1.z, c1.w, c2.x, p1.z, p1.w, p2.x, t1) << 8;
+    v |= fg4<kLow>(c2.y, c2.z, c2.w, p2.y, p2.z, p2.w, t1) << 12;
     bits |= v << (16 * h);
   }
   return bits;
-}
-
-__device__ __forceinline__ uint32_t spread16(uint32_t x) {
-  x &= 0xffffu;
-  x = (x | (x << 8)) & 0x00ff00ffu;
-  x = (x | (x << 4)) & 0x0f0f0f0fu;
-  x = (x | (x << 2)) & 0x33333333u;
-  x = (x | (x << 1)) & 0x55555555u;
-  return x;
 }
 
 __device__ __forceinline__ uint32_t pack_cell(int occ, uint32_t cols, uint32_t rows) {
@@ -128,173 +124,187 @@ __device__ __forceinline__ uint32_t pack_cell(int occ, uint32_t cols, uint32_t r
   return static_cast<uint32_t>(occ) | x0 << 9 | x1 << 13 | y0 << 17 | y1 << 21;
 }
 
-__global__ void __launch_bounds__(kK1Threads, 1) mask_cells_kernel(const MaskArgs a) {
+__device__ __forceinline__ void consumer_bar(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(kK1MaxThreads, 1) mask_cells_kernel(const MaskArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int NS = a.nstages, RP = a.rows_per_stage;
   const int slot_bytes = 2 * RP * a.rowbytes;
   uint8_t* slots = smem;
-  uint32_t* ring = reinterpret_cast<uint32_t*>(smem + NS * slot_bytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kK1Ring * kK1MaxWords);
-  const int tid = threadIdx.x;
-  const bool t_low = a.threshold <= 127;
-  const uint32_t t1 = static_cast<uint32_t>(t_low ? a.threshold + 1 : a.threshold - 127) * 0x01010101u;
+  uint32_t* F = reinterpret_cast<uint32_t*>(smem + NS * slot_bytes);  // item bitmap
+  const int f_rows = a.seg_rows + 2 * a.radius;
+  uint32_t* act_s = F + f_rows * a.nwords;                          // [bands][act words]
+  uint64_t* full = reinterpret_cast<uint64_t*>(act_s + kK1MaxBands * kK1MaxActWords);
+  uint64_t* empty = full + NS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  if (tid == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
     fence_mbar_init();
   }
+  for (int i = threadIdx.x; i < kK1MaxBands * kK1MaxActWords; i += blockDim.x) act_s[i] = 0;
   __syncthreads();
 
-  // Producer cursor (thread 0 only) runs NS stages ahead of the consumers.
-  ItemCursor pc{static_cast<int>(blockIdx.x), 0, 0, 0, 0, 0, 0, 0};
-  cursor_load(pc, a);
-  auto issue = [&](long long g) {
-    const int slot = static_cast<int>(g % NS);
-    const int y0 = pc.ya + pc.st * RP;
-    const int nr = min(RP, pc.yb - y0);
-    const uint32_t bytes = static_cast<uint32_t>(nr * a.rowbytes);
-    uint8_t* dc = slots + slot * slot_bytes;
-    uint8_t* dp = dc + RP * a.rowbytes;
-    const uint8_t* sc = a.cur[pc.f] + static_cast<size_t>(y0) * a.pitch;
-    const uint8_t* sp = a.prev[pc.f] + static_cast<size_t>(y0) * a.pitch;
-    mbar_arrive_expect_tx(&bars[slot], 2 * bytes);
-    if (a.pitch == a.rowbytes) {
-      bulk_g2s(dc, sc, bytes, &bars[slot]);
-      bulk_g2s(dp, sp, bytes, &bars[slot]);
-    } else {
-      for (int k = 0; k < nr; ++k) {
-        bulk_g2s(dc + k * a.rowbytes, sc + static_cast<size_t>(k) * a.pitch, a.rowbytes, &bars[slot]);
-        bulk_g2s(dp + k * a.rowbytes, sp + static_cast<size_t>(k) * a.pitch, a.rowbytes, &bars[slot]);
-      }
-    }
-    cursor_next(pc, a);
-  };
-  long long issued = 0;
-  if (tid == 0) {
-    while (issued < NS && pc.item < a.total_items) issue(issued++);
-  }
-
-  // Consumer state (identical in every thread).
-  ItemCursor cc{static_cast<int>(blockIdx.x), 0, 0, 0, 0, 0, 0, 0};
-  cursor_load(cc, a);
-  long long g = 0;          // stage counter
-  long long ring_base = 0;  // ring row of this item's row ya
-  long long ring_next = 0;  // ring row counter
-  int out_next = 0;         // next output row of the current item
-  const int w = tid;        // output word owned in the dilation phase
-  const bool owns_word = w < a.nwords;
-  const bool in_warp_range = w < ((a.nwords + 31) & ~31);
-  int occ_lo = 0, occ_hi = 0;
-  uint32_t col_lo = 0, col_hi = 0, row_lo = 0, row_hi = 0;
-  const uint32_t lastmask =
-      (a.W & 31) ? ((1u << (a.W & 31)) - 1u) : 0xffffffffu;
-
-  while (cc.item < a.total_items) {
-    if (cc.st == 0) {
-      ring_base = ring_next;
-      out_next = cc.s0;
-    }
-    const int slot = static_cast<int>(g % NS);
-    const uint32_t parity = static_cast<uint32_t>((g / NS) & 1);
-    const int y0 = cc.ya + cc.st * RP;
-    const int nr = min(RP, cc.yb - y0);
-    mbar_wait(&bars[slot], parity);
-
-    // ---- raw foreground words for the nr rows of this stage ----
-    const uint8_t* sc = slots + slot * slot_bytes;
-    const uint8_t* sp = sc + RP * a.rowbytes;
-    for (int it = tid; it < nr * a.nwords; it += kK1Threads) {
-      const int k = it / a.nwords, ww = it - k * a.nwords;
-      const int off = 96 * ww;
-      const int nbytes = min(96, a.rowbytes - off);
-      const uint8_t* cw = sc + k * a.rowbytes + off;
-      const uint8_t* pw = sp + k * a.rowbytes + off;
-      uint32_t f = t_low ? fg_word<true>(cw, pw, nbytes, t1) : fg_word<false>(cw, pw, nbytes, t1);
-      if (ww == a.nwords - 1) f &= lastmask;
-      const long long rr = ring_base + (y0 - cc.ya) + k;
-      ring[(rr & (kK1Ring - 1)) * kK1MaxWords + ww] = f;
-    }
-    ring_next = ring_base + (y0 - cc.ya) + nr;
-    __syncthreads();
-    if (tid == 0 && pc.item < a.total_items) {
-      fence_proxy_async_smem();
-      issue(g + NS);
-    }
-
-    // ---- dilation + cell accumulation for rows that now have look-ahead ----
-    const int y_last = y0 + nr - 1;
-    const bool item_done = (cc.st == cc.nst - 1);
-    const int out_hi = item_done ? cc.s1 - 1 : min(cc.s1 - 1, y_last - a.radius);
-    if (in_warp_range) {
-      for (int y = out_next; y <= out_hi; ++y) {
-        uint32_t vm = 0, vc = 0, vp = 0;
-        const int lo = max(y - a.radius, 0), hi = min(y + a.radius, a.H - 1);
-        if (owns_word) {
-          for (int yy = lo; yy <= hi; ++yy) {
-            const uint32_t* rrow = ring + ((ring_base + (yy - cc.ya)) & (kK1Ring - 1)) * kK1MaxWords;
-            vc |= rrow[w];
-            if (w > 0) vm |= rrow[w - 1];
-            if (w + 1 < a.nwords) vp |= rrow[w + 1];
+  const int ncw = NS;  // consumer warps
+  if (warp == ncw) {
+    // ================= producer: one elected lane issues every copy =========
+    if (lane == 0) {
+      long long g = 0;
+      for (int item = blockIdx.x; item < a.total_items; item += gridDim.x) {
+        const Item it = load_item(a, item);
+        const uint8_t* cur = a.cur[it.f];
+        const uint8_t* prev = a.prev[it.f];
+        for (int st = 0; st < it.nst; ++st, ++g) {
+          const int slot = static_cast<int>(g % NS);
+          if (g >= NS) mbar_wait(&empty[slot], static_cast<uint32_t>(((g / NS) - 1) & 1));
+          const int y0 = it.ya + st * RP;
+          const int nr = min(RP, it.yb - y0);
+          const uint32_t bytes = static_cast<uint32_t>(nr * a.rowbytes);
+          uint8_t* dc = slots + slot * slot_bytes;
+          uint8_t* dp = dc + RP * a.rowbytes;
+          const uint8_t* sc = cur + static_cast<size_t>(y0) * a.pitch;
+          const uint8_t* sp = prev + static_cast<size_t>(y0) * a.pitch;
+          mbar_arrive_expect_tx(&full[slot], 2 * bytes);
+          if (a.pitch == a.rowbytes) {
+            bulk_g2s(dc, sc, bytes, &full[slot]);
+            bulk_g2s(dp, sp, bytes, &full[slot]);
+          } else {
+            for (int k = 0; k < nr; ++k) {
+              bulk_g2s(dc + k * a.rowbytes, sc + static_cast<size_t>(k) * a.pitch, a.rowbytes,
+                       &full[slot]);
+              bulk_g2s(dp + k * a.rowbytes, sp + static_cast<size_t>(k) * a.pitch, a.rowbytes,
+                       &full[slot]);
+            }
           }
         }
-        uint32_t d = vc;
+      }
+    }
+    return;
+  }
+
+  // ===================== consumers ===========================================
+  const bool t_low = a.threshold <= 127;
+  const uint32_t t1 =
+      static_cast<uint32_t>(t_low ? a.threshold + 1 : a.threshold - 127) * 0x01010101u;
+  const uint32_t lastmask = (a.W & 31) ? ((1u << (a.W & 31)) - 1u) : 0xffffffffu;
+  const int ngroups = ceil_div(a.nwords, kK1GroupWords);
+  long long g = 0;  // global stage counter (same sequence as the producer)
+  for (int item = blockIdx.x; item < a.total_items; item += gridDim.x) {
+    const Item it = load_item(a, item);
+    // ---- raw foreground words: this warp's stages of the item ----
+    for (int st = 0; st < it.nst; ++st, ++g) {
+      const int slot = static_cast<int>(g % NS);
+      if (slot != warp) continue;  // stage g belongs to the warp owning its slot
+      mbar_wait(&full[slot], static_cast<uint32_t>((g / NS) & 1));
+      const int y0 = it.ya + st * RP;
+      const int nr = min(RP, it.yb - y0);
+      const uint8_t* sc = slots + slot * slot_bytes;
+      const uint8_t* sp = sc + RP * a.rowbytes;
+      for (int k = 0; k < nr; ++k) {
+        uint32_t* frow = F + (y0 + k - it.ya) * a.nwords;
+        for (int w = lane; w < a.nwords; w += 32) {
+          const int off = 96 * w;
+          const int nbytes = min(96, a.rowbytes - off);
+          const uint8_t* cw = sc + k * a.rowbytes + off;
+          const uint8_t* pw = sp + k * a.rowbytes + off;
+          uint32_t fw = t_low ? fg_word<true>(cw, pw, nbytes, t1) : fg_word<false>(cw, pw, nbytes, t1);
+          if (w == a.nwords - 1) fw &= lastmask;
+          frow[w] = fw;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);  // slot may be refilled
+    }
+    consumer_bar(ncw * 32);  // bitmap of the item complete
+
+    // ---- dilation + cell summaries, one (16-row band, 30-word group) task
+    //      per warp at a time ----
+    const int nbands = ceil_div(it.s1 - it.s0, kCell);
+    for (int task = warp; task < nbands * ngroups; task += ncw) {
+      const int band = task / ngroups, grp = task - band * ngroups;
+      const int w = grp * kK1GroupWords + lane - 1;
+      const bool col_ok = w >= 0 && w < a.nwords;
+      const bool owns = lane >= 1 && lane <= kK1GroupWords && col_ok;
+      const int yb0 = it.s0 + band * kCell;
+      const int yb1 = min(yb0 + kCell, it.s1);
+      int occ_lo = 0, occ_hi = 0;
+      uint32_t col_lo = 0, col_hi = 0, row_lo = 0, row_hi = 0;
+      for (int y = yb0; y < yb1; ++y) {
+        uint32_t v = 0;
+        if (col_ok) {
+          const int lo = max(y - a.radius, it.ya), hi = min(y + a.radius, it.yb - 1);
+          for (int yy = lo; yy <= hi; ++yy) v |= F[(yy - it.ya) * a.nwords + w];
+        }
+        const uint32_t vm = __shfl_up_sync(0xffffffffu, v, 1);
+        const uint32_t vp = __shfl_down_sync(0xffffffffu, v, 1);
+        uint32_t d = v;
         for (int k = 1; k <= a.radius; ++k)
-          d |= __funnelshift_r(vc, vp, k) | __funnelshift_l(vm, vc, k);
+          d |= __funnelshift_r(v, vp, k) | __funnelshift_l(vm, v, k);
         if (w == a.nwords - 1) d &= lastmask;
-        if (!owns_word) d = 0;
-        if (a.mask_out && owns_word)
-          a.mask_out[(static_cast<size_t>(cc.f) * a.H + y) * a.nwords + w] = d;
+        if (!owns) d = 0;
+        if (a.mask_out && owns) a.mask_out[(static_cast<size_t>(it.f) * a.H + y) * a.nwords + w] = d;
         const uint32_t dl = d & 0xffffu, dh = d >> 16;
-        const int ly = y & (kCell - 1);
+        const int ly = y - yb0;
         occ_lo += __popc(dl);
         occ_hi += __popc(dh);
         col_lo |= dl;
         col_hi |= dh;
         row_lo |= (dl ? 1u : 0u) << ly;
         row_hi |= (dh ? 1u : 0u) << ly;
-        if (ly == kCell - 1 || y == a.H - 1) {
-          const int cy = y / kCell;
-          const size_t cbase = (static_cast<size_t>(cc.f) * a.cells_y + cy) * a.cells_x;
-          if (owns_word) {
-            const int cx = 2 * w;
-            a.cells[cbase + cx] = pack_cell(occ_lo, col_lo, row_lo);
-            if (cx + 1 < a.cells_x) a.cells[cbase + cx + 1] = pack_cell(occ_hi, col_hi, row_hi);
-          }
-          const uint32_t blo = __ballot_sync(0xffffffffu, occ_lo > 0);
-          const uint32_t bhi = __ballot_sync(0xffffffffu, occ_hi > 0);
-          const int lane = tid & 31, wq = tid >> 5;
-          const size_t abase = (static_cast<size_t>(cc.f) * a.cells_y + cy) * a.act_words;
-          if (lane < 2 && 2 * wq + lane < a.act_words) {
-            const uint32_t lo16 = lane ? (blo >> 16) : blo, hi16 = lane ? (bhi >> 16) : bhi;
-            a.active[abase + 2 * wq + lane] = spread16(lo16) | (spread16(hi16) << 1);
-          }
-          occ_lo = occ_hi = 0;
-          col_lo = col_hi = row_lo = row_hi = 0;
-        }
+      }
+      if (owns) {
+        const int cy = yb0 / kCell, cx = 2 * w;
+        const size_t cbase = (static_cast<size_t>(it.f) * a.cells_y + cy) * a.cells_x;
+        a.cells[cbase + cx] = pack_cell(occ_lo, col_lo, row_lo);
+        if (cx + 1 < a.cells_x) a.cells[cbase + cx + 1] = pack_cell(occ_hi, col_hi, row_hi);
+        const uint32_t bits = (occ_lo > 0 ? 1u : 0u) | (occ_hi > 0 ? 2u : 0u);
+        if (bits) atomicOr(&act_s[band * kK1MaxActWords + (cx >> 5)], bits << (cx & 31));
       }
     }
-    out_next = max(out_next, out_hi + 1);  // stages of pure look-behind halo output nothing
-    ++g;
-    cursor_next(cc, a);
+    consumer_bar(ncw * 32);  // act_s complete, bitmap free for the next item
+    for (int i = threadIdx.x; i < nbands * a.act_words; i += ncw * 32) {
+      const int band = i / a.act_words, aw = i - band * a.act_words;
+      const int cy = (it.s0 / kCell) + band;
+      a.active[(static_cast<size_t>(it.f) * a.cells_y + cy) * a.act_words + aw] =
+          act_s[band * kK1MaxActWords + aw];
+      act_s[band * kK1MaxActWords + aw] = 0;
+    }
+    // act_s is next touched after the next item's first consumer_bar().
   }
 }
 
 // ---- host launcher ---------------------------------------------------------
 struct MaskPlan {
-  int rows_per_stage, nstages;
+  int rows_per_stage, nstages, seg_rows;
   size_t smem;
 };
 
-MaskPlan plan_mask(int W) {
-  const int rowbytes = 3 * W;
+static MaskPlan plan_mask(int W, int radius) {
+  const int rowbytes = 3 * W, nwords = ceil_div(W, 32);
   MaskPlan p;
-  p.rows_per_stage = std::max(1, std::min(8, kK1StageTarget / (2 * rowbytes)));
-  const size_t fixed = static_cast<size_t>(kK1Ring) * kK1MaxWords * 4 + 8 * 8;
-  p.nstages = 4;
-  while (p.nstages > 2 &&
-         fixed + static_cast<size_t>(p.nstages) * 2 * p.rows_per_stage * rowbytes > 227 * 1024)
-    --p.nstages;
-  p.smem = fixed + static_cast<size_t>(p.nstages) * 2 * p.rows_per_stage * rowbytes;
+  p.rows_per_stage = std::max(1, std::min(8, kK1SlotTarget / (2 * rowbytes)));
+  const size_t slot = static_cast<size_t>(2) * p.rows_per_stage * rowbytes;
+  const size_t fixed = static_cast<size_t>(kK1MaxBands) * kK1MaxActWords * 4 + 2 * 8 * 8 + 128;
+  p.nstages = kK1MaxSlots;
+  p.seg_rows = kK1MaxSeg;
+  auto total = [&](int ns, int seg) {
+    return fixed + ns * slot + static_cast<size_t>(seg + 2 * radius) * nwords * 4;
+  };
+  const size_t budget = static_cast<size_t>(kK1SmemBudget);
+  while (total(p.nstages, p.seg_rows) > budget && p.nstages > 4) --p.nstages;
+  while (total(p.nstages, p.seg_rows) > budget && p.seg_rows > 64) p.seg_rows -= kCell;
+  while (total(p.nstages, p.seg_rows) > budget && p.nstages > 2) --p.nstages;
+  while (total(p.nstages, p.seg_rows) > budget && p.seg_rows > kCell) p.seg_rows -= kCell;
+  p.smem = total(p.nstages, p.seg_rows);
   return p;
 }
 
@@ -317,10 +327,13 @@ cudaError_t launch_mask_cells(const uint8_t* const* d_cur, const uint8_t* const*
   a.cells_x = ceil_div(W, kCell);
   a.cells_y = ceil_div(H, kCell);
   a.act_words = ceil_div(a.cells_x, 32);
-  const MaskPlan mp = plan_mask(W);
+  const MaskPlan mp = plan_mask(W, radius);
+  if (mp.smem > static_cast<size_t>(kK1SmemBudget) || a.act_words > kK1MaxActWords)
+    return cudaErrorInvalidConfiguration;
   a.rows_per_stage = mp.rows_per_stage;
   a.nstages = mp.nstages;
-  a.nseg = ceil_div(H, kK1SegRows);
+  a.seg_rows = mp.seg_rows;
+  a.nseg = ceil_div(H, a.seg_rows);
   a.total_items = a.nseg * n_frames;
   a.cells = d_cells;
   a.active = d_active;
@@ -331,7 +344,7 @@ cudaError_t launch_mask_cells(const uint8_t* const* d_cur, const uint8_t* const*
   if (e != cudaSuccess) return e;
   int grid = std::min(a.total_items, sms);
   if (const char* g = std::getenv("TG_K1_GRID")) grid = std::max(1, std::min(a.total_items, std::atoi(g)));
-  mask_cells_kernel<<<grid, kK1Threads, mp.smem, stream>>>(a);
+  mask_cells_kernel<<<grid, (mp.nstages + 1) * 32, mp.smem, stream>>>(a);
   return cudaGetLastError();
 }
 

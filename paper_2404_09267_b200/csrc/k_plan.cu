@@ -1,94 +1,38 @@
 // k_plan.cu -- per-frame planner (K2 RoI boxes + K3 partition + K4 stitch
 // plan), the frame-order scan, and the drop-in rect-level kernels.
 //
-// K2 (absent from the reference): 8-connected components over
-// the active patch-grid cells by union-find on 16-bit labels in shared
-// memory (atomic-CAS min linking, so every root is its component's first
-// cell in raster order), then one pixel-tight box per component from the
-// per-cell bboxes K1 wrote.  Boxes are ranked by their root cell, i.e. in
-// the oracle's raster order.
-// K3 = partition() (partition.hpp:119-143) and K4 = stitch_all()
-// (stitch.hpp:108-146) on that frame's admitted patches (sim.hpp:262,
-// 302-332), both from rect_core.cuh.  The planner finally emits the gather
-// jobs: every placement plus every final free rect, which tile each canvas
-// exactly, grouped by canvas.
+// One CTA per frame:
+//   K2 (absent from the reference): ccl.cuh -- 8-connected
+//      components over the active cells, one pixel-tight box per component
+//      in the oracle's raster order;
+//   K3 partition() (partition.hpp:119-143) and admission (sim.hpp:262);
+//   K4 stitch_all() (stitch.hpp:108-146) on the frame's admitted patches
+//      (sim.hpp:302-332), one warp;
+// then the gather jobs: every placement plus every final free rect, which
+// tile each canvas exactly, grouped by canvas and sorted
+// by x so the gather can walk canvas rows left to right.
 #include <algorithm>
 
+#include "ccl.cuh"
 #include "kernels.cuh"
 #include "rect_core.cuh"
 
 namespace tg {
 
-constexpr int kPlanThreads = 512;
+constexpr int kPlanThreads = 256;
 
-__device__ __forceinline__ int uf_find(volatile uint16_t* L, int x) {
-  int p = L[x];
-  while (p != x) {
-    x = p;
-    p = L[x];
+// Rank sort of one canvas's jobs by (dx, dy) -- unique, since a canvas's
+// placements and free rects are disjoint -- from tmp into out.  One warp.
+__device__ __forceinline__ void sort_jobs_by_x(const Job* tmp, int n, Job* out, int lane) {
+  for (int i = lane; i < n; i += 32) {
+    const Job a = tmp[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const Job b = tmp[j];
+      rank += (b.dx < a.dx) || (b.dx == a.dx && (b.dy < a.dy || (b.dy == a.dy && j < i)));
+    }
+    out[rank] = a;
   }
-  return x;
-}
-
-__device__ __forceinline__ void uf_merge(uint16_t* L, int a, int b) {
-  volatile uint16_t* VL = L;
-  while (true) {
-    a = uf_find(VL, a);
-    b = uf_find(VL, b);
-    if (a == b) return;
-    if (a < b) {
-      const int t = a;
-      a = b;
-      b = t;
-    }
-    // Link root a (larger) under b: 16-bit atomic min via CAS.
-    unsigned short old = VL[a];
-    while (old > b) {
-      const unsigned short prev =
-          atomicCAS(reinterpret_cast<unsigned short*>(&L[a]), old, static_cast<unsigned short>(b));
-      if (prev == old) break;
-      old = prev;
-    }
-    if (old == a) return;  // a was still a root and now points at b
-    a = old;               // someone re-linked a meanwhile: retry from there
-  }
-}
-
-__device__ __forceinline__ bool act_bit(const uint32_t* act, int aw, int cy, int cx) {
-  return (act[cy * aw + (cx >> 5)] >> (cx & 31)) & 1u;
-}
-
-// Block-wide exclusive scan of n ints in place (n <= any), returns total.
-__device__ int block_exclusive_scan(int* v, int n, int* warp_tmp) {
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
-  int carry = 0;
-  for (int base = 0; base < n; base += nt) {
-    const int i = base + tid;
-    const int x = i < n ? v[i] : 0;
-    int s = x;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += y;
-    }
-    if (lane == 31) warp_tmp[wid] = s;
-    __syncthreads();
-    if (wid == 0) {
-      int t = lane < nt / 32 ? warp_tmp[lane] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, t, o);
-        if (lane >= o) t += y;
-      }
-      warp_tmp[lane] = t;  // inclusive warp totals
-    }
-    __syncthreads();
-    const int before = (wid ? warp_tmp[wid - 1] : 0) + s - x;
-    const int total = warp_tmp[nt / 32 - 1];
-    __syncthreads();
-    if (i < n) v[i] = carry + before;
-    carry += total;
-  }
-  __syncthreads();
-  return carry;
 }
 
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
@@ -98,126 +42,35 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   __shared__ int adm_w[kMaxZones], adm_h[kMaxZones], adm_idx[kMaxZones];
   __shared__ FreeRect freel[2 * kMaxZones + 2];
   __shared__ StitchOut souts[kMaxZones];
+  __shared__ Job sjobs[3 * kMaxZones];
   __shared__ int warp_tmp[32];
   __shared__ int s_nrois;
 
   const int f = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-  const int aw = a.act_words, ncw = a.cells_y * aw, cx_n = a.cells_x;
-  uint32_t* act = reinterpret_cast<uint32_t*>(dsm);
-  uint32_t* rootm = act + ncw;
-  int* wpre = reinterpret_cast<int*>(rootm + ncw);
-  int* bx0 = wpre + ncw + 1;
-  int* by0 = bx0 + a.max_rois;
-  int* bx1 = by0 + a.max_rois;
-  int* by1 = bx1 + a.max_rois;
-  uint16_t* L = reinterpret_cast<uint16_t*>(by1 + a.max_rois);
+  const int cx_n = a.cells_x, cy_n = a.cells_y, aw = a.act_words, ncw = cy_n * aw;
+  CclSmem cs;
+  cs.act = reinterpret_cast<uint32_t*>(dsm);
+  cs.rootm = cs.act + ncw;
+  cs.wpre = reinterpret_cast<int*>(cs.rootm + ncw);
+  cs.bx0 = cs.wpre + ncw + 1;
+  cs.by0 = cs.bx0 + a.max_rois;
+  cs.bx1 = cs.by0 + a.max_rois;
+  cs.by1 = cs.bx1 + a.max_rois;
+  cs.L = reinterpret_cast<uint16_t*>(cs.by1 + a.max_rois);
 
-  const uint32_t* gact = a.active + static_cast<size_t>(f) * ncw;
-  const uint32_t* gcells = a.cells + static_cast<size_t>(f) * a.cells_y * cx_n;
-
-  // ---- K2: labels on active cells --------------------------------------
-  for (int i = tid; i < ncw; i += nt) {
-    const uint32_t bits = gact[i];
-    act[i] = bits;
-    uint32_t m = bits;
-    const int cy = i / aw, cxb = (i - cy * aw) * 32;
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      const int idx = cy * cx_n + cxb + b;
-      L[idx] = static_cast<uint16_t>(idx);
-    }
-  }
-  __syncthreads();
-  for (int i = tid; i < ncw; i += nt) {
-    uint32_t m = act[i];
-    const int cy = i / aw, cxb = (i - cy * aw) * 32;
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      const int cx = cxb + b, idx = cy * cx_n + cx;
-      if (cx > 0 && act_bit(act, aw, cy, cx - 1)) uf_merge(L, idx, idx - 1);
-      if (cy > 0) {
-        if (cx > 0 && act_bit(act, aw, cy - 1, cx - 1)) uf_merge(L, idx, idx - cx_n - 1);
-        if (act_bit(act, aw, cy - 1, cx)) uf_merge(L, idx, idx - cx_n);
-        if (cx + 1 < cx_n && act_bit(act, aw, cy - 1, cx + 1)) uf_merge(L, idx, idx - cx_n + 1);
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = tid; i < ncw; i += nt) {
-    uint32_t m = act[i], roots = 0;
-    const int cy = i / aw, cxb = (i - cy * aw) * 32;
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      const int idx = cy * cx_n + cxb + b;
-      const int r = uf_find(L, idx);
-      if (r == idx) roots |= 1u << b;
-    }
-    rootm[i] = roots;
-    wpre[i] = __popc(roots);
-  }
-  __syncthreads();
-  // Full path compression (separate pass: finds above must see stable roots).
-  for (int i = tid; i < ncw; i += nt) {
-    uint32_t m = act[i];
-    const int cy = i / aw, cxb = (i - cy * aw) * 32;
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      const int idx = cy * cx_n + cxb + b;
-      L[idx] = static_cast<uint16_t>(uf_find(L, idx));
-    }
-  }
-  const int ncomp = block_exclusive_scan(wpre, ncw, warp_tmp);
-  if (tid == 0) {
-    wpre[ncw] = ncomp;
-    int n = ncomp;
-    if (n > a.max_rois) {
-      raise_error(a.err, TG_ERR_CAPACITY, kErrRoiCapacity, f, ncomp, a.max_rois);
-      n = a.max_rois;
-    }
-    s_nrois = n;
-  }
-  __syncthreads();
-  const int nr = s_nrois;
-  for (int r = tid; r < nr; r += nt) {
-    bx0[r] = INT_MAX;
-    by0[r] = INT_MAX;
-    bx1[r] = INT_MIN;
-    by1[r] = INT_MIN;
-  }
-  __syncthreads();
-  for (int i = tid; i < ncw; i += nt) {
-    uint32_t m = act[i];
-    const int cy = i / aw, cxb = (i - cy * aw) * 32;
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      const int cx = cxb + b, idx = cy * cx_n + cx;
-      const int root = L[idx];
-      const int rcy = root / cx_n, rcx = root - rcy * cx_n;
-      const int rw = rcy * aw + (rcx >> 5);
-      const int rank = wpre[rw] + __popc(rootm[rw] & ((1u << (rcx & 31)) - 1u));
-      if (rank >= nr) continue;
-      const uint32_t v = gcells[idx];
-      atomicMin(&bx0[rank], cx * kCell + static_cast<int>(v >> 9 & 15u));
-      atomicMax(&bx1[rank], cx * kCell + static_cast<int>(v >> 13 & 15u));
-      atomicMin(&by0[rank], cy * kCell + static_cast<int>(v >> 17 & 15u));
-      atomicMax(&by1[rank], cy * kCell + static_cast<int>(v >> 21 & 15u));
-    }
-  }
-  __syncthreads();
+  // ---- K2: RoI boxes ---------------------------------------------------------
+  const int nr = ccl_frame(a.active + static_cast<size_t>(f) * ncw,
+                           a.cells + static_cast<size_t>(f) * cy_n * cx_n, cx_n, cy_n, a.max_rois,
+                           cs, warp_tmp, &s_nrois, a.err, f);
   tg_rect* frois = a.rois + static_cast<size_t>(f) * a.max_rois;
   for (int r = tid; r < nr; r += nt)
-    frois[r] = tg_rect{bx0[r], by0[r], bx1[r] - bx0[r] + 1, by1[r] - by0[r] + 1};
+    frois[r] = tg_rect{cs.bx0[r], cs.by0[r], cs.bx1[r] - cs.bx0[r] + 1, cs.by1[r] - cs.by0[r] + 1};
   const int nz = a.X * a.Y;
   zone_acc_init(zacc, nz, tid, nt);
   if (tid == 0) a.n_rois[f] = nr;
   __syncthreads();
 
-  // ---- K3: partition (Alg. 1) ------------------------------------------
+  // ---- K3: partition (Alg. 1) --------------------------------------------
   partition_accumulate(frois, nr, a.W, a.H, a.X, a.Y, zacc, a.err, f, nullptr, tid, nt);
   __syncthreads();
   if (tid >= 32) return;
@@ -247,7 +100,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   for (int j = np + lane; j < nz; j += 32) a.admitted[static_cast<size_t>(f) * nz + j] = 0;
   __syncwarp();
 
-  // ---- K4: stitch plan (Alg. 2 solver) ---------------------------------
+  // ---- K4: stitch plan (Alg. 2 solver) -------------------------------------
   int nfree = 0;
   const int nc = na ? bssf_stitch(adm_w, adm_h, nullptr, na, a.M, a.N, freel, 2 * kMaxZones + 2,
                                   souts, &nfree, a.err, f, lane)
@@ -268,13 +121,13 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     p.reserved = 0;
     fpl[k] = p;
   }
-  // Gather jobs grouped by canvas: placements (queue order) then free rects.
+  // Gather jobs: placements and free rects grouped by canvas, sorted by x.
   Job* fj = a.jobs + static_cast<size_t>(f) * a.job_cap;
   uint32_t* fcj = a.canvas_jobs + static_cast<size_t>(f) * nz;
   const int nitems = na + nfree;
   int pos = 0;
   for (int c = 0; c < nc; ++c) {
-    const int start = pos;
+    int cnt = 0;
     for (int ib = 0; ib < nitems; ib += 32) {
       const int it = ib + lane;
       bool mine = false;
@@ -293,10 +146,14 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
                  static_cast<uint16_t>(fr.seq & 0xffff), static_cast<uint16_t>(fr.seq >> 16)};
       }
       const unsigned m = __ballot_sync(0xffffffffu, mine);
-      if (mine) fj[pos + __popc(m & ((1u << lane) - 1u))] = jb;
-      pos += __popc(m);
+      if (mine) sjobs[cnt + __popc(m & ((1u << lane) - 1u))] = jb;
+      cnt += __popc(m);
     }
-    if (lane == 0) fcj[c] = static_cast<uint32_t>(start) | static_cast<uint32_t>(pos - start) << 16;
+    __syncwarp();
+    sort_jobs_by_x(sjobs, cnt, fj + pos, lane);
+    __syncwarp();
+    if (lane == 0) fcj[c] = static_cast<uint32_t>(pos) | static_cast<uint32_t>(cnt) << 16;
+    pos += cnt;
   }
 }
 

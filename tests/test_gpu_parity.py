@@ -299,6 +299,22 @@ def test_pipeline_cfg2_full_300_frames(ctx):
     run.close()
 
 
+@pytest.mark.parametrize("density", [0.10, 0.40, 0.59])
+def test_ccl_many_frames_vs_oracle_on_gpu_cells(ctx, density):
+    """K2 over many dense 4K frames: the GPU's RoI boxes equal the oracle's
+    components computed from the GPU's own cell grid (K1 is covered by the
+    bit-exact tests; this isolates the concurrent union-find)."""
+    run = GpuRun(ctx, 3840, 2160, 90, seed=2000, keep_mask=False,
+                 trace_kw=dict(roi_proportion_mean=density, roi_max_dim=1024, roi_count_max=24))
+    gpu = run.run()
+    cells = run.pipe.cells(run.n)
+    for i in range(run.n):
+        want = O.extract_rois(cells[i])
+        got = [tuple(r) for r in gpu["rois"][i, :gpu["n_rois"][i]].tolist()]
+        assert got == want, i
+    run.close()
+
+
 def test_round_trip_fixture(ctx):
     """Cell-aligned separated rects, static background, r=0: the GPU RoIs
     equal the rects, so the patches equal the reference's partition() of
