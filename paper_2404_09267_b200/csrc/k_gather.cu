@@ -83,35 +83,53 @@ __device__ __forceinline__ void write_row(uint8_t* row, int len, const RowIv* iv
   const uintptr_t base = rb & ~static_cast<uintptr_t>(15);
   const int lead = static_cast<int>(rb - base);  // bytes of the first chunk before the row
   const int nch = (lead + len + 15) >> 4;
-  for (int c = lane; c < nch; c += 32) {
-    const int A = 16 * c - lead;  // chunk start relative to the row
-    const int olo = max(A, 0), ohi = min(A + 16, len);
-    // last interval with s <= olo
-    int lo = 0, hi = n_iv - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (iv[mid].s <= olo) lo = mid;
-      else hi = mid - 1;
-    }
-    int k = lo;
-    uint4 out = make_uint4(0, 0, 0, 0);
-    const RowIv first = n_iv ? iv[k] : RowIv{0, len, nullptr};
-    if (first.e >= ohi && olo == A && ohi == A + 16) {
-      if (first.src) out = window16(first.src + (A - first.s), 0, 16);
-    } else {
-      for (; k < n_iv && iv[k].s < ohi; ++k) {
-        const RowIv I = iv[k];
-        if (!I.src) continue;  // zero bytes: out already zero there
-        const int blo = max(olo, I.s) - A, bhi = min(ohi, I.e) - A;
-        merge16(out, window16(I.src + (A - I.s), blo, bhi), blo, bhi);
+  constexpr int U = 4;  // chunks per lane in flight
+  for (int c0 = lane; c0 < nch; c0 += 32 * U) {
+    uint4 out[U];
+    int kk[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {  // phase 1: locate + issue the fast-path loads
+      const int c = c0 + 32 * u;
+      out[u] = make_uint4(0, 0, 0, 0);
+      kk[u] = -1;
+      if (c >= nch) continue;
+      const int A = 16 * c - lead;
+      const int olo = max(A, 0), ohi = min(A + 16, len);
+      int lo = 0, hi = n_iv - 1;  // last interval with s <= olo
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (iv[mid].s <= olo) lo = mid;
+        else hi = mid - 1;
+      }
+      const RowIv first = n_iv ? iv[lo] : RowIv{0, len, nullptr};
+      if (first.e >= ohi && olo == A && ohi == A + 16) {
+        if (first.src) out[u] = window16(first.src + (A - first.s), 0, 16);
+      } else {
+        kk[u] = lo;  // straddles intervals or the row edge: phase 2
       }
     }
-    uint8_t* dst = reinterpret_cast<uint8_t*>(base) + 16 * c;
-    if (olo == A && ohi == A + 16) {
-      *reinterpret_cast<uint4*>(dst) = out;
-    } else {  // row edge that is not 16-byte aligned: store only the row's bytes
-      const uint32_t w[4] = {out.x, out.y, out.z, out.w};
-      for (int b = olo - A; b < ohi - A; ++b) dst[b] = static_cast<uint8_t>(w[b >> 2] >> (8 * (b & 3)));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {  // phase 2: merge slow chunks, store
+      const int c = c0 + 32 * u;
+      if (c >= nch) break;
+      const int A = 16 * c - lead;
+      const int olo = max(A, 0), ohi = min(A + 16, len);
+      if (kk[u] >= 0) {
+        for (int k = kk[u]; k < n_iv && iv[k].s < ohi; ++k) {
+          const RowIv I = iv[k];
+          if (!I.src) continue;  // zero bytes: out already zero there
+          const int blo = max(olo, I.s) - A, bhi = min(ohi, I.e) - A;
+          merge16(out[u], window16(I.src + (A - I.s), blo, bhi), blo, bhi);
+        }
+      }
+      uint8_t* dst = reinterpret_cast<uint8_t*>(base) + 16 * c;
+      if (olo == A && ohi == A + 16) {
+        *reinterpret_cast<uint4*>(dst) = out[u];
+      } else {  // row edge that is not 16-byte aligned: store only the row's bytes
+        const uint32_t w[4] = {out[u].x, out[u].y, out[u].z, out[u].w};
+        for (int b = olo - A; b < ohi - A; ++b)
+          dst[b] = static_cast<uint8_t>(w[b >> 2] >> (8 * (b & 3)));
+      }
     }
   }
 }

@@ -33,7 +33,7 @@ namespace tg {
 // always waited on by the same warp, so mbarrier parity waits can never run
 // two phases ahead.
 constexpr int kK1MaxSlots = 8;
-constexpr int kK1MaxThreads = (kK1MaxSlots + 1) * 32;
+constexpr int kK1MaxThreads = 768;  // (NS*G + 1) warps; keeps <= 85 registers per thread
 constexpr int kK1MaxSeg = 128;          // rows per work item (multiple of kCell)
 constexpr int kK1SlotTarget = 24 * 1024;
 constexpr int kK1SmemBudget = 227 * 1024;
@@ -49,6 +49,7 @@ struct MaskArgs {
   int cells_x, cells_y, act_words;
   int rows_per_stage;  // RP
   int nstages;         // NS smem slots
+  int group;           // G consumer warps per slot
   int seg_rows;        // SEG
   int nseg, total_items;
   uint32_t* cells;     // [F][cells_y][cells_x]
@@ -144,28 +145,30 @@ __global__ void __launch_bounds__(kK1MaxThreads, 1) mask_cells_kernel(const Mask
   uint64_t* empty = full + NS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  const int G = a.group;       // consumer warps per slot
+  const int ncw = NS * G;      // consumer warps; warp ncw is the producer
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], G);
     }
     fence_mbar_init();
   }
   for (int i = threadIdx.x; i < kK1MaxBands * kK1MaxActWords; i += blockDim.x) act_s[i] = 0;
   __syncthreads();
 
-  const int ncw = NS;  // consumer warps
   if (warp == ncw) {
     // ================= producer: one elected lane issues every copy =========
     if (lane == 0) {
-      long long g = 0;
+      int slot = 0;
+      uint32_t phase = 0;   // parity of the slot's current use
+      bool wrapped = false; // every slot used once already
       for (int item = blockIdx.x; item < a.total_items; item += gridDim.x) {
         const Item it = load_item(a, item);
         const uint8_t* cur = a.cur[it.f];
         const uint8_t* prev = a.prev[it.f];
-        for (int st = 0; st < it.nst; ++st, ++g) {
-          const int slot = static_cast<int>(g % NS);
-          if (g >= NS) mbar_wait(&empty[slot], static_cast<uint32_t>(((g / NS) - 1) & 1));
+        for (int st = 0; st < it.nst; ++st) {
+          if (wrapped) mbar_wait(&empty[slot], phase ^ 1u);  // previous use released
           const int y0 = it.ya + st * RP;
           const int nr = min(RP, it.yb - y0);
           const uint32_t bytes = static_cast<uint32_t>(nr * a.rowbytes);
@@ -185,6 +188,11 @@ __global__ void __launch_bounds__(kK1MaxThreads, 1) mask_cells_kernel(const Mask
                        &full[slot]);
             }
           }
+          if (++slot == NS) {
+            slot = 0;
+            phase ^= 1u;
+            wrapped = true;
+          }
         }
       }
     }
@@ -197,21 +205,27 @@ __global__ void __launch_bounds__(kK1MaxThreads, 1) mask_cells_kernel(const Mask
       static_cast<uint32_t>(t_low ? a.threshold + 1 : a.threshold - 127) * 0x01010101u;
   const uint32_t lastmask = (a.W & 31) ? ((1u << (a.W & 31)) - 1u) : 0xffffffffu;
   const int ngroups = ceil_div(a.nwords, kK1GroupWords);
-  long long g = 0;  // global stage counter (same sequence as the producer)
+  const int my_slot = warp / G, sub = warp - my_slot * G;
+  // Stages are dealt to slots round-robin; this warp group owns every NS-th
+  // stage.  first_st: this group's first stage within the current item;
+  // phase: parity of its slot's next use.
+  int first_st = my_slot;
+  uint32_t phase = 0;
   for (int item = blockIdx.x; item < a.total_items; item += gridDim.x) {
     const Item it = load_item(a, item);
-    // ---- raw foreground words: this warp's stages of the item ----
-    for (int st = 0; st < it.nst; ++st, ++g) {
-      const int slot = static_cast<int>(g % NS);
-      if (slot != warp) continue;  // stage g belongs to the warp owning its slot
-      mbar_wait(&full[slot], static_cast<uint32_t>((g / NS) & 1));
+    // ---- raw foreground words: this group's stages of the item ----
+    int st = first_st;
+    for (; st < it.nst; st += NS) {
+      const int slot = my_slot;
+      mbar_wait(&full[slot], phase);
+      phase ^= 1u;
       const int y0 = it.ya + st * RP;
       const int nr = min(RP, it.yb - y0);
       const uint8_t* sc = slots + slot * slot_bytes;
       const uint8_t* sp = sc + RP * a.rowbytes;
       for (int k = 0; k < nr; ++k) {
         uint32_t* frow = F + (y0 + k - it.ya) * a.nwords;
-        for (int w = lane; w < a.nwords; w += 32) {
+        for (int w = sub * 32 + lane; w < a.nwords; w += 32 * G) {
           const int off = 96 * w;
           const int nbytes = min(96, a.rowbytes - off);
           const uint8_t* cw = sc + k * a.rowbytes + off;
@@ -224,6 +238,7 @@ __global__ void __launch_bounds__(kK1MaxThreads, 1) mask_cells_kernel(const Mask
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);  // slot may be refilled
     }
+    first_st = st - it.nst;  // stages continue into the next item
     consumer_bar(ncw * 32);  // bitmap of the item complete
 
     // ---- dilation + cell summaries, one (16-row band, 30-word group) task
@@ -332,6 +347,12 @@ cudaError_t launch_mask_cells(const uint8_t* const* d_cur, const uint8_t* const*
     return cudaErrorInvalidConfiguration;
   a.rows_per_stage = mp.rows_per_stage;
   a.nstages = mp.nstages;
+  // consumer warps per slot: enough lanes for a stage's words, within the
+  // thread budget
+  int G = std::min(4, std::max(1, ceil_div(a.nwords, 32)));
+  if (const char* gs = std::getenv("TG_K1_GROUP")) G = std::max(1, std::atoi(gs));
+  while (G > 1 && (mp.nstages * G + 1) * 32 > kK1MaxThreads) --G;
+  a.group = G;
   a.seg_rows = mp.seg_rows;
   a.nseg = ceil_div(H, a.seg_rows);
   a.total_items = a.nseg * n_frames;
@@ -344,7 +365,7 @@ cudaError_t launch_mask_cells(const uint8_t* const* d_cur, const uint8_t* const*
   if (e != cudaSuccess) return e;
   int grid = std::min(a.total_items, sms);
   if (const char* g = std::getenv("TG_K1_GRID")) grid = std::max(1, std::min(a.total_items, std::atoi(g)));
-  mask_cells_kernel<<<grid, (mp.nstages + 1) * 32, mp.smem, stream>>>(a);
+  mask_cells_kernel<<<grid, (mp.nstages * a.group + 1) * 32, mp.smem, stream>>>(a);
   return cudaGetLastError();
 }
 
