@@ -310,6 +310,7 @@ static MaskPlan plan_mask(int W, int radius) {
   const size_t slot = static_cast<size_t>(2) * p.rows_per_stage * rowbytes;
   const size_t fixed = static_cast<size_t>(kK1MaxBands) * kK1MaxActWords * 4 + 2 * 8 * 8 + 128;
   p.nstages = kK1MaxSlots;
+  if (const char* e = std::getenv("TG_K1_SLOTS")) p.nstages = std::max(2, std::min(kK1MaxSlots, std::atoi(e)));
   p.seg_rows = kK1MaxSeg;
   auto total = [&](int ns, int seg) {
     return fixed + ns * slot + static_cast<size_t>(seg + 2 * radius) * nwords * 4;
