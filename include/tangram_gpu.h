@@ -244,6 +244,81 @@ tg_status tg_pipeline_download(tg_pipeline* p, int32_t n_frames, void* stream,
 tg_status tg_pipeline_free_rects(tg_pipeline* p, int32_t frame, tg_free_rect* out, int32_t cap,
                                  int32_t* n_out);
 
+/* ---- generic canvas writer ----------------------------------------------
+ * K5 on an explicit plan: canvas k is tiled by jobs[canvas_job_offsets[k] ..
+ * canvas_job_offsets[k+1]) (placements: src_frame >= 0 indexes d_frames;
+ * free rects: src_frame = -1, zero fill).  The jobs of a canvas must tile it
+ * exactly (placements + final free rects of a stitch result).  Host arrays
+ * are staged and launched on `stream`; returns before the copy completes. */
+typedef struct {
+  tg_rect dst;        /* canvas rect */
+  int32_t src_frame;  /* index into d_frames, -1 = zeros */
+  int32_t src_x, src_y;
+} tg_gather_job;
+tg_status tg_stitch_gather(tg_ctx* ctx, const tg_gather_job* jobs, int32_t n_jobs,
+                           const int32_t* canvas_job_offsets, int32_t n_canvases,
+                           tg_canvas_spec spec, const uint8_t* const* d_frames, int32_t pitch,
+                           uint8_t* d_canvases, void* stream);
+
+/* ---- SLO-aware batcher (scheduler.hpp:79-215, Alg. 2 invoker) ------------
+ * Host state machine over patch descriptors, identical in decisions, timer
+ * epochs, triggers and stitch results to the reference SloScheduler, with an
+ * incremental repack: stitch_all is prefix-consistent, so a tentative arrival
+ * is one BSSF placement on the current state (O(free rects)) instead of a
+ * full repack of the queue (O(queue x free rects)).  Each event's canvases
+ * can be materialized on the device with tg_batcher_gather. */
+typedef struct { int32_t batch_size; double mu_ms, sigma_ms; } tg_profile_entry; /* latency.hpp:33-37 */
+typedef enum { TG_TRIGGER_DEADLINE_TIMER = 0, TG_TRIGGER_INFEASIBLE_ARRIVAL = 1,
+               TG_TRIGGER_MEMORY_CAP = 2 } tg_trigger;                            /* scheduler.hpp:29-33 */
+typedef struct {
+  int64_t fire_time_us;
+  int32_t batch_size;          /* canvases */
+  int32_t trigger;             /* tg_trigger */
+  int64_t estimated_slack_us;
+  int32_t n_patches;           /* patch ids in queue order */
+  int32_t n_free;              /* free rects over all canvases */
+} tg_invoke_info;
+typedef struct tg_batcher tg_batcher;
+
+/* slack_us(k) = ms_to_us(mu_k + 3 sigma_k), interpolated (latency.hpp:78-118) */
+tg_status tg_profile_slack_us(const tg_profile_entry* entries, int32_t n, int32_t k,
+                              int64_t* slack_us);
+/* cost.hpp:107-115 */
+tg_status tg_max_canvases_per_batch(double gpu_memory_gb, double model_size_gb,
+                                    double vram_per_canvas_gb, int32_t* k);
+/* trace.hpp:247-267: per-link FIFO arrival times, patches in generation order */
+tg_status tg_transmission_schedule(const tg_patch_meta* patches, int32_t n, double bandwidth_mbps,
+                                   int64_t* arrival_us);
+
+tg_status tg_batcher_create(tg_canvas_spec spec, const tg_profile_entry* entries, int32_t n_entries,
+                            int32_t max_canvases, tg_batcher** out);
+void tg_batcher_destroy(tg_batcher* b);
+/* on_patch_arrival (scheduler.hpp:90-126).  src_frame tags the patch's pixels
+ * for tg_batcher_gather.  *n_events (0..2) events become readable through
+ * tg_batcher_event(b, 0..n-1) until the next call. */
+tg_status tg_batcher_on_patch_arrival(tg_batcher* b, const tg_patch_meta* patch, int32_t src_frame,
+                                      int64_t now_us, int32_t* n_events);
+/* on_timer (scheduler.hpp:130-135); stale epochs produce no event. */
+tg_status tg_batcher_on_timer(tg_batcher* b, int64_t now_us, uint64_t epoch, int32_t* n_events);
+tg_status tg_batcher_pending_timer(tg_batcher* b, int32_t* has_timer, int64_t* fire_at_us,
+                                   uint64_t* epoch);
+tg_status tg_batcher_status(tg_batcher* b, int32_t* queue_len, int32_t* canvases,
+                            int64_t* earliest_deadline_us, int64_t* remaining_time_us);
+/* Event i of the last call: patch ids (queue order), placements (canvas-major,
+ * placement order), free rects (canvas-major, reference list order); arrays
+ * may be NULL. */
+tg_status tg_batcher_event(tg_batcher* b, int32_t i, tg_invoke_info* info, uint64_t* patch_ids,
+                           tg_placement* placements, tg_free_rect* free_rects);
+/* Writes event i's canvases: d_frames[src_frame] holds each patch's frame. */
+tg_status tg_batcher_gather(tg_ctx* ctx, tg_batcher* b, int32_t i, const uint8_t* const* d_frames,
+                            int32_t pitch, uint8_t* d_canvases, void* stream);
+/* Offline driver of the reference event loop for the tangram policy
+ * (sim.hpp:334-342, 425-458): arrivals ordered by (arrival_us, input order),
+ * a timer is queued when its epoch is new and loses ties to arrivals.  All
+ * events are kept; *n_events is their count (tg_batcher_event reads them). */
+tg_status tg_batcher_replay(tg_batcher* b, const tg_patch_meta* patches, const int32_t* src_frames,
+                            const int64_t* arrival_us, int32_t n, int32_t* n_events);
+
 /* ---- synthetic workload (fixture source; not part of the timed path) -----
  * trace.hpp:145-231 generate_trace, restated (std::mt19937_64 + the
  * reference's hand-rolled distributions).  Writes t_us[n_frames],

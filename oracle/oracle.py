@@ -339,3 +339,127 @@ def process_frames(params: dict, cur_frames, prev_frames, frame_ids, gen_us, fir
          for pl in (res["placements"][f * nz + k] for k in range(res["n_placements"][f]))]
         for f in range(n)]
     return res
+
+
+# ------------------------------------------------------ reference scheduler
+class SimCfg(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("zones_x", C.c_int32),
+                ("zones_y", C.c_int32), ("canvas_w", C.c_int32), ("canvas_h", C.c_int32),
+                ("per_scene_link", C.c_int32), ("vram_per_canvas_gb", C.c_double),
+                ("gpu_memory_gb", C.c_double), ("model_size_gb", C.c_double),
+                ("bandwidth_mbps", C.c_double), ("bytes_per_pixel", C.c_double),
+                ("slo_us", C.c_int64)]
+
+
+def _profile_arr(entries):
+    flat = [float(v) for e in entries for v in e]
+    return (C.c_double * max(1, len(flat)))(*flat), len(entries)
+
+
+def run_tangram(scenes, width, height, profile, zones=(4, 4), canvas=(1024, 1024),
+                vram_per_canvas_gb=1.0, gpu_memory_gb=6.0, model_size_gb=2.0, bandwidth_mbps=80.0,
+                per_scene_link=True, bytes_per_pixel=1.5, slo_us=1_000_000):
+    """The reference's tangram::run() (sim.hpp:206-552, tangram policy) on
+    scenes = [(t_us list, per-frame rect lists)].  Returns per-patch
+    (admitted, arrival_us) and the scheduler's invoke events from its log."""
+    dll = load("ref")
+    dll.ref_run_tangram.restype = C.c_int
+    cfg = SimCfg(width, height, zones[0], zones[1], canvas[0], canvas[1], int(per_scene_link),
+                 vram_per_canvas_gb, gpu_memory_gb, model_size_gb, bandwidth_mbps, bytes_per_pixel,
+                 slo_us)
+    fps = (C.c_int32 * len(scenes))(*[len(t) for t, _ in scenes])
+    t_flat = [t for ts, _ in scenes for t in ts]
+    cnt = [len(f) for _, fr in scenes for f in fr]
+    rects = [r for _, fr in scenes for f in fr for r in f]
+    t_arr = (C.c_int64 * max(1, len(t_flat)))(*t_flat)
+    c_arr = (C.c_int32 * max(1, len(cnt)))(*cnt)
+    r_arr = (Rect * max(1, len(rects)))(*[Rect(*r) for r in rects])
+    prof, n_prof = _profile_arr(profile)
+    pcap = max(1, len(t_flat) * zones[0] * zones[1])
+    arrival = (C.c_int64 * pcap)()
+    adm = (C.c_uint8 * pcap)()
+    npatch = C.c_int32()
+    ecap, icap = pcap, pcap
+    ev_fire = (C.c_int64 * ecap)()
+    ev_trig = (C.c_int32 * ecap)()
+    ev_k = (C.c_int32 * ecap)()
+    ev_slack = (C.c_int64 * ecap)()
+    ev_np = (C.c_int32 * ecap)()
+    ev_ids = (C.c_uint64 * icap)()
+    nev = C.c_int32()
+    rc = dll.ref_run_tangram(C.byref(cfg), len(scenes), fps, t_arr, c_arr, r_arr, prof, n_prof,
+                             arrival, adm, C.byref(npatch), C.c_int64(pcap), C.byref(nev), ev_fire,
+                             ev_trig, ev_k, ev_slack, ev_np, ev_ids, C.c_int64(ecap),
+                             C.c_int64(icap))
+    if rc:
+        raise OracleError(_err(dll, "ref"))
+    events, k = [], 0
+    for i in range(nev.value):
+        ids = [ev_ids[k + j] for j in range(ev_np[i])]
+        k += ev_np[i]
+        events.append(dict(fire_time_us=ev_fire[i], trigger=ev_trig[i], batch_size=ev_k[i],
+                           estimated_slack_us=ev_slack[i], patch_ids=ids))
+    return dict(admitted=[adm[i] for i in range(npatch.value)],
+                arrival_us=[arrival[i] for i in range(npatch.value)], events=events)
+
+
+class RefScheduler:
+    """The reference SloScheduler (scheduler.hpp:79-215), call by call."""
+
+    def __init__(self, canvas_w, canvas_h, profile, max_canvases):
+        self.dll = dll = load("ref")
+        dll.ref_sched_create.restype = C.c_void_p
+        dll.ref_sched_create.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int]
+        for n in ("ref_sched_arrival", "ref_sched_timer", "ref_sched_pending", "ref_sched_event"):
+            getattr(dll, n).restype = C.c_int
+        dll.ref_sched_arrival.argtypes = [C.c_void_p, C.POINTER(Patch), C.c_int64]
+        dll.ref_sched_timer.argtypes = [C.c_void_p, C.c_int64, C.c_uint64]
+        dll.ref_sched_pending.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_uint64)]
+        dll.ref_sched_destroy.argtypes = [C.c_void_p]
+        prof, n = _profile_arr(profile)
+        self.h = dll.ref_sched_create(canvas_w, canvas_h, prof, n, max_canvases)
+        if not self.h:
+            raise OracleError(_err(dll, "ref"))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.dll.ref_sched_destroy(self.h)
+
+    def _events(self, n):
+        out = []
+        for i in range(n):
+            fire, slack = C.c_int64(), C.c_int64()
+            trig, k, nid, nf = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+            ids = (C.c_uint64 * 4096)()
+            pl = (Placement * 4096)()
+            fr = (FreeRect * 8192)()
+            self.dll.ref_sched_event(C.c_void_p(self.h), i, C.byref(fire), C.byref(trig), C.byref(k),
+                                     C.byref(slack), C.byref(nid), ids, pl, C.byref(nf), fr)
+            out.append(dict(
+                fire_time_us=fire.value, trigger=trig.value, batch_size=k.value,
+                estimated_slack_us=slack.value, patch_ids=[ids[j] for j in range(nid.value)],
+                placements=[(pl[j].patch_id, pl[j].canvas_index, pl[j].position.x, pl[j].position.y,
+                             pl[j].position.w, pl[j].position.h) for j in range(nid.value)],
+                free=[(fr[j].canvas, fr[j].r.x, fr[j].r.y, fr[j].r.w, fr[j].r.h)
+                      for j in range(nf.value)]))
+        return out
+
+    def on_patch_arrival(self, patch: dict, now: int):
+        p = Patch(patch["patch_id"], patch.get("source_frame_id", 0), Rect(*patch["rect"]),
+                  patch["generation_time_us"], patch["slo_us"], patch["deadline_us"],
+                  patch.get("size_bytes", 0))
+        n = self.dll.ref_sched_arrival(C.c_void_p(self.h), C.byref(p), now)
+        if n < 0:
+            raise OracleError(_err(self.dll, "ref"))
+        return self._events(n)
+
+    def on_timer(self, now: int, epoch: int):
+        n = self.dll.ref_sched_timer(C.c_void_p(self.h), now, epoch)
+        ev = self._events(n)
+        return ev[0] if ev else None
+
+    def pending_timer(self):
+        at, ep = C.c_int64(), C.c_uint64()
+        if self.dll.ref_sched_pending(C.c_void_p(self.h), C.byref(at), C.byref(ep)):
+            return at.value, ep.value
+        return None

@@ -8,12 +8,16 @@
 // into oracle/_ref/libtangram_ref.so; nothing in the product links it.
 #include <cstring>
 #include <exception>
+#include <memory>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "tangram/partition.hpp"
 #include "tangram/rng.hpp"
+#include "tangram/scheduler.hpp"
+#include "tangram/sim.hpp"
 #include "tangram/stitch.hpp"
 #include "tangram/trace.hpp"
 
@@ -179,6 +183,180 @@ int ref_stitch_all(const orc_patch* queue, int n, int M, int N, orc_placement* p
   } catch (const std::exception& e) {
     return fail(e);
   }
+}
+
+// ---- the reference's own simulator, tangram policy (sim.hpp:206-552) ------
+// Runs tangram::run() on the given scenes and returns, from its event log,
+// every invoke the SloScheduler made plus each patch's admission and arrival
+// time from RunMetrics -- the parity target for the device batcher.
+typedef struct {
+  int32_t width, height, zones_x, zones_y, canvas_w, canvas_h, per_scene_link;
+  double vram_per_canvas_gb, gpu_memory_gb, model_size_gb, bandwidth_mbps, bytes_per_pixel;
+  int64_t slo_us;
+} ref_sim_cfg;
+
+int ref_run_tangram(const ref_sim_cfg* c, int n_scenes, const int32_t* frames_per_scene,
+                    const int64_t* t_us, const int32_t* roi_counts, const orc_rect* rois,
+                    const double* profile, int n_profile, int64_t* arrival_us, uint8_t* admitted,
+                    int32_t* n_patches, int64_t patch_cap, int32_t* n_events, int64_t* ev_fire,
+                    int32_t* ev_trigger, int32_t* ev_k, int64_t* ev_slack, int32_t* ev_npatch,
+                    uint64_t* ev_ids, int64_t ev_cap, int64_t ids_cap) {
+  try {
+    std::vector<tangram::TraceScene> scenes;
+    int64_t fi = 0, ri = 0;
+    for (int s = 0; s < n_scenes; ++s) {
+      tangram::TraceScene sc;
+      sc.scene_id = "cam" + std::to_string(s);
+      for (int f = 0; f < frames_per_scene[s]; ++f, ++fi) {
+        tangram::TraceFrame tf;
+        tf.frame_id = static_cast<uint64_t>(f);
+        tf.t_us = t_us[fi];
+        tf.width = c->width;
+        tf.height = c->height;
+        for (int k = 0; k < roi_counts[fi]; ++k, ++ri) tf.rois.push_back(to_rect(rois[ri]));
+        sc.frames.push_back(std::move(tf));
+      }
+      scenes.push_back(std::move(sc));
+    }
+    tangram::SimConfig cfg;
+    cfg.partition = tangram::PartitionConfig{c->zones_x, c->zones_y};
+    cfg.canvas.width = c->canvas_w;
+    cfg.canvas.height = c->canvas_h;
+    cfg.canvas.vram_per_canvas_gb = c->vram_per_canvas_gb;
+    cfg.function.gpu_memory_gb = c->gpu_memory_gb;
+    cfg.function.model_size_gb = c->model_size_gb;
+    cfg.link.bandwidth_mbps = c->bandwidth_mbps;
+    cfg.link.bytes_per_pixel = c->bytes_per_pixel;
+    cfg.link.per_scene = c->per_scene_link != 0;
+    cfg.policy = tangram::Policy::tangram;
+    cfg.slo_us = c->slo_us;
+    std::vector<tangram::ProfileEntry> entries;
+    for (int i = 0; i < n_profile; ++i)
+      entries.push_back(tangram::ProfileEntry{static_cast<int>(profile[3 * i]), profile[3 * i + 1],
+                                              profile[3 * i + 2]});
+    const auto prof = tangram::LatencyProfile::from_entries(c->canvas_w, c->canvas_h, entries);
+    std::ostringstream log_text;
+    tangram::EventLog log(&log_text, "tangram");
+    const tangram::RunMetrics m = tangram::run(scenes, cfg, prof, &log);
+    if (static_cast<int64_t>(m.patches.size()) > patch_cap) throw std::length_error("patch cap");
+    for (std::size_t i = 0; i < m.patches.size(); ++i) {
+      admitted[i] = m.patches[i].admitted ? 1 : 0;
+      arrival_us[i] = m.patches[i].admitted ? m.patches[i].arrival_us : -1;
+    }
+    *n_patches = static_cast<int32_t>(m.patches.size());
+    std::istringstream in(log_text.str());
+    std::string line;
+    int64_t ne = 0, nid = 0;
+    while (std::getline(in, line)) {
+      const auto j = nlohmann::json::parse(line);
+      if (j.at("event").get<std::string>() != "invoke") continue;
+      if (ne >= ev_cap) throw std::length_error("event cap");
+      ev_fire[ne] = j.at("t_us").get<int64_t>();
+      const std::string trig = j.at("trigger").get<std::string>();
+      ev_trigger[ne] = trig == "deadline_timer" ? 0 : trig == "infeasible_arrival" ? 1 : 2;
+      ev_k[ne] = j.at("k").get<int32_t>();
+      ev_slack[ne] = j.at("slack_us").get<int64_t>();
+      const auto ids = j.at("patches");
+      ev_npatch[ne] = static_cast<int32_t>(ids.size());
+      for (const auto& id : ids) {
+        if (nid >= ids_cap) throw std::length_error("ids cap");
+        ev_ids[nid++] = id.get<uint64_t>();
+      }
+      ++ne;
+    }
+    *n_events = static_cast<int32_t>(ne);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// The reference SloScheduler driven call by call (scheduler_test.cpp style).
+struct RefSched {
+  tangram::LatencyProfile prof;
+  std::unique_ptr<tangram::SloScheduler> s;
+  std::vector<tangram::InvokeEvent> events;
+};
+
+void* ref_sched_create(int canvas_w, int canvas_h, const double* profile, int n_profile,
+                       int max_canvases) {
+  try {
+    std::vector<tangram::ProfileEntry> entries;
+    for (int i = 0; i < n_profile; ++i)
+      entries.push_back(tangram::ProfileEntry{static_cast<int>(profile[3 * i]), profile[3 * i + 1],
+                                              profile[3 * i + 2]});
+    auto* r = new RefSched{tangram::LatencyProfile::from_entries(canvas_w, canvas_h, entries), {}, {}};
+    tangram::CanvasSpec spec;
+    spec.width = canvas_w;
+    spec.height = canvas_h;
+    r->s = std::make_unique<tangram::SloScheduler>(spec, &r->prof, max_canvases);
+    return r;
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
+void ref_sched_destroy(void* h) { delete static_cast<RefSched*>(h); }
+
+int ref_sched_arrival(void* h, const orc_patch* p, int64_t now) {
+  auto* r = static_cast<RefSched*>(h);
+  try {
+    tangram::PatchMeta m;
+    m.patch_id = p->patch_id;
+    m.source_frame_id = p->source_frame_id;
+    m.rect = to_rect(p->rect);
+    m.generation_time_us = p->generation_time_us;
+    m.slo_us = p->slo_us;
+    m.deadline_us = p->deadline_us;
+    m.size_bytes = p->size_bytes;
+    r->events = r->s->on_patch_arrival(m, now);
+    return static_cast<int>(r->events.size());
+  } catch (const std::exception& e) {
+    fail(e);
+    return -1;
+  }
+}
+
+int ref_sched_timer(void* h, int64_t now, uint64_t epoch) {
+  auto* r = static_cast<RefSched*>(h);
+  r->events.clear();
+  if (auto ev = r->s->on_timer(now, epoch)) r->events.push_back(std::move(*ev));
+  return static_cast<int>(r->events.size());
+}
+
+int ref_sched_pending(void* h, int64_t* at, uint64_t* epoch) {
+  auto* r = static_cast<RefSched*>(h);
+  const auto t = r->s->pending_timer();
+  if (!t) return 0;
+  *at = t->fire_at_us;
+  *epoch = t->epoch;
+  return 1;
+}
+
+// Event i: header fields, ids (queue order), placements canvas-major in
+// placement order, free rects canvas-major in list order.
+int ref_sched_event(void* h, int i, int64_t* fire, int32_t* trigger, int32_t* k, int64_t* slack,
+                    int32_t* n_ids, uint64_t* ids, orc_placement* placements, int32_t* n_free,
+                    orc_free_rect* free_out) {
+  auto* r = static_cast<RefSched*>(h);
+  if (i < 0 || i >= static_cast<int>(r->events.size())) return -1;
+  const auto& e = r->events[static_cast<std::size_t>(i)];
+  *fire = e.fire_time_us;
+  *trigger = static_cast<int32_t>(e.trigger);
+  *k = e.batch_size;
+  *slack = e.estimated_slack_us;
+  *n_ids = static_cast<int32_t>(e.patch_ids.size());
+  for (std::size_t j = 0; j < e.patch_ids.size(); ++j) ids[j] = e.patch_ids[j];
+  int np = 0, nf = 0;
+  for (std::size_t c = 0; c < e.stitch.canvases.size(); ++c) {
+    for (const auto& p : e.stitch.canvases[c].placements)
+      placements[np++] = orc_placement{p.patch_id, p.canvas_index, from_rect(p.position), 0};
+    for (const auto& fr : e.stitch.canvases[c].free_rects)
+      free_out[nf++] = orc_free_rect{from_rect(fr), static_cast<int32_t>(c)};
+  }
+  *n_free = nf;
+  return 0;
 }
 
 // The reference CPU implementation of the whole per-frame path: the pixel

@@ -79,6 +79,21 @@ class tg_workload_config(C.Structure):
                 ("roi_aspect_max", C.c_double), ("roi_max_dim", C.c_int32), ("seed", C.c_uint64)]
 
 
+class tg_gather_job(C.Structure):
+    _fields_ = [("dst", tg_rect), ("src_frame", C.c_int32), ("src_x", C.c_int32),
+                ("src_y", C.c_int32)]
+
+
+class tg_profile_entry(C.Structure):
+    _fields_ = [("batch_size", C.c_int32), ("mu_ms", C.c_double), ("sigma_ms", C.c_double)]
+
+
+class tg_invoke_info(C.Structure):
+    _fields_ = [("fire_time_us", C.c_int64), ("batch_size", C.c_int32), ("trigger", C.c_int32),
+                ("estimated_slack_us", C.c_int64), ("n_patches", C.c_int32),
+                ("n_free", C.c_int32)]
+
+
 P = C.POINTER
 vp = C.c_void_p
 i32 = C.c_int32
@@ -131,6 +146,21 @@ SIGNATURES = {
     "tg_pipeline_device_views": (st, [vp, P(tg_pipeline_views)]),
     "tg_pipeline_download": (st, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, P(i64)]),
     "tg_pipeline_free_rects": (st, [vp, i32, P(tg_free_rect), i32, P(i32)]),
+    "tg_stitch_gather": (st, [vp, P(tg_gather_job), i32, P(i32), i32, tg_canvas_spec, vp, i32, vp,
+                              vp]),
+    "tg_profile_slack_us": (st, [P(tg_profile_entry), i32, i32, P(i64)]),
+    "tg_max_canvases_per_batch": (st, [C.c_double, C.c_double, C.c_double, P(i32)]),
+    "tg_transmission_schedule": (st, [P(tg_patch_meta), i32, C.c_double, P(i64)]),
+    "tg_batcher_create": (st, [tg_canvas_spec, P(tg_profile_entry), i32, i32, P(vp)]),
+    "tg_batcher_destroy": (None, [vp]),
+    "tg_batcher_on_patch_arrival": (st, [vp, P(tg_patch_meta), i32, i64, P(i32)]),
+    "tg_batcher_on_timer": (st, [vp, i64, u64, P(i32)]),
+    "tg_batcher_pending_timer": (st, [vp, P(i32), P(i64), P(u64)]),
+    "tg_batcher_status": (st, [vp, P(i32), P(i32), P(i64), P(i64)]),
+    "tg_batcher_event": (st, [vp, i32, P(tg_invoke_info), P(u64), P(tg_placement),
+                              P(tg_free_rect)]),
+    "tg_batcher_gather": (st, [vp, vp, i32, vp, i32, vp, vp]),
+    "tg_batcher_replay": (st, [vp, P(tg_patch_meta), P(i32), P(i64), i32, P(i32)]),
     "tg_workload_default": (st, [P(tg_workload_config)]),
     "tg_derive_seed": (u64, [u64, C.c_char_p]),
     "tg_generate_trace": (st, [P(tg_workload_config), P(i64), P(i32), P(tg_rect), i64, P(i64)]),

@@ -586,3 +586,165 @@ class Graph:
         if self.handle:
             N.lib().tg_graph_destroy(self.handle)
             self.handle = None
+
+
+# ------------------------------------------------------------- SLO batcher
+_TRIGGERS = {0: "deadline_timer", 1: "infeasible_arrival", 2: "memory_cap"}
+
+
+@dataclass
+class InvokeEvent:
+    """scheduler.hpp:46-53."""
+    fire_time_us: int = 0
+    stitch: StitchResult = field(default_factory=StitchResult)
+    patch_ids: list = field(default_factory=list)
+    batch_size: int = 0
+    estimated_slack_us: int = 0
+    trigger: str = "deadline_timer"
+
+
+@dataclass
+class TimerHandle:
+    fire_at_us: int = 0
+    epoch: int = 0
+
+
+class LatencyProfile:
+    """latency.hpp:44-118 (slack = mu + 3 sigma, interpolated)."""
+
+    def __init__(self, canvas_w: int, canvas_h: int, entries):
+        self.canvas_w, self.canvas_h = canvas_w, canvas_h
+        self.entries = [tuple(e) for e in entries]
+        self._arr = (N.tg_profile_entry * max(1, len(self.entries)))(
+            *[N.tg_profile_entry(int(k), float(mu), float(sd)) for k, mu, sd in self.entries])
+        self.slack_us(1)  # validates like LatencyProfile::from_entries
+
+    @classmethod
+    def from_entries(cls, canvas_w, canvas_h, entries):
+        return cls(canvas_w, canvas_h, entries)
+
+    def slack_us(self, k: int) -> int:
+        out = C.c_int64()
+        check(N.lib().tg_profile_slack_us(self._arr, len(self.entries), k, C.byref(out)))
+        return out.value
+
+
+def max_canvases_per_batch(gpu_memory_gb: float, model_size_gb: float,
+                           vram_per_canvas_gb: float) -> int:
+    """cost.hpp:107-115."""
+    k = C.c_int32()
+    check(N.lib().tg_max_canvases_per_batch(gpu_memory_gb, model_size_gb, vram_per_canvas_gb,
+                                            C.byref(k)))
+    return k.value
+
+
+def transmission_schedule(patches: Sequence[PatchMeta], bandwidth_mbps: float) -> list[int]:
+    """trace.hpp:255-267 (per-link FIFO)."""
+    n = len(patches)
+    arr = (N.tg_patch_meta * max(1, n))(*[_c_patch(p) for p in patches])
+    out = (C.c_int64 * max(1, n))()
+    check(N.lib().tg_transmission_schedule(arr, n, float(bandwidth_mbps), out))
+    return [out[i] for i in range(n)]
+
+
+class SloScheduler:
+    """The Alg. 2 invoker (scheduler.hpp:79-215) with an incremental repack;
+    decisions, epochs and stitch results equal the reference's."""
+
+    def __init__(self, spec: CanvasSpec, profile: LatencyProfile, max_canvases: int):
+        if profile is None:
+            raise InvalidArgument("scheduler needs a latency profile")
+        self.spec = spec
+        h = C.c_void_p()
+        check(N.lib().tg_batcher_create(
+            N.tg_canvas_spec(spec.width, spec.height, spec.vram_per_canvas_gb), profile._arr,
+            len(profile.entries), max_canvases, C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            N.lib().tg_batcher_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _events(self, n: int) -> list[InvokeEvent]:
+        out = []
+        for i in range(n):
+            info = N.tg_invoke_info()
+            check(N.lib().tg_batcher_event(self.handle, i, C.byref(info), None, None, None))
+            ids = (C.c_uint64 * max(1, info.n_patches))()
+            pl = (N.tg_placement * max(1, info.n_patches))()
+            fr = (N.tg_free_rect * max(1, info.n_free))()
+            check(N.lib().tg_batcher_event(self.handle, i, None, ids, pl, fr))
+            res = StitchResult(spec=self.spec, canvases=[CanvasState() for _ in range(info.batch_size)])
+            for k in range(info.n_patches):
+                p = Placement(pl[k].patch_id, pl[k].canvas_index, _py_rect(pl[k].position))
+                cs = res.canvases[p.canvas_index]
+                cs.placements.append(p)
+                cs.used_area += area(p.position)
+                res.placement_index[p.patch_id] = p
+            for k in range(info.n_free):
+                res.canvases[fr[k].canvas_index].free_rects.append(_py_rect(fr[k].rect))
+            out.append(InvokeEvent(info.fire_time_us, res, [ids[k] for k in range(info.n_patches)],
+                                   info.batch_size, info.estimated_slack_us,
+                                   _TRIGGERS[info.trigger]))
+        return out
+
+    def on_patch_arrival(self, patch: PatchMeta, now: int, src_frame: int = -1):
+        n = C.c_int32()
+        check(N.lib().tg_batcher_on_patch_arrival(self.handle, C.byref(_c_patch(patch)), src_frame,
+                                                  now, C.byref(n)))
+        return self._events(n.value)
+
+    def on_timer(self, now: int, epoch: int):
+        n = C.c_int32()
+        check(N.lib().tg_batcher_on_timer(self.handle, now, epoch, C.byref(n)))
+        ev = self._events(n.value)
+        return ev[0] if ev else None
+
+    def pending_timer(self):
+        has, at, ep = C.c_int32(), C.c_int64(), C.c_uint64()
+        check(N.lib().tg_batcher_pending_timer(self.handle, C.byref(has), C.byref(at), C.byref(ep)))
+        return TimerHandle(at.value, ep.value) if has.value else None
+
+    def _status(self):
+        q, c, d, r = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()
+        check(N.lib().tg_batcher_status(self.handle, C.byref(q), C.byref(c), C.byref(d), C.byref(r)))
+        return q.value, c.value, d.value, r.value
+
+    def idle(self) -> bool:
+        return self._status()[0] == 0
+
+    def queue_size(self) -> int:
+        return self._status()[0]
+
+    def current_canvas_count(self) -> int:
+        return self._status()[1]
+
+    def earliest_deadline_us(self) -> int:
+        return self._status()[2]
+
+    def remaining_time_us(self) -> int:
+        return self._status()[3]
+
+    def replay(self, patches: Sequence[PatchMeta], arrival_us: Sequence[int],
+               src_frames: Sequence[int] | None = None) -> list[InvokeEvent]:
+        """The reference event loop for the tangram policy (sim.hpp:334-458)."""
+        n = len(patches)
+        arr = (N.tg_patch_meta * max(1, n))(*[_c_patch(p) for p in patches])
+        arv = (C.c_int64 * max(1, n))(*arrival_us)
+        src = (C.c_int32 * max(1, n))(*(src_frames if src_frames is not None else [-1] * n))
+        cnt = C.c_int32()
+        check(N.lib().tg_batcher_replay(self.handle, arr, src, arv, n, C.byref(cnt)))
+        return self._events(cnt.value)
+
+    def gather(self, ctx: Context, event_index: int, d_frames: int, pitch: int, d_canvases: int,
+               stream=None) -> None:
+        """Writes event `event_index` (of the last call) into d_canvases."""
+        check(N.lib().tg_batcher_gather(ctx.handle, self.handle, event_index, d_frames, pitch,
+                                        d_canvases, stream))

@@ -56,6 +56,12 @@ struct tg_ctx {
   // grow-only scratch for the blocking drop-in calls
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
+  // stream-ordered staging for explicit gather plans (tg_stitch_gather,
+  // tg_batcher_gather)
+  Job* g_jobs = nullptr;
+  uint2* g_ranges = nullptr;
+  int32_t* g_units = nullptr;
+  size_t g_job_cap = 0, g_range_cap = 0;
 };
 
 struct tg_pipeline {
@@ -71,7 +77,7 @@ struct tg_pipeline {
   int64_t* canvas_base = nullptr;
   Job* jobs = nullptr;
   uint32_t* canvas_jobs = nullptr;
-  uint32_t* canvas_map = nullptr;
+  uint2* ranges = nullptr;
   int32_t* gather_units = nullptr;
   uint64_t* id_state = nullptr;
   int last_frames = 0;
@@ -162,6 +168,55 @@ extern "C" {
 
 int tg_abi_version(void) { return TG_ABI_VERSION; }
 
+// ---- internal hooks for batcher.cu (not part of the public header) ---------
+void tg_internal_set_error(const char* msg) { g_err = msg; }
+
+// Uploads an explicit gather plan (host Job[] + per-canvas ranges) on the
+// stream and launches K5 over it.  Pageable host sources: cudaMemcpyAsync
+// returns once they are consumed, so callers may free them immediately.
+tg_status tg_internal_run_gather(tg_ctx* ctx, const void* jobs, int32_t n_jobs, const void* ranges,
+                                 int32_t n_canvases, tg_canvas_spec spec,
+                                 const uint8_t* const* d_frames, int32_t pitch, uint8_t* d_out,
+                                 void* stream) {
+  tg_status s = use_device(ctx);
+  if (s) return s;
+  if (n_canvases == 0) return TG_OK;
+  if (!d_out || !d_frames) return fail(TG_ERR_INVALID_ARGUMENT, "null frame table or canvas buffer");
+  cudaStream_t st = pick(ctx, stream);
+  if (static_cast<size_t>(n_jobs) > ctx->g_job_cap) {
+    TG_CUDA(cudaStreamSynchronize(st));
+    if (ctx->g_jobs) TG_CUDA(cudaFree(ctx->g_jobs));
+    ctx->g_job_cap = std::max<size_t>(n_jobs, 4096);
+    TG_CUDA(cudaMalloc(&ctx->g_jobs, ctx->g_job_cap * sizeof(Job)));
+  }
+  if (static_cast<size_t>(n_canvases) > ctx->g_range_cap) {
+    TG_CUDA(cudaStreamSynchronize(st));
+    if (ctx->g_ranges) TG_CUDA(cudaFree(ctx->g_ranges));
+    ctx->g_range_cap = std::max<size_t>(n_canvases, 1024);
+    TG_CUDA(cudaMalloc(&ctx->g_ranges, ctx->g_range_cap * sizeof(uint2)));
+  }
+  if (!ctx->g_units) TG_CUDA(cudaMalloc(&ctx->g_units, sizeof(int32_t)));
+  const int nbands = gather_bands(spec.height);
+  const int32_t units = n_canvases * nbands;
+  if (n_jobs > 0)
+    TG_CUDA(cudaMemcpyAsync(ctx->g_jobs, jobs, sizeof(Job) * n_jobs, cudaMemcpyHostToDevice, st));
+  TG_CUDA(cudaMemcpyAsync(ctx->g_ranges, ranges, sizeof(uint2) * n_canvases,
+                          cudaMemcpyHostToDevice, st));
+  TG_CUDA(cudaMemcpyAsync(ctx->g_units, &units, sizeof(units), cudaMemcpyHostToDevice, st));
+  GatherArgs g;
+  g.frames = d_frames;
+  g.pitch = pitch;
+  g.M = spec.width;
+  g.N = spec.height;
+  g.nbands = nbands;
+  g.jobs = ctx->g_jobs;
+  g.ranges = ctx->g_ranges;
+  g.units = ctx->g_units;
+  g.out = d_out;
+  TG_CUDA(launch_gather(g, ctx->sms, st));
+  return TG_OK;
+}
+
 const char* tg_last_error(void) { return g_err.c_str(); }
 
 tg_status tg_device_count(int32_t* count) {
@@ -196,6 +251,9 @@ void tg_ctx_destroy(tg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->d_scratch) cudaFree(ctx->d_scratch);
+  if (ctx->g_jobs) cudaFree(ctx->g_jobs);
+  if (ctx->g_ranges) cudaFree(ctx->g_ranges);
+  if (ctx->g_units) cudaFree(ctx->g_units);
   cudaFree(ctx->d_err);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -568,7 +626,7 @@ void tg_pipeline_destroy(tg_pipeline* p) {
   cudaSetDevice(p->ctx->device);
   void* bufs[] = {p->cells, p->active, p->mask, p->n_rois, p->n_patches, p->n_placements,
                   p->n_canvases, p->rois, p->patches, p->admitted, p->placements,
-                  p->canvas_base, p->jobs, p->canvas_jobs, p->canvas_map, p->gather_units,
+                  p->canvas_base, p->jobs, p->canvas_jobs, p->ranges, p->gather_units,
                   p->id_state};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -629,7 +687,7 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
   if (!e) e = alloc(&p->canvas_base, F + 1);
   if (!e) e = alloc(&p->jobs, F * p->job_cap);
   if (!e) e = alloc(&p->canvas_jobs, F * Z);
-  if (!e) e = alloc(&p->canvas_map, static_cast<size_t>(q.max_canvases));
+  if (!e) e = alloc(&p->ranges, static_cast<size_t>(q.max_canvases));
   if (!e) e = alloc(&p->gather_units, 1);
   if (!e) e = alloc(&p->id_state, 1);
   if (!e) e = cudaMemset(p->id_state, 0, sizeof(uint64_t));
@@ -697,6 +755,8 @@ tg_status tg_pipeline_stage_plan(tg_pipeline* p, int32_t n_frames, const uint64_
   ScanArgs sa;
   sa.n_frames = n_frames;
   sa.zones = p->zones;
+  sa.job_cap = p->job_cap;
+  sa.canvas_jobs = p->canvas_jobs;
   sa.first_id = first_patch_id;
   sa.max_canvases = p->p.max_canvases;
   sa.nbands = p->nbands;
@@ -706,7 +766,7 @@ tg_status tg_pipeline_stage_plan(tg_pipeline* p, int32_t n_frames, const uint64_
   sa.patches = p->patches;
   sa.placements = p->placements;
   sa.canvas_base = p->canvas_base;
-  sa.canvas_map = p->canvas_map;
+  sa.ranges = p->ranges;
   sa.gather_units = p->gather_units;
   sa.id_state = p->id_state;
   sa.err = p->ctx->d_err;
@@ -729,12 +789,9 @@ tg_status tg_pipeline_stage_gather(tg_pipeline* p, int32_t n_frames, const uint8
   g.pitch = p->p.pitch;
   g.M = p->p.canvas.width;
   g.N = p->p.canvas.height;
-  g.zones = p->zones;
-  g.job_cap = p->job_cap;
   g.nbands = p->nbands;
   g.jobs = p->jobs;
-  g.canvas_jobs = p->canvas_jobs;
-  g.canvas_map = p->canvas_map;
+  g.ranges = p->ranges;
   g.units = p->gather_units;
   g.out = d_canvases;
   TG_CUDA(launch_gather(g, p->ctx->sms, pick(p->ctx, stream)));

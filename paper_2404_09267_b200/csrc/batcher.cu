@@ -1,0 +1,491 @@
+// batcher.cu -- SLO-aware batching invoker (Alg. 2, scheduler.hpp:79-215),
+// its arrival model (trace.hpp:247-267), latency estimator (latency.hpp:
+// 78-118), memory cap (cost.hpp:107-115), and the generic canvas writer the
+// invoke events feed (tg_stitch_gather -> K5 on the device).
+//
+// The scheduler is host code over descriptors only -- pixels never leave the
+// device.  Its decisions are identical to the reference's, but a tentative
+// arrival costs one BSSF placement on the live packing instead of a full
+// stitch_all() of the queue: stitch_all is prefix-consistent (SURVEY
+// Appendix P4; SPEC.md:197 allows incremental placement when identical), so
+// stitch_all(Q + [p]) == place(p, stitch_all(Q)).  Free lists keep the
+// reference's order (erase in place, append split pieces), so every event's
+// StitchResult matches the reference field for field.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <optional>
+#include <queue>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "kernels.cuh"
+#include "tangram_gpu.h"
+
+using namespace tg;
+
+// Shared with api.cu (the context and the error slot live there).
+extern "C" void tg_internal_set_error(const char* msg);
+extern "C" tg_status tg_internal_run_gather(tg_ctx* ctx, const void* jobs, int32_t n_jobs,
+                                            const void* ranges, int32_t n_canvases,
+                                            tg_canvas_spec spec, const uint8_t* const* d_frames,
+                                            int32_t pitch, uint8_t* d_out, void* stream);
+
+namespace {
+
+tg_status bfail(tg_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  tg_internal_set_error(buf);
+  return s;
+}
+
+int64_t ms_to_us(double ms) {  // partition.hpp:34-36
+  return static_cast<int64_t>(ms < 0 ? ms * 1000.0 - 0.5 : ms * 1000.0 + 0.5);
+}
+
+// ---- latency.hpp:44-118 -----------------------------------------------------
+struct Profile {
+  std::vector<tg_profile_entry> e;  // sorted by batch size
+
+  static tg_status make(const tg_profile_entry* in, int n, Profile* out) {
+    if (n <= 0) return bfail(TG_ERR_INVALID_ARGUMENT, "latency profile has no entries");
+    std::vector<tg_profile_entry> es(in, in + n);
+    std::sort(es.begin(), es.end(), [](const tg_profile_entry& a, const tg_profile_entry& b) {
+      return a.batch_size < b.batch_size;
+    });
+    for (size_t i = 0; i < es.size(); ++i) {
+      if (es[i].batch_size < 1) return bfail(TG_ERR_INVALID_ARGUMENT, "profile entry with batch size < 1");
+      if (es[i].mu_ms <= 0) return bfail(TG_ERR_INVALID_ARGUMENT, "profile entry with non-positive mu");
+      if (es[i].sigma_ms < 0) return bfail(TG_ERR_INVALID_ARGUMENT, "profile entry with negative sigma");
+      if (i > 0 && es[i - 1].batch_size == es[i].batch_size)
+        return bfail(TG_ERR_INVALID_ARGUMENT, "duplicate profile entry for batch size %d",
+                     es[i].batch_size);
+    }
+    out->e = std::move(es);
+    return TG_OK;
+  }
+
+  // mu + 3 sigma, linear interpolation / extrapolation on slack values,
+  // clamped at zero.
+  double slack_ms(int k) const {
+    auto val = [](const tg_profile_entry& x) { return x.mu_ms + 3.0 * x.sigma_ms; };
+    if (e.size() == 1) return val(e[0]);
+    auto it = std::lower_bound(e.begin(), e.end(), k, [](const tg_profile_entry& x, int key) {
+      return x.batch_size < key;
+    });
+    const tg_profile_entry *lo, *hi;
+    if (it == e.begin()) {
+      lo = &e[0];
+      hi = &e[1];
+    } else if (it == e.end()) {
+      lo = &e[e.size() - 2];
+      hi = &e[e.size() - 1];
+    } else if (it->batch_size == k) {
+      return val(*it);
+    } else {
+      hi = &*it;
+      lo = hi - 1;
+    }
+    const double t = static_cast<double>(k - lo->batch_size) /
+                     static_cast<double>(hi->batch_size - lo->batch_size);
+    return std::max(0.0, val(*lo) + t * (val(*hi) - val(*lo)));
+  }
+
+  int64_t slack_us(int k) const { return ms_to_us(slack_ms(k)); }
+};
+
+// ---- incremental guillotine packing (stitch.hpp:66-146) ---------------------
+struct Placed {
+  tg_placement pl;
+  int queue_index;
+};
+
+struct CanvasSt {
+  std::vector<tg_rect> free;  // reference list order
+  std::vector<Placed> placed;
+  int64_t used = 0;
+};
+
+struct Packing {
+  std::vector<CanvasSt> canvases;
+};
+
+struct Choice {
+  int canvas, fi;  // fi < 0: a new canvas
+  tg_rect chosen;
+};
+
+// BSSF over every free rect of every open canvas; ties by canvas, y, x
+// (candidate_better, stitch.hpp:72-81).
+Choice choose(const Packing& st, int w, int h, int M, int N) {
+  Choice best{-1, -1, tg_rect{0, 0, 0, 0}};
+  int bs = 0;
+  for (int ci = 0; ci < static_cast<int>(st.canvases.size()); ++ci) {
+    const auto& fr = st.canvases[ci].free;
+    for (int fi = 0; fi < static_cast<int>(fr.size()); ++fi) {
+      const tg_rect& c = fr[fi];
+      if (c.w < w || c.h < h) continue;
+      const int s = std::min(c.w - w, c.h - h);
+      bool better;
+      if (best.canvas < 0) better = true;
+      else if (s != bs) better = s < bs;
+      else if (ci != best.canvas) better = ci < best.canvas;
+      else better = c.y != best.chosen.y ? c.y < best.chosen.y : c.x < best.chosen.x;
+      if (better) {
+        best = Choice{ci, fi, c};
+        bs = s;
+      }
+    }
+  }
+  if (best.canvas < 0) best = Choice{static_cast<int>(st.canvases.size()), -1, tg_rect{0, 0, M, N}};
+  return best;
+}
+
+void commit(Packing& st, const Choice& ch, const tg_patch_meta& p, int queue_index, int M, int N) {
+  if (ch.fi < 0) {
+    st.canvases.emplace_back();
+    st.canvases.back().free.push_back(tg_rect{0, 0, M, N});
+  }
+  CanvasSt& cv = st.canvases[ch.canvas];
+  const int fi = ch.fi < 0 ? 0 : ch.fi;
+  const tg_rect c = cv.free[fi];
+  cv.free.erase(cv.free.begin() + fi);
+  const int w = p.rect.w, h = p.rect.h, lw = c.w - w, lh = c.h - h;
+  tg_rect a, b;  // split_free_rect, stitch.hpp:86-99
+  if (lw <= lh) {
+    a = tg_rect{c.x + w, c.y, lw, c.h};
+    b = tg_rect{c.x, c.y + h, w, lh};
+  } else {
+    a = tg_rect{c.x + w, c.y, lw, h};
+    b = tg_rect{c.x, c.y + h, c.w, lh};
+  }
+  if (a.w > 0 && a.h > 0) cv.free.push_back(a);
+  if (b.w > 0 && b.h > 0) cv.free.push_back(b);
+  tg_placement pl;
+  pl.patch_id = p.patch_id;
+  pl.canvas_index = ch.canvas;
+  pl.position = tg_rect{c.x, c.y, w, h};
+  pl.reserved = 0;
+  cv.placed.push_back(Placed{pl, queue_index});
+  cv.used += static_cast<int64_t>(w) * h;
+}
+
+struct Queued {
+  tg_patch_meta meta;
+  int32_t src_frame;
+};
+
+struct Event {
+  tg_invoke_info info;
+  std::vector<Queued> patches;    // queue order
+  std::vector<Placed> placements; // canvas-major
+  std::vector<tg_free_rect> free; // canvas-major, list order
+};
+
+}  // namespace
+
+struct tg_batcher {
+  tg_canvas_spec spec{};
+  Profile prof;
+  int max_canvases = 1;
+  std::vector<Queued> queue;
+  Packing st;
+  int64_t t_ddl = 0, t_remain = 0;
+  bool has_timer = false;
+  int64_t timer_at = 0;
+  uint64_t timer_epoch = 0, next_epoch = 1;
+  std::vector<Event> events;
+
+  void reset() {
+    queue.clear();
+    st = Packing{};
+    has_timer = false;
+    t_ddl = 0;
+    t_remain = 0;
+  }
+
+  void make_event(int64_t now, tg_trigger trig) {
+    Event ev;
+    ev.info.fire_time_us = now;
+    ev.info.batch_size = static_cast<int32_t>(st.canvases.size());
+    ev.info.trigger = trig;
+    ev.info.estimated_slack_us = prof.slack_us(ev.info.batch_size);
+    ev.info.n_patches = static_cast<int32_t>(queue.size());
+    ev.patches = queue;
+    for (int ci = 0; ci < static_cast<int>(st.canvases.size()); ++ci) {
+      const CanvasSt& c = st.canvases[ci];
+      for (const Placed& p : c.placed) ev.placements.push_back(p);
+      for (int k = 0; k < static_cast<int>(c.free.size()); ++k)
+        ev.free.push_back(tg_free_rect{c.free[k], ci, k});
+    }
+    ev.info.n_free = static_cast<int32_t>(ev.free.size());
+    events.push_back(std::move(ev));
+  }
+
+  tg_status arrival(const tg_patch_meta& p, int32_t src, int64_t now) {
+    const int M = spec.width, N = spec.height;
+    if (p.rect.w > M || p.rect.h > N)  // stitch.hpp:114-118 (raised inside repack)
+      return bfail(TG_ERR_INVALID_ARGUMENT, "patch exceeds canvas (patch %llu, %dx%d)",
+                   static_cast<unsigned long long>(p.patch_id), p.rect.w, p.rect.h);
+    // tentative repack (scheduler.hpp:101-104) as one incremental placement
+    const Choice ch = choose(st, p.rect.w, p.rect.h, M, N);
+    const int k = static_cast<int>(st.canvases.size()) + (ch.fi < 0 ? 1 : 0);
+    const int64_t ddl = queue.empty() ? p.deadline_us : std::min(t_ddl, p.deadline_us);
+    const int64_t remain = ddl - prof.slack_us(k);
+    const bool over_cap = k > max_canvases;
+    if (over_cap || remain < now) {                      // :106-123
+      const tg_trigger trig = over_cap ? TG_TRIGGER_MEMORY_CAP : TG_TRIGGER_INFEASIBLE_ARRIVAL;
+      if (!queue.empty()) make_event(now, trig);         // the pre-arrival batch
+      reset();
+      queue.push_back(Queued{p, src});
+      commit(st, choose(st, p.rect.w, p.rect.h, M, N), p, 0, M, N);
+      t_ddl = p.deadline_us;
+      t_remain = t_ddl - prof.slack_us(1);
+      if (t_remain < now) {                              // infeasible even alone
+        make_event(now, TG_TRIGGER_INFEASIBLE_ARRIVAL);
+        reset();
+        return TG_OK;
+      }
+    } else {
+      commit(st, ch, p, static_cast<int>(queue.size()), M, N);
+      queue.push_back(Queued{p, src});
+      t_ddl = ddl;
+      t_remain = remain;
+    }
+    has_timer = true;                                    // arm_timer :124
+    timer_at = t_remain;
+    timer_epoch = next_epoch++;
+    return TG_OK;
+  }
+
+  void timer(int64_t now, uint64_t epoch) {               // :130-135
+    if (!has_timer || timer_epoch != epoch || queue.empty()) return;
+    make_event(now, TG_TRIGGER_DEADLINE_TIMER);
+    reset();
+  }
+};
+
+namespace {
+
+tg_status to_job(const tg_gather_job& j, Job* out) {
+  const tg_rect& d = j.dst;
+  if (d.x < 0 || d.y < 0 || d.w < 1 || d.h < 1 || d.x + d.w > 65535 || d.y + d.h > 65535 ||
+      j.src_x < 0 || j.src_y < 0 || j.src_x > 65535 || j.src_y > 65535)
+    return bfail(TG_ERR_INVALID_ARGUMENT, "gather job out of the 16-bit coordinate range");
+  *out = Job{static_cast<uint16_t>(d.x), static_cast<uint16_t>(d.y), static_cast<uint16_t>(d.w),
+             static_cast<uint16_t>(d.h), j.src_frame, static_cast<uint16_t>(j.src_x),
+             static_cast<uint16_t>(j.src_y)};
+  return TG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tg_status tg_stitch_gather(tg_ctx* ctx, const tg_gather_job* jobs, int32_t n_jobs,
+                           const int32_t* canvas_job_offsets, int32_t n_canvases,
+                           tg_canvas_spec spec, const uint8_t* const* d_frames, int32_t pitch,
+                           uint8_t* d_canvases, void* stream) {
+  if (!ctx) return bfail(TG_ERR_INVALID_ARGUMENT, "null context");
+  if (n_canvases < 0 || n_jobs < 0) return bfail(TG_ERR_INVALID_ARGUMENT, "negative counts");
+  if (pitch % 16) return bfail(TG_ERR_INVALID_ARGUMENT, "pitch must be a multiple of 16");
+  std::vector<Job> hj(static_cast<size_t>(n_jobs));
+  std::vector<uint2> ranges(static_cast<size_t>(n_canvases));
+  for (int c = 0; c < n_canvases; ++c) {
+    const int a = canvas_job_offsets[c], b = canvas_job_offsets[c + 1];
+    if (a < 0 || b < a || b > n_jobs) return bfail(TG_ERR_INVALID_ARGUMENT, "bad job offsets");
+    for (int i = a; i < b; ++i) {
+      const tg_status s = to_job(jobs[i], &hj[i]);
+      if (s) return s;
+    }
+    std::sort(hj.begin() + a, hj.begin() + b, [](const Job& x, const Job& y) {
+      return x.dx != y.dx ? x.dx < y.dx : x.dy < y.dy;
+    });
+    ranges[c] = make_uint2(static_cast<uint32_t>(a), static_cast<uint32_t>(b - a));
+  }
+  return tg_internal_run_gather(ctx, hj.data(), n_jobs, ranges.data(), n_canvases, spec, d_frames,
+                                pitch, d_canvases, stream);
+}
+
+tg_status tg_profile_slack_us(const tg_profile_entry* entries, int32_t n, int32_t k,
+                              int64_t* slack_us) {
+  Profile p;
+  const tg_status s = Profile::make(entries, n, &p);
+  if (s) return s;
+  if (k < 1) return bfail(TG_ERR_INVALID_ARGUMENT, "invalid batch size");
+  *slack_us = p.slack_us(k);
+  return TG_OK;
+}
+
+tg_status tg_max_canvases_per_batch(double gpu_memory_gb, double model_size_gb,
+                                    double vram_per_canvas_gb, int32_t* k) {
+  if (vram_per_canvas_gb <= 0) return bfail(TG_ERR_INVALID_ARGUMENT, "vram per canvas must be positive");
+  const double head_room = gpu_memory_gb - model_size_gb;
+  const int v = static_cast<int>(std::floor(head_room / vram_per_canvas_gb + 1e-9));
+  if (v < 1) return bfail(TG_ERR_INVALID_ARGUMENT, "cannot fit one canvas in GPU memory");
+  *k = v;
+  return TG_OK;
+}
+
+tg_status tg_transmission_schedule(const tg_patch_meta* patches, int32_t n, double bandwidth_mbps,
+                                   int64_t* arrival_us) {
+  if (!(bandwidth_mbps > 0.0)) return bfail(TG_ERR_INVALID_ARGUMENT, "bandwidth must be positive");
+  int64_t link_free_at = 0;
+  for (int i = 0; i < n; ++i) {
+    const int64_t start = std::max(patches[i].generation_time_us, link_free_at);
+    const double bits = static_cast<double>(patches[i].size_bytes) * 8.0;
+    const int64_t arrival = start + std::llround(bits / bandwidth_mbps);  // Mbps == bits/us
+    arrival_us[i] = arrival;
+    link_free_at = arrival;
+  }
+  return TG_OK;
+}
+
+tg_status tg_batcher_create(tg_canvas_spec spec, const tg_profile_entry* entries, int32_t n_entries,
+                            int32_t max_canvases, tg_batcher** out) {
+  *out = nullptr;
+  if (n_entries > 0 && entries == nullptr)
+    return bfail(TG_ERR_INVALID_ARGUMENT, "scheduler needs a latency profile");
+  if (n_entries <= 0) return bfail(TG_ERR_INVALID_ARGUMENT, "scheduler needs a latency profile");
+  if (max_canvases < 1) return bfail(TG_ERR_INVALID_ARGUMENT, "max canvases must be >= 1");
+  if (spec.width < 1 || spec.height < 1 || spec.width > 65535 || spec.height > 65535)
+    return bfail(TG_ERR_INVALID_ARGUMENT, "canvas dimensions must be in [1, 65535]");
+  tg_batcher* b = new tg_batcher();
+  const tg_status s = Profile::make(entries, n_entries, &b->prof);
+  if (s) {
+    delete b;
+    return s;
+  }
+  b->spec = spec;
+  b->max_canvases = max_canvases;
+  *out = b;
+  return TG_OK;
+}
+
+void tg_batcher_destroy(tg_batcher* b) { delete b; }
+
+tg_status tg_batcher_on_patch_arrival(tg_batcher* b, const tg_patch_meta* patch, int32_t src_frame,
+                                      int64_t now_us, int32_t* n_events) {
+  b->events.clear();
+  const tg_status s = b->arrival(*patch, src_frame, now_us);
+  *n_events = static_cast<int32_t>(b->events.size());
+  return s;
+}
+
+tg_status tg_batcher_on_timer(tg_batcher* b, int64_t now_us, uint64_t epoch, int32_t* n_events) {
+  b->events.clear();
+  b->timer(now_us, epoch);
+  *n_events = static_cast<int32_t>(b->events.size());
+  return TG_OK;
+}
+
+tg_status tg_batcher_pending_timer(tg_batcher* b, int32_t* has_timer, int64_t* fire_at_us,
+                                   uint64_t* epoch) {
+  *has_timer = b->has_timer ? 1 : 0;
+  *fire_at_us = b->has_timer ? b->timer_at : 0;
+  *epoch = b->has_timer ? b->timer_epoch : 0;
+  return TG_OK;
+}
+
+tg_status tg_batcher_status(tg_batcher* b, int32_t* queue_len, int32_t* canvases,
+                            int64_t* earliest_deadline_us, int64_t* remaining_time_us) {
+  *queue_len = static_cast<int32_t>(b->queue.size());
+  *canvases = static_cast<int32_t>(b->st.canvases.size());
+  *earliest_deadline_us = b->t_ddl;
+  *remaining_time_us = b->t_remain;
+  return TG_OK;
+}
+
+tg_status tg_batcher_event(tg_batcher* b, int32_t i, tg_invoke_info* info, uint64_t* patch_ids,
+                           tg_placement* placements, tg_free_rect* free_rects) {
+  if (i < 0 || i >= static_cast<int32_t>(b->events.size()))
+    return bfail(TG_ERR_OUT_OF_RANGE, "event index out of range");
+  const Event& ev = b->events[i];
+  if (info) *info = ev.info;
+  if (patch_ids)
+    for (size_t k = 0; k < ev.patches.size(); ++k) patch_ids[k] = ev.patches[k].meta.patch_id;
+  if (placements)
+    for (size_t k = 0; k < ev.placements.size(); ++k) placements[k] = ev.placements[k].pl;
+  if (free_rects) std::copy(ev.free.begin(), ev.free.end(), free_rects);
+  return TG_OK;
+}
+
+tg_status tg_batcher_gather(tg_ctx* ctx, tg_batcher* b, int32_t i, const uint8_t* const* d_frames,
+                            int32_t pitch, uint8_t* d_canvases, void* stream) {
+  if (i < 0 || i >= static_cast<int32_t>(b->events.size()))
+    return bfail(TG_ERR_OUT_OF_RANGE, "event index out of range");
+  const Event& ev = b->events[i];
+  const int nc = ev.info.batch_size;
+  std::vector<std::vector<Job>> per(static_cast<size_t>(nc));
+  for (const Placed& p : ev.placements) {
+    const Queued& q = ev.patches[p.queue_index];
+    Job j;
+    const tg_status s = to_job(tg_gather_job{p.pl.position, q.src_frame, q.meta.rect.x, q.meta.rect.y}, &j);
+    if (s) return s;
+    per[p.pl.canvas_index].push_back(j);
+  }
+  for (const tg_free_rect& f : ev.free) {
+    Job j;
+    const tg_status s = to_job(tg_gather_job{f.rect, -1, 0, 0}, &j);
+    if (s) return s;
+    per[f.canvas_index].push_back(j);
+  }
+  std::vector<Job> jobs;
+  std::vector<uint2> ranges;
+  for (auto& v : per) {
+    std::sort(v.begin(), v.end(), [](const Job& x, const Job& y) {
+      return x.dx != y.dx ? x.dx < y.dx : x.dy < y.dy;
+    });
+    ranges.push_back(make_uint2(static_cast<uint32_t>(jobs.size()), static_cast<uint32_t>(v.size())));
+    jobs.insert(jobs.end(), v.begin(), v.end());
+  }
+  return tg_internal_run_gather(ctx, jobs.data(), static_cast<int32_t>(jobs.size()), ranges.data(),
+                                static_cast<int32_t>(ranges.size()), b->spec, d_frames, pitch,
+                                d_canvases, stream);
+}
+
+tg_status tg_batcher_replay(tg_batcher* b, const tg_patch_meta* patches, const int32_t* src_frames,
+                            const int64_t* arrival_us, int32_t n, int32_t* n_events) {
+  // sim.hpp:334-342 (arrival seqs first, scene-major), 392-400 (timer pushed
+  // when its epoch is new), 425-458 (heap by (t, seq)).
+  struct Ev {
+    int64_t t;
+    uint64_t seq;
+    int kind;  // 0 arrival, 1 timer
+    uint64_t a;
+    bool operator>(const Ev& o) const { return std::tie(t, seq) > std::tie(o.t, o.seq); }
+  };
+  std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> heap;
+  uint64_t seq = 0;
+  for (int i = 0; i < n; ++i) heap.push(Ev{arrival_us[i], seq++, 0, static_cast<uint64_t>(i)});
+  std::vector<Event> all;
+  uint64_t pushed_epoch = 0;
+  while (!heap.empty()) {
+    const Ev ev = heap.top();
+    heap.pop();
+    b->events.clear();
+    if (ev.kind == 0) {
+      const tg_status s = b->arrival(patches[ev.a], src_frames ? src_frames[ev.a] : -1, ev.t);
+      if (s) return s;
+      if (b->has_timer && b->timer_epoch != pushed_epoch) {
+        heap.push(Ev{b->timer_at, seq++, 1, b->timer_epoch});
+        pushed_epoch = b->timer_epoch;
+      }
+    } else {
+      b->timer(ev.t, ev.a);
+    }
+    for (auto& e : b->events) all.push_back(std::move(e));
+  }
+  b->events = std::move(all);
+  *n_events = static_cast<int32_t>(b->events.size());
+  if (!b->queue.empty()) return bfail(TG_ERR_INVALID_ARGUMENT, "scheduler queue not drained");
+  return TG_OK;
+}
+
+}  // extern "C"

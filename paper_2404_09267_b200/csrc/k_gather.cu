@@ -118,11 +118,9 @@ __global__ void __launch_bounds__(kGatherThreads, 2) gather_kernel(const GatherA
   const int nch = row_len >> 4;  // chunks per row on the aligned path
   for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
     const int k = u / a.nbands, b = u - k * a.nbands;
-    const uint32_t packed = a.canvas_map[k];
-    const int f = static_cast<int>(packed >> 6), c = static_cast<int>(packed & 63u);
-    const uint32_t cj = a.canvas_jobs[static_cast<size_t>(f) * a.zones + c];
-    const int start = static_cast<int>(cj & 0xffffu), cnt = static_cast<int>(cj >> 16);
-    const Job* gj = a.jobs + static_cast<size_t>(f) * a.job_cap + start;
+    const uint2 range = a.ranges[k];
+    const int cnt = static_cast<int>(range.y);
+    const Job* gj = a.jobs + range.x;
     const int b0 = b * kGatherBand, b1 = min(a.N, b0 + kGatherBand);
     uint8_t* canvas = a.out + static_cast<size_t>(k) * canvas_bytes;
     const uintptr_t cbase = reinterpret_cast<uintptr_t>(canvas);

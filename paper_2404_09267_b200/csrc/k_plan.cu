@@ -207,9 +207,11 @@ __global__ void __launch_bounds__(1024) scan_kernel(const ScanArgs a) {
       tg_placement* fl = a.placements + static_cast<size_t>(f) * a.zones;
       for (int k = 0; k < a.n_placements[f]; ++k) fl[k].patch_id = id0 + fl[k].patch_id;
       a.canvas_base[f] = cb;
+      const uint32_t* fcj = a.canvas_jobs + static_cast<size_t>(f) * a.zones;
       for (int c = 0; c < vc; ++c)
         if (cb + c < a.max_canvases)
-          a.canvas_map[cb + c] = static_cast<uint32_t>(f) << 6 | static_cast<uint32_t>(c);
+          a.ranges[cb + c] = make_uint2(static_cast<uint32_t>(f) * a.job_cap + (fcj[c] & 0xffffu),
+                                        fcj[c] >> 16);
     }
     run_p += wtmp_p[nt / 32 - 1];
     run_c += wtmp_c[nt / 32 - 1];

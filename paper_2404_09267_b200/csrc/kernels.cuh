@@ -35,17 +35,18 @@ struct PlanArgs {
 };
 
 struct ScanArgs {
-  int n_frames, zones;
+  int n_frames, zones, job_cap;
   uint64_t first_id;
   int64_t max_canvases;
   int nbands;
   const int32_t* n_patches;
   const int32_t* n_placements;
   const int32_t* n_canvases;
+  const uint32_t* canvas_jobs;  // [F][Z] local start | count << 16 (from the planner)
   tg_patch_meta* patches;
   tg_placement* placements;
   int64_t* canvas_base;
-  uint32_t* canvas_map;   // [max_canvases] frame << 6 | local canvas
+  uint2* ranges;          // [max_canvases] (first job, job count) in the flat job array
   int32_t* gather_units;  // out: min(total, cap) * nbands
   uint64_t* id_state;     // next patch id after this run; read when first_id == ~0
   DevError* err;
@@ -84,13 +85,14 @@ cudaError_t launch_partition_batch(const PartitionBatchArgs& a, cudaStream_t str
 cudaError_t launch_stitch_batch(const StitchBatchArgs& a, cudaStream_t stream);
 
 // ---- K5 (k_gather.cu) -------------------------------------------------------
+// Canvas k is tiled by jobs[ranges[k].x .. ranges[k].x + ranges[k].y),
+// sorted by dx; src_frame indexes `frames`.
 struct GatherArgs {
   const uint8_t* const* frames;
-  int pitch, M, N, zones, job_cap, nbands;
+  int pitch, M, N, nbands;
   const Job* jobs;
-  const uint32_t* canvas_jobs;
-  const uint32_t* canvas_map;
-  const int32_t* units;
+  const uint2* ranges;
+  const int32_t* units;   // device count of (canvas, band) units
   uint8_t* out;
 };
 cudaError_t launch_gather(const GatherArgs& a, int sms, cudaStream_t stream);

@@ -1,0 +1,236 @@
+"""The SLO batcher (Alg. 2 invoker) against the reference scheduler.
+
+The batcher is host code over descriptors (it never touches pixels), so
+these run without a GPU.  Checks, all exact:
+* the reference's own unit-test KATs (scheduler_test.cpp:56-151);
+* random arrival streams driven event by event against the reference
+  SloScheduler compiled as-is (oracle/_ref), comparing every event's fire
+  time, trigger, batch size, slack, patch ids, placements and free lists;
+* multi-camera streams through the reference's whole simulator
+  (tangram::run, tangram policy): admission, per-link arrival times
+  (transmission_schedule) and every invoke in its event log.
+"""
+import pytest
+
+from oracle import oracle as O
+from paper_2404_09267_b200 import api as A
+
+need_ref = pytest.mark.skipif(not O.have_ref(), reason="reference build (oracle/_ref) absent")
+
+TEST_PROFILE = [(1, 100.0, 10.0), (2, 170.0, 10.0)]  # scheduler_test.cpp:33-35
+
+
+def full_patch(pid, gen, slo):
+    return A.PatchMeta(pid, pid, A.Rect(0, 0, 100, 100), gen, slo, gen + slo, 15000)
+
+
+def sched(max_canvases=2, profile=TEST_PROFILE, canvas=(100, 100)):
+    return A.SloScheduler(A.CanvasSpec(*canvas), A.LatencyProfile(*canvas, profile), max_canvases)
+
+
+def test_single_arrival_arms_deadline_timer():
+    s = sched()
+    assert s.on_patch_arrival(full_patch(1, 0, 500_000), 0) == []
+    assert not s.idle()
+    assert s.earliest_deadline_us() == 500_000 and s.remaining_time_us() == 370_000
+    t = s.pending_timer()
+    assert t.fire_at_us == 370_000
+    ev = s.on_timer(370_000, t.epoch)
+    assert (ev.fire_time_us, ev.batch_size, ev.patch_ids, ev.estimated_slack_us, ev.trigger) == \
+        (370_000, 1, [1], 130_000, "deadline_timer")
+    assert s.idle() and s.pending_timer() is None
+
+
+def test_second_arrival_rearms_with_batch_slack():
+    s = sched()
+    s.on_patch_arrival(full_patch(1, 0, 500_000), 0)
+    stale = s.pending_timer().epoch
+    assert s.on_patch_arrival(full_patch(2, 100_000, 500_000), 100_000) == []
+    assert s.queue_size() == 2 and s.current_canvas_count() == 2
+    assert s.remaining_time_us() == 300_000 and s.pending_timer().fire_at_us == 300_000
+    assert s.on_timer(370_000, stale) is None
+    ev = s.on_timer(300_000, s.pending_timer().epoch)
+    assert ev.batch_size == 2 and ev.patch_ids == [1, 2] and ev.estimated_slack_us == 200_000
+
+
+def test_memory_cap_flushes_previous_batch():
+    s = sched()
+    s.on_patch_arrival(full_patch(1, 0, 500_000), 0)
+    s.on_patch_arrival(full_patch(2, 100_000, 500_000), 100_000)
+    evs = s.on_patch_arrival(full_patch(3, 250_000, 500_000), 250_000)
+    assert len(evs) == 1
+    e = evs[0]
+    assert (e.trigger, e.fire_time_us, e.batch_size, e.patch_ids, e.estimated_slack_us) == \
+        ("memory_cap", 250_000, 2, [1, 2], 200_000)
+
+
+def test_constructor_validation_and_profile():
+    with pytest.raises(A.InvalidArgument):
+        A.SloScheduler(A.CanvasSpec(100, 100), A.LatencyProfile(100, 100, TEST_PROFILE), 0)
+    with pytest.raises(A.InvalidArgument, match="latency profile has no entries"):
+        A.LatencyProfile(100, 100, [])
+    with pytest.raises(A.InvalidArgument, match="duplicate profile entry"):
+        A.LatencyProfile(100, 100, [(1, 10.0, 1.0), (1, 11.0, 1.0)])
+    p = A.LatencyProfile(100, 100, TEST_PROFILE)
+    assert [p.slack_us(k) for k in (1, 2, 3)] == [130_000, 200_000, 270_000]
+    assert A.max_canvases_per_batch(6.0, 2.0, 1.0) == 4
+    with pytest.raises(A.InvalidArgument, match="cannot fit one canvas"):
+        A.max_canvases_per_batch(2.5, 2.0, 1.0)
+
+
+def random_patches(seed, n):
+    """scheduler_test.cpp:236-255."""
+    rng = O.Rng(seed)
+    out, t = [], 0
+    for i in range(n):
+        t += rng.uniform_int(0, 120_000)
+        w, h = rng.uniform_int(10, 100), rng.uniform_int(10, 100)
+        slo = rng.uniform_int(125_000, 2_000_000)
+        out.append(A.PatchMeta(i + 1, i, A.Rect(0, 0, w, h), t, slo, t + slo, w * h))
+    return out
+
+
+def drive(s, patches, ref=None):
+    """scheduler_test.cpp:216-233: timers due at or before each generation
+    time fire first; every call is mirrored on the reference scheduler."""
+    ours, theirs = [], []
+
+    def d(p):
+        return dict(patch_id=p.patch_id, source_frame_id=p.source_frame_id,
+                    rect=(p.rect.x, p.rect.y, p.rect.w, p.rect.h),
+                    generation_time_us=p.generation_time_us, slo_us=p.slo_us,
+                    deadline_us=p.deadline_us, size_bytes=p.size_bytes)
+
+    def fire_due(limit):
+        while s.pending_timer() is not None and (limit is None or s.pending_timer().fire_at_us <= limit):
+            t = s.pending_timer()
+            if ref is not None:
+                assert ref.pending_timer() == (t.fire_at_us, t.epoch)
+                r = ref.on_timer(t.fire_at_us, t.epoch)
+                if r:
+                    theirs.append(r)
+            e = s.on_timer(t.fire_at_us, t.epoch)
+            if e:
+                ours.append(e)
+
+    for p in patches:
+        fire_due(p.generation_time_us)
+        ours.extend(s.on_patch_arrival(p, p.generation_time_us))
+        if ref is not None:
+            theirs.extend(ref.on_patch_arrival(d(p), p.generation_time_us))
+    fire_due(None)
+    return ours, theirs
+
+
+def event_tuple(e):
+    pl = [(p.patch_id, p.canvas_index, p.position.x, p.position.y, p.position.w, p.position.h)
+          for c in e.stitch.canvases for p in c.placements]
+    fr = [(ci, r.x, r.y, r.w, r.h) for ci, c in enumerate(e.stitch.canvases) for r in c.free_rects]
+    trig = {"deadline_timer": 0, "infeasible_arrival": 1, "memory_cap": 2}[e.trigger]
+    return (e.fire_time_us, trig, e.batch_size, e.estimated_slack_us, e.patch_ids, pl, fr)
+
+
+def ref_tuple(e):
+    return (e["fire_time_us"], e["trigger"], e["batch_size"], e["estimated_slack_us"],
+            e["patch_ids"], e["placements"], e["free"])
+
+
+def test_every_admitted_patch_fires_exactly_once():
+    """scheduler_test.cpp:257-290 invariants."""
+    prof = A.LatencyProfile(100, 100, TEST_PROFILE)
+    for seed in range(1, 21):
+        s = sched(3)
+        patches = random_patches(seed, 200)
+        events, _ = drive(s, patches)
+        deadline = {p.patch_id: p.deadline_us for p in patches}
+        seen, last = set(), 0
+        for e in events:
+            assert e.fire_time_us >= last
+            last = e.fire_time_us
+            assert 1 <= e.batch_size <= 3
+            assert e.estimated_slack_us == prof.slack_us(e.batch_size)
+            for pid in e.patch_ids:
+                assert pid not in seen
+                seen.add(pid)
+            if e.trigger == "deadline_timer":
+                assert e.fire_time_us == min(deadline[i] for i in e.patch_ids) - e.estimated_slack_us
+        assert len(seen) == len(patches) and s.idle()
+
+
+@need_ref
+@pytest.mark.parametrize("canvas,max_canvases,profile", [
+    ((100, 100), 3, TEST_PROFILE),
+    ((256, 256), 2, [(1, 40.0, 4.0), (2, 60.0, 5.0), (4, 95.0, 8.0)]),
+    ((1024, 1024), 8, [(1, 60.0, 3.0), (2, 85.0, 4.0), (4, 135.0, 6.0), (8, 235.0, 10.0)]),
+])
+def test_random_streams_match_reference_scheduler(canvas, max_canvases, profile):
+    for seed in range(1, 31):
+        s = sched(max_canvases, profile, canvas)
+        ref = O.RefScheduler(canvas[0], canvas[1], profile, max_canvases)
+        patches = random_patches(seed * 7 + canvas[0], 150)
+        ours, theirs = drive(s, patches, ref)
+        assert [event_tuple(e) for e in ours] == [ref_tuple(e) for e in theirs], seed
+
+
+def scenes_for(n_cams, n_frames, W, H, **kw):
+    out = []
+    for c in range(n_cams):
+        cfg = O.gen_cfg(seed=1000 + c, n_frames=n_frames, fps=30.0, frame_width=W, frame_height=H, **kw)
+        out.append(O.generate_trace(cfg))
+    return out
+
+
+def our_run(scenes, W, H, profile, bandwidth, zones=(4, 4), canvas=(1024, 1024), gpu_mem=6.0,
+            model=2.0, slo=1_000_000):
+    """The device-side pipeline's host half for configs 3/4: partition (here
+    the oracle's, bit-identical to the device's), admission (sim.hpp:262),
+    per-camera link arrivals, then the batcher's reference event loop."""
+    first = 0
+    admitted_all, arrival_of = [], {}
+    order_patches, order_arrivals = [], []
+    for t_us, frames in scenes:
+        adm = []
+        for i, rois in enumerate(frames):
+            patches = O.partition(i, W, H, t_us[i], slo, zones[0], zones[1], rois, 1.5, first)
+            first += len(patches)
+            for p in patches:
+                ok = p["rect"][2] <= canvas[0] and p["rect"][3] <= canvas[1]
+                admitted_all.append(ok)
+                if ok:
+                    adm.append(A.PatchMeta(p["patch_id"], p["source_frame_id"], A.Rect(*p["rect"]),
+                                           p["generation_time_us"], p["slo_us"], p["deadline_us"],
+                                           p["size_bytes"]))
+        arr = A.transmission_schedule(adm, bandwidth)
+        for p, a in zip(adm, arr):
+            arrival_of[p.patch_id] = a
+        order_patches += adm
+        order_arrivals += arr
+    s = A.SloScheduler(A.CanvasSpec(*canvas), A.LatencyProfile(*canvas, profile),
+                       A.max_canvases_per_batch(gpu_mem, model, 1.0))
+    events = s.replay(order_patches, order_arrivals)
+    return admitted_all, arrival_of, events
+
+
+SIM_PROFILE = [(1, 60.0, 3.0), (2, 85.0, 4.0), (4, 135.0, 6.0), (8, 235.0, 10.0)]
+
+
+@need_ref
+@pytest.mark.parametrize("n_cams,W,H,bw,kw", [
+    (1, 1920, 1080, 80.0, {}),
+    (5, 3840, 2160, 80.0, dict(roi_max_dim=480)),            # config 3 geometry
+    (5, 3840, 2160, 20.0, dict(roi_max_dim=1024, roi_proportion_mean=0.3)),
+    (8, 1920, 1080, 40.0, dict(roi_proportion_mean=0.2)),
+])
+def test_multi_camera_stream_matches_reference_simulator(n_cams, W, H, bw, kw):
+    scenes = scenes_for(n_cams, 24, W, H, **kw)
+    ref = O.run_tangram(scenes, W, H, SIM_PROFILE, bandwidth_mbps=bw)
+    admitted, arrival_of, events = our_run(scenes, W, H, SIM_PROFILE, bw)
+    assert admitted == [bool(a) for a in ref["admitted"]]
+    for pid, a in arrival_of.items():
+        assert ref["arrival_us"][pid] == a
+    ours = [(e.fire_time_us, {"deadline_timer": 0, "infeasible_arrival": 1, "memory_cap": 2}[e.trigger],
+             e.batch_size, e.estimated_slack_us, e.patch_ids) for e in events]
+    theirs = [(e["fire_time_us"], e["trigger"], e["batch_size"], e["estimated_slack_us"],
+               e["patch_ids"]) for e in ref["events"]]
+    assert ours == theirs
+    assert len(ours) > 0
