@@ -312,12 +312,26 @@ tg_status tg_batcher_event(tg_batcher* b, int32_t i, tg_invoke_info* info, uint6
 /* Writes event i's canvases: d_frames[src_frame] holds each patch's frame. */
 tg_status tg_batcher_gather(tg_ctx* ctx, tg_batcher* b, int32_t i, const uint8_t* const* d_frames,
                             int32_t pitch, uint8_t* d_canvases, void* stream);
+/* Writes the canvases of every event of the last call back to back (event
+ * order, canvas order) in one launch; *n_canvases receives their count. */
+tg_status tg_batcher_gather_all(tg_ctx* ctx, tg_batcher* b, const uint8_t* const* d_frames,
+                                int32_t pitch, uint8_t* d_canvases, int64_t canvas_cap,
+                                int64_t* n_canvases, void* stream);
 /* Offline driver of the reference event loop for the tangram policy
  * (sim.hpp:334-342, 425-458): arrivals ordered by (arrival_us, input order),
  * a timer is queued when its epoch is new and loses ties to arrivals.  All
  * events are kept; *n_events is their count (tg_batcher_event reads them). */
 tg_status tg_batcher_replay(tg_batcher* b, const tg_patch_meta* patches, const int32_t* src_frames,
                             const int64_t* arrival_us, int32_t n, int32_t* n_events);
+/* Multi-camera front end (sim.hpp:274-290): admitted patches camera-major
+ * (cam_offsets[n_cams+1]), each camera's in generation order, delivered over
+ * one FIFO uplink per camera (per_camera_link = 1) or one shared link sorted
+ * by (generation time, patch id); then tg_batcher_replay.  arrival_us_out
+ * (optional) receives each patch's arrival time. */
+tg_status tg_batcher_replay_links(tg_batcher* b, int32_t n_cams, const int32_t* cam_offsets,
+                                  const tg_patch_meta* patches, const int32_t* src_frames,
+                                  double bandwidth_mbps, int32_t per_camera_link,
+                                  int64_t* arrival_us_out, int32_t* n_events);
 
 /* ---- synthetic workload (fixture source; not part of the timed path) -----
  * trace.hpp:145-231 generate_trace, restated (std::mt19937_64 + the

@@ -416,18 +416,23 @@ tg_status tg_batcher_event(tg_batcher* b, int32_t i, tg_invoke_info* info, uint6
   return TG_OK;
 }
 
-tg_status tg_batcher_gather(tg_ctx* ctx, tg_batcher* b, int32_t i, const uint8_t* const* d_frames,
-                            int32_t pitch, uint8_t* d_canvases, void* stream) {
-  if (i < 0 || i >= static_cast<int32_t>(b->events.size()))
-    return bfail(TG_ERR_OUT_OF_RANGE, "event index out of range");
-  const Event& ev = b->events[i];
+}  // extern "C"
+
+namespace {
+// Appends one event's canvases to the flat plan: placements pull from their
+// patch's frame, final free rects zero-fill; jobs x-sorted per canvas.
+tg_status append_event_plan(const Event& ev, std::vector<Job>& jobs, std::vector<uint2>& ranges) {
   const int nc = ev.info.batch_size;
   std::vector<std::vector<Job>> per(static_cast<size_t>(nc));
   for (const Placed& p : ev.placements) {
     const Queued& q = ev.patches[p.queue_index];
     Job j;
-    const tg_status s = to_job(tg_gather_job{p.pl.position, q.src_frame, q.meta.rect.x, q.meta.rect.y}, &j);
+    const tg_status s =
+        to_job(tg_gather_job{p.pl.position, q.src_frame, q.meta.rect.x, q.meta.rect.y}, &j);
     if (s) return s;
+    if (q.src_frame < 0)
+      return bfail(TG_ERR_INVALID_ARGUMENT, "patch %llu has no source frame",
+                   static_cast<unsigned long long>(q.meta.patch_id));
     per[p.pl.canvas_index].push_back(j);
   }
   for (const tg_free_rect& f : ev.free) {
@@ -436,8 +441,6 @@ tg_status tg_batcher_gather(tg_ctx* ctx, tg_batcher* b, int32_t i, const uint8_t
     if (s) return s;
     per[f.canvas_index].push_back(j);
   }
-  std::vector<Job> jobs;
-  std::vector<uint2> ranges;
   for (auto& v : per) {
     std::sort(v.begin(), v.end(), [](const Job& x, const Job& y) {
       return x.dx != y.dx ? x.dx < y.dx : x.dy < y.dy;
@@ -445,6 +448,38 @@ tg_status tg_batcher_gather(tg_ctx* ctx, tg_batcher* b, int32_t i, const uint8_t
     ranges.push_back(make_uint2(static_cast<uint32_t>(jobs.size()), static_cast<uint32_t>(v.size())));
     jobs.insert(jobs.end(), v.begin(), v.end());
   }
+  return TG_OK;
+}
+}  // namespace
+
+extern "C" {
+
+tg_status tg_batcher_gather(tg_ctx* ctx, tg_batcher* b, int32_t i, const uint8_t* const* d_frames,
+                            int32_t pitch, uint8_t* d_canvases, void* stream) {
+  if (i < 0 || i >= static_cast<int32_t>(b->events.size()))
+    return bfail(TG_ERR_OUT_OF_RANGE, "event index out of range");
+  std::vector<Job> jobs;
+  std::vector<uint2> ranges;
+  const tg_status s = append_event_plan(b->events[i], jobs, ranges);
+  if (s) return s;
+  return tg_internal_run_gather(ctx, jobs.data(), static_cast<int32_t>(jobs.size()), ranges.data(),
+                                static_cast<int32_t>(ranges.size()), b->spec, d_frames, pitch,
+                                d_canvases, stream);
+}
+
+tg_status tg_batcher_gather_all(tg_ctx* ctx, tg_batcher* b, const uint8_t* const* d_frames,
+                                int32_t pitch, uint8_t* d_canvases, int64_t canvas_cap,
+                                int64_t* n_canvases, void* stream) {
+  std::vector<Job> jobs;
+  std::vector<uint2> ranges;
+  for (const Event& ev : b->events) {
+    const tg_status s = append_event_plan(ev, jobs, ranges);
+    if (s) return s;
+  }
+  *n_canvases = static_cast<int64_t>(ranges.size());
+  if (static_cast<int64_t>(ranges.size()) > canvas_cap)
+    return bfail(TG_ERR_CAPACITY, "canvas capacity exceeded (%lld canvases > %lld)",
+                 static_cast<long long>(ranges.size()), static_cast<long long>(canvas_cap));
   return tg_internal_run_gather(ctx, jobs.data(), static_cast<int32_t>(jobs.size()), ranges.data(),
                                 static_cast<int32_t>(ranges.size()), b->spec, d_frames, pitch,
                                 d_canvases, stream);
@@ -486,6 +521,36 @@ tg_status tg_batcher_replay(tg_batcher* b, const tg_patch_meta* patches, const i
   *n_events = static_cast<int32_t>(b->events.size());
   if (!b->queue.empty()) return bfail(TG_ERR_INVALID_ARGUMENT, "scheduler queue not drained");
   return TG_OK;
+}
+
+tg_status tg_batcher_replay_links(tg_batcher* b, int32_t n_cams, const int32_t* cam_offsets,
+                                  const tg_patch_meta* patches, const int32_t* src_frames,
+                                  double bandwidth_mbps, int32_t per_camera_link,
+                                  int64_t* arrival_us_out, int32_t* n_events) {
+  const int n = cam_offsets[n_cams];
+  std::vector<int64_t> arrival(static_cast<size_t>(n));
+  if (per_camera_link) {
+    for (int c = 0; c < n_cams; ++c) {
+      const int a = cam_offsets[c], e = cam_offsets[c + 1];
+      const tg_status s = tg_transmission_schedule(patches + a, e - a, bandwidth_mbps, arrival.data() + a);
+      if (s) return s;
+    }
+  } else {  // one shared link: (generation time, patch id) order (sim.hpp:280-289)
+    std::vector<int> order(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](int x, int y) {
+      return std::tie(patches[x].generation_time_us, patches[x].patch_id) <
+             std::tie(patches[y].generation_time_us, patches[y].patch_id);
+    });
+    std::vector<tg_patch_meta> merged(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) merged[i] = patches[order[i]];
+    std::vector<int64_t> arr(static_cast<size_t>(n));
+    const tg_status s = tg_transmission_schedule(merged.data(), n, bandwidth_mbps, arr.data());
+    if (s) return s;
+    for (int i = 0; i < n; ++i) arrival[order[i]] = arr[i];
+  }
+  if (arrival_us_out) std::copy(arrival.begin(), arrival.end(), arrival_us_out);
+  return tg_batcher_replay(b, patches, src_frames, arrival.data(), n, n_events);
 }
 
 }  // extern "C"

@@ -1,0 +1,67 @@
+"""Configs 3/4 on the device: cameras -> K1-K4 -> descriptors -> SLO batcher
+-> event canvases, against the reference's own simulator.
+
+The RoIs the GPU extracts from pixels are fed, as trace rects, to the
+reference's tangram::run(): it partitions them itself, models the uplinks
+and drives its SloScheduler.  Every invoke it logs must equal ours, and every
+canvas byte we write must equal a host fill of that event's placements from
+the same frames.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2404_09267_b200 import api as A
+from paper_2404_09267_b200 import multicam as MC
+
+pytestmark = pytest.mark.gpu
+
+PROFILE = [(1, 60.0, 3.0), (2, 85.0, 4.0), (4, 135.0, 6.0), (8, 235.0, 10.0)]
+
+
+@pytest.mark.parametrize("cams,W,H,n,bw,link", [
+    ([0, 1, 2], 1920, 1080, 12, 80.0, True),
+    ([3, 4, 5, 6, 7], 3840, 2160, 6, 20.0, True),
+    ([0, 1], 1920, 1080, 10, 40.0, False),
+])
+def test_multicam_events_and_canvases_match_reference(ctx, cams, W, H, n, bw, link):
+    path = MC.MultiCameraPath(ctx, cams, W, H, n, PROFILE, bandwidth_mbps=bw, per_camera_link=link,
+                              trace_kw=dict(roi_proportion_mean=0.15))
+    desc, n_events, n_canvases = path.step()
+    ctx.stream_sync(path.stream)
+    assert n_events > 0 and n_canvases > 0
+    events = path.events()
+    # the GPU's RoIs, as the reference simulator's input scenes
+    scenes, frames = [], []
+    for k, c in enumerate(cams):
+        res = path.pipes[k].results(n)
+        rois = [[tuple(r) for r in res["rois"][f, :res["n_rois"][f]].tolist()] for f in range(n)]
+        scenes.append((path.t_us[k], rois))
+        frames.append([path.rings[k].download_frame(s) for s in range(n + 1)])
+    if O.have_ref():
+        ref = O.run_tangram(scenes, W, H, PROFILE, bandwidth_mbps=bw, per_scene_link=link)
+        names = {0: "deadline_timer", 1: "infeasible_arrival", 2: "memory_cap"}
+        assert [(e.fire_time_us, e.trigger, e.batch_size, e.estimated_slack_us, e.patch_ids)
+                for e in events] == \
+            [(e["fire_time_us"], names[e["trigger"]], e["batch_size"], e["estimated_slack_us"],
+              e["patch_ids"]) for e in ref["events"]]
+        adm_ids = [i for i, a in enumerate(ref["admitted"]) if a]
+        assert list(path.arrival) == [ref["arrival_us"][i] for i in adm_ids]
+    # canvas bytes: host fill of every event canvas from the same frames
+    plan = path._last
+    by_id = {int(p["patch_id"]): (int(s), p) for p, s in zip(plan["patches"], plan["src"])}
+    got = path.canvases(n_canvases)
+    k = 0
+    for e in events:
+        for cv in e.stitch.canvases:
+            want = np.zeros((1024, 1024 * 3), np.uint8)
+            for pl in cv.placements:
+                src, p = by_id[pl.patch_id]
+                cam_slot, slot = divmod(src, n + 1)
+                fr = frames[cam_slot][slot]
+                x, y, w, h = pl.position.x, pl.position.y, pl.position.w, pl.position.h
+                want[y:y + h, 3 * x:3 * (x + w)] = fr[p["y"]:p["y"] + h, 3 * p["x"]:3 * (p["x"] + w)]
+            assert np.array_equal(got[k], want), (k, e.fire_time_us)
+            k += 1
+    assert k == n_canvases
+    path.close()
