@@ -221,7 +221,9 @@ __global__ void __launch_bounds__(1024) scan_kernel(const ScanArgs a) {
     *a.id_state = first_id + static_cast<uint64_t>(run_p);
     a.canvas_base[a.n_frames] = run_c;
     long long total = run_c;
-    if (total > a.max_canvases) {
+    if (a.max_canvases == 0) {
+      total = 0;  // planning only: per-frame canvases are not materialized
+    } else if (total > a.max_canvases) {
       raise_error(a.err, TG_ERR_CAPACITY, kErrCanvasCapacity, total, a.max_canvases);
       total = a.max_canvases;
     }
