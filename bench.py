@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--frames", type=int, default=300)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="cfg2 (default, the headline): per-frame path, 1 camera x 300 frames per "
+                         "GPU; cfg3: 5 cameras batched across cameras on 1 GPU; cfg4: 64 cameras "
+                         "sharded over the ranks; cfg5: RoI-density sweep")
     return ap.parse_args()
 
 
@@ -425,10 +429,167 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+# ============================================== configs 3/4: batched cameras
+# SURVEY Appendix P3 setting: mu = 60 + 25 k ms, sigma = 0.05 mu, 1e6 Mbps
+# links, 80 GB GPU (a 4 GB model leaves room for 76 canvases per batch).
+SIM_PROFILE = [(k, 60.0 + 25.0 * k, 0.05 * (60.0 + 25.0 * k)) for k in (1, 2, 4, 8, 16, 32, 64)]
+SIM_BANDWIDTH_MBPS = 1e6
+SIM_GPU_MEMORY_GB = 80.0
+
+
+def run_multicam(args):
+    """Config 3 (5 cameras, cross-camera batching on 1 GPU) / config 4 (64
+    cameras sharded over the ranks, descriptors all-gathered).  A step:
+    K1-K4 for every camera, descriptors to the host, SLO batcher replay,
+    one K5 launch for every invoke event's canvases."""
+    rank, world, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    from paper_2404_09267_b200 import api as A
+    from paper_2404_09267_b200 import multicam as MC
+    n_cams_total = 5 if args.config == "cfg3" else 64
+    frames = min(args.frames, 300 if args.config == "cfg3" else 30)
+    cams = MC.shard_cameras(n_cams_total, world, rank)
+    ctx = A.Context(local)
+    path = MC.MultiCameraPath(ctx, cams, W, H, frames, SIM_PROFILE,
+                              bandwidth_mbps=SIM_BANDWIDTH_MBPS,
+                              gpu_memory_gb=SIM_GPU_MEMORY_GB, model_size_gb=4.0,
+                              trace_kw=dict(roi_proportion_mean=0.10, roi_max_dim=480))
+    e0, e1 = ctx.event(), ctx.event()
+
+    def step():
+        path.run_planes()
+        desc = path.descriptors()
+        if dist is not None:
+            import torch
+            MC.gather_descriptors(desc, dist, device=f"cuda:{local}")
+        path.schedule(desc)
+        return path.gather()
+
+    for _ in range(args.warmup):
+        n_canv = step()
+    ctx.stream_sync(path.stream)
+    clocks = Clocks(local)
+    if dist is not None:
+        dist.barrier()
+    ctx.synchronize()
+    clocks.start()
+    t0 = time.perf_counter()
+    ctx.record(e0, path.stream)
+    for _ in range(args.steps):
+        n_canv = step()
+    ctx.record(e1, path.stream)
+    ctx.stream_sync(path.stream)
+    clk = clocks.stop()
+    ms = ctx.elapsed_ms(e0, e1)
+    if dist is not None:
+        import torch
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    n_events = path._nev
+    out = {
+        "metric": METRIC, "value": round(len(cams) * frames * args.steps * world / (ms / 1e3), 1),
+        "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (generate_trace rects, frozen pixel spec, device-resident)",
+        "config": {"workload": f"BASELINE configs[{2 if args.config == 'cfg3' else 3}]: "
+                               f"{n_cams_total} synthetic 4K cameras, {frames} frames each, "
+                               "SLO batcher across cameras, shard-local canvases",
+                   "cameras_per_gpu": len(cams), "frames_per_camera": frames,
+                   "bandwidth_mbps": SIM_BANDWIDTH_MBPS, "profile": SIM_PROFILE,
+                   "max_canvases_per_batch": path.max_canvases,
+                   "parallelism": f"cameras sharded over {world} GPU(s)" +
+                                  (", NCCL all-gather of patch descriptors" if world > 1 else "")},
+        "batching": {"events": n_events, "canvases": n_canv,
+                     "patches_admitted": int(len(path._last["patches"]))},
+        "clocks": clk, "gpu_launches": (2 * len(cams) + 1) * args.steps,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    path.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# =================================================== config 5: density sweep
+def run_density(args):
+    """Config 5: 8 cameras (one after another on this GPU), per-frame path,
+    roi_proportion_mean in {0.01 .. 0.59}, roi_max_dim 1024; reports frames/s,
+    measured active-cell fraction, stitch efficiency and path GB/s."""
+    from paper_2404_09267_b200 import api as A
+    from paper_2404_09267_b200 import _native as N
+    ctx = A.Context(0)
+    n = min(args.frames, 60)
+    lines = []
+    for rho in (0.01, 0.05, 0.10, 0.20, 0.40, 0.59):
+        tot_ms, frames, b_run, canv_bytes, adm_bytes, act, cells = 0.0, 0, 0, 0, 0, 0, 0
+        for cam in range(8):
+            t_us, rects = A.generate_trace(n_frames=n, fps=30.0, frame_width=W, frame_height=H,
+                                           roi_proportion_mean=rho, roi_max_dim=1024,
+                                           roi_count_max=24, seed=1000 + cam)
+            ring = A.FrameRing(ctx, W, H, n)
+            ring.synthesize(A.derive_seed(1000 + cam, "pixels"), rects)
+            pipe = A.Pipeline(ctx, W, H, max_frames=n, max_canvases=n * 16)
+            d_cur, d_prev = ring.tables()
+            d_ids, d_gen = ctx.malloc(8 * n), ctx.malloc(8 * n)
+            ctx.upload(d_ids, np.arange(n, dtype=np.uint64))
+            ctx.upload(d_gen, np.array(t_us, np.int64))
+            d_canv = ctx.malloc(pipe.canvas_bytes * n * 16)
+            for _ in range(2):
+                pipe.run(n, d_cur, d_prev, d_ids, d_gen, 0, d_canv)
+            e0, e1 = ctx.event(), ctx.event()
+            ctx.synchronize()
+            ctx.record(e0)
+            for _ in range(args.steps):
+                pipe.run(n, d_cur, d_prev, d_ids, d_gen, 0, d_canv)
+            ctx.record(e1)
+            ctx.stream_sync()
+            tot_ms += ctx.elapsed_ms(e0, e1) / args.steps
+            res = pipe.results(n)
+            c = pipe.cells(n)
+            act += int((c != 0).sum())
+            cells += c.size
+            for f in range(n):
+                for j, p in enumerate(res["patch_list"][f]):
+                    if res["admitted"][f, j]:
+                        adm_bytes += p.rect.w * p.rect.h * 3
+            canv_bytes += res["total_canvases"] * pipe.canvas_bytes
+            frames += n
+            pipe.close()
+            ring.close()
+            for p in (d_ids, d_gen, d_canv):
+                ctx.free(p)
+        b_run = frames * 2 * FRAME_BYTES + adm_bytes + canv_bytes
+        lines.append({"roi_proportion_mean": rho, "frames_per_s": round(frames / (tot_ms / 1e3), 1),
+                      "active_cell_fraction": round(act / cells, 4),
+                      "stitch_efficiency": round(adm_bytes / max(1, canv_bytes), 4),
+                      "canvases_per_frame": round(canv_bytes / pipe.canvas_bytes / frames, 3),
+                      "path_GBps": round(b_run / (tot_ms / 1e3) / 1e9, 1)})
+    peak, _ = peaks()
+    out = {"metric": METRIC, "value": lines[2]["frames_per_s"], "unit": "frames/s", "n_gpus": 1,
+           "steps": args.steps, "warmup": 2, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+           "config": {"workload": "BASELINE configs[4]: RoI-density sweep, 8 synthetic 4K cameras, "
+                                  f"{n} frames each, roi_max_dim 1024", "peak_GBps": peak},
+           "sweep": lines}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config in ("cfg3", "cfg4"):
+        run_multicam(args)
+    elif args.config == "cfg5":
+        run_density(args)
     else:
         run_ours(args)
 
