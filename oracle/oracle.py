@@ -387,10 +387,11 @@ def run_tangram(scenes, width, height, profile, zones=(4, 4), canvas=(1024, 1024
     ev_np = (C.c_int32 * ecap)()
     ev_ids = (C.c_uint64 * icap)()
     nev = C.c_int32()
+    eff_mean, eff_median = C.c_double(), C.c_double()
     rc = dll.ref_run_tangram(C.byref(cfg), len(scenes), fps, t_arr, c_arr, r_arr, prof, n_prof,
                              arrival, adm, C.byref(npatch), C.c_int64(pcap), C.byref(nev), ev_fire,
                              ev_trig, ev_k, ev_slack, ev_np, ev_ids, C.c_int64(ecap),
-                             C.c_int64(icap))
+                             C.c_int64(icap), C.byref(eff_mean), C.byref(eff_median))
     if rc:
         raise OracleError(_err(dll, "ref"))
     events, k = [], 0
@@ -400,7 +401,28 @@ def run_tangram(scenes, width, height, profile, zones=(4, 4), canvas=(1024, 1024
         events.append(dict(fire_time_us=ev_fire[i], trigger=ev_trig[i], batch_size=ev_k[i],
                            estimated_slack_us=ev_slack[i], patch_ids=ids))
     return dict(admitted=[adm[i] for i in range(npatch.value)],
-                arrival_us=[arrival[i] for i in range(npatch.value)], events=events)
+                arrival_us=[arrival[i] for i in range(npatch.value)], events=events,
+                mean_canvas_efficiency=eff_mean.value, median_canvas_efficiency=eff_median.value)
+
+
+def save_trace_ref(scenes, width, height) -> str:
+    """The reference's save_trace (trace.hpp:79-90) text for scenes =
+    [(t_us list, per-frame rect lists)], scene ids cam0, cam1, ..."""
+    dll = load("ref")
+    dll.ref_save_trace.restype = C.c_int64
+    fps = (C.c_int32 * len(scenes))(*[len(t) for t, _ in scenes])
+    t_flat = [t for ts, _ in scenes for t in ts]
+    cnt = [len(f) for _, fr in scenes for f in fr]
+    rects = [r for _, fr in scenes for f in fr for r in f]
+    t_arr = (C.c_int64 * max(1, len(t_flat)))(*t_flat)
+    c_arr = (C.c_int32 * max(1, len(cnt)))(*cnt)
+    r_arr = (Rect * max(1, len(rects)))(*[Rect(*r) for r in rects])
+    cap = 64 * 1024 * 1024
+    buf = C.create_string_buffer(cap)
+    n = dll.ref_save_trace(len(scenes), fps, t_arr, c_arr, r_arr, width, height, buf, C.c_int64(cap))
+    if n < 0:
+        raise OracleError(_err(dll, "ref"))
+    return buf.raw[:n].decode()
 
 
 class RefScheduler:

@@ -200,7 +200,8 @@ int ref_run_tangram(const ref_sim_cfg* c, int n_scenes, const int32_t* frames_pe
                     const double* profile, int n_profile, int64_t* arrival_us, uint8_t* admitted,
                     int32_t* n_patches, int64_t patch_cap, int32_t* n_events, int64_t* ev_fire,
                     int32_t* ev_trigger, int32_t* ev_k, int64_t* ev_slack, int32_t* ev_npatch,
-                    uint64_t* ev_ids, int64_t ev_cap, int64_t ids_cap) {
+                    uint64_t* ev_ids, int64_t ev_cap, int64_t ids_cap, double* eff_mean,
+                    double* eff_median) {
   try {
     std::vector<tangram::TraceScene> scenes;
     int64_t fi = 0, ri = 0;
@@ -244,6 +245,8 @@ int ref_run_tangram(const ref_sim_cfg* c, int n_scenes, const int32_t* frames_pe
       arrival_us[i] = m.patches[i].admitted ? m.patches[i].arrival_us : -1;
     }
     *n_patches = static_cast<int32_t>(m.patches.size());
+    *eff_mean = m.summary.mean_canvas_efficiency;
+    *eff_median = m.summary.median_canvas_efficiency;
     std::istringstream in(log_text.str());
     std::string line;
     int64_t ne = 0, nid = 0;
@@ -268,6 +271,39 @@ int ref_run_tangram(const ref_sim_cfg* c, int n_scenes, const int32_t* frames_pe
     return 0;
   } catch (const std::exception& e) {
     return fail(e);
+  }
+}
+
+// tangram::save_trace (trace.hpp:79-90) of the given scenes; returns the
+// text length (or -1), writing up to cap bytes into out.
+int64_t ref_save_trace(int n_scenes, const int32_t* frames_per_scene, const int64_t* t_us,
+                       const int32_t* roi_counts, const orc_rect* rois, int width, int height,
+                       char* out, int64_t cap) {
+  try {
+    std::vector<tangram::TraceScene> scenes;
+    int64_t fi = 0, ri = 0;
+    for (int s = 0; s < n_scenes; ++s) {
+      tangram::TraceScene sc;
+      sc.scene_id = "cam" + std::to_string(s);
+      for (int f = 0; f < frames_per_scene[s]; ++f, ++fi) {
+        tangram::TraceFrame tf;
+        tf.frame_id = static_cast<uint64_t>(f);
+        tf.t_us = t_us[fi];
+        tf.width = width;
+        tf.height = height;
+        for (int k = 0; k < roi_counts[fi]; ++k, ++ri) tf.rois.push_back(to_rect(rois[ri]));
+        sc.frames.push_back(std::move(tf));
+      }
+      scenes.push_back(std::move(sc));
+    }
+    std::ostringstream os;
+    tangram::save_trace(os, scenes);
+    const std::string s = os.str();
+    if (static_cast<int64_t>(s.size()) <= cap) std::memcpy(out, s.data(), s.size());
+    return static_cast<int64_t>(s.size());
+  } catch (const std::exception& e) {
+    fail(e);
+    return -1;
   }
 }
 
