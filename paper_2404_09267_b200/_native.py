@@ -10,7 +10,7 @@ import os
 
 from . import build as _build
 
-LIB_PATH = _build.LIB
+LIB_PATH = os.environ.get("TANGRAM_GPU_LIB") or _build.LIB  # override: build variants
 
 TG_OK = 0
 TG_ERR_INVALID_ARGUMENT = 1

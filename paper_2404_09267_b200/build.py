@@ -40,36 +40,43 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compiles every csrc/*.cu for sm_100a and links lib/libtangram_gpu.so.
+    `defines`/`out` build tuning variants (e.g. -DTG_GATHER_PLAN_CHUNKS=4)
+    into another file, loaded with TANGRAM_GPU_LIB=<path>."""
+    target = out or LIB
+    if not force and not defines and out is None and not needs_build():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(PKG, "_obj")
+    os.makedirs(os.path.dirname(target), exist_ok=True)
+    objdir = os.path.join(PKG, "_obj" if not defines else "_obj_variant")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-               "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-dc" if False else "-c", src, "-o", obj]
+               "-I", os.path.join(ROOT, "include"), "-I", CSRC, *defines, "-c", src, "-o", obj]
         if verbose:
             cmd[1:1] = ["-Xptxas", "-v"]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
     failed = []
     for src, p in procs:
-        out, _ = p.communicate()
+        log, _ = p.communicate()
         if p.returncode != 0 or verbose:
-            sys.stderr.write(out.decode())
+            sys.stderr.write(log.decode())
         if p.returncode != 0:
             failed.append(src)
     if failed:
         raise RuntimeError("nvcc failed for: " + ", ".join(failed))
-    tmp = LIB + ".tmp"
+    tmp = target + ".tmp"
     subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", tmp, *objs])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    args = sys.argv[1:]
+    defs = [a for a in args if a.startswith("-D")]
+    out = next((a.split("=", 1)[1] for a in args if a.startswith("--out=")), None)
+    print(build(force="--force" in args, verbose="-v" in args, defines=defs, out=out))

@@ -20,11 +20,20 @@
 
 namespace tg {
 
+#ifndef TG_GATHER_PLAN_CHUNKS
+#define TG_GATHER_PLAN_CHUNKS 6
+#endif
+#ifndef TG_GATHER_MIN_BLOCKS
+#define TG_GATHER_MIN_BLOCKS 2
+#endif
+#ifndef TG_GATHER_BAND
+#define TG_GATHER_BAND 256
+#endif
+
 constexpr int kGatherThreads = 256;
 constexpr int kGatherWarps = kGatherThreads / 32;
-constexpr int kGatherBand = 256;                           // rows per unit
-constexpr int kRowsPerWarp = kGatherBand / kGatherWarps;   // contiguous rows per warp
-constexpr int kPlanChunks = 6;                             // chunks per lane per segment
+constexpr int kGatherBand = TG_GATHER_BAND;                // rows per unit
+constexpr int kPlanChunks = TG_GATHER_PLAN_CHUNKS;         // chunks per lane per segment
 constexpr int kSegChunks = 32 * kPlanChunks;               // 3 KB (one 1024-px row) per segment
 constexpr int kGatherMaxJobs = 192;                        // rects of one canvas cached in smem
 
@@ -38,8 +47,11 @@ __device__ __forceinline__ uint4 ldg128(uintptr_t p) {
   return __ldg(reinterpret_cast<const uint4*>(p));
 }
 
+// Plain (weak) global store: __stcg would emit STG.STRONG.GPU.
 __device__ __forceinline__ void stg128(uintptr_t p, const uint4& v) {
-  __stcg(reinterpret_cast<uint4*>(p), v);
+  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
 }
 
 // Bytes [s, s+16) of the 32-byte pair (v0, v1); branch-free (selects +
@@ -106,7 +118,7 @@ __device__ void copy_rect_row(uint8_t* dst, const uint8_t* src, int len, int lan
 
 enum : int { kChunkNone = 0, kChunkZero = 1, kChunkCopy = 2, kChunkMerge = 3 };
 
-__global__ void __launch_bounds__(kGatherThreads, 2) gather_kernel(const GatherArgs a) {
+__global__ void __launch_bounds__(kGatherThreads, TG_GATHER_MIN_BLOCKS) gather_kernel(const GatherArgs a) {
   __shared__ Job sj[kGatherMaxJobs];
   __shared__ RowIv siv[kGatherWarps][kGatherMaxJobs];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
