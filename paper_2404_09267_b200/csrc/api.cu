@@ -68,7 +68,7 @@ struct tg_pipeline {
   tg_ctx* ctx = nullptr;
   tg_pipeline_params p{};
   int zones = 0, cells_x = 0, cells_y = 0, act_words = 0, mask_words = 0, job_cap = 0, nbands = 0;
-  uint32_t *cells = nullptr, *active = nullptr, *mask = nullptr;
+  uint32_t *raw = nullptr, *cells = nullptr, *active = nullptr, *mask = nullptr;
   int32_t *n_rois = nullptr, *n_patches = nullptr, *n_placements = nullptr, *n_canvases = nullptr;
   tg_rect* rois = nullptr;
   tg_patch_meta* patches = nullptr;
@@ -624,7 +624,7 @@ tg_status tg_pipeline_params_default(int32_t width, int32_t height, tg_pipeline_
 void tg_pipeline_destroy(tg_pipeline* p) {
   if (!p) return;
   cudaSetDevice(p->ctx->device);
-  void* bufs[] = {p->cells, p->active, p->mask, p->n_rois, p->n_patches, p->n_placements,
+  void* bufs[] = {p->raw, p->cells, p->active, p->mask, p->n_rois, p->n_patches, p->n_placements,
                   p->n_canvases, p->rois, p->patches, p->admitted, p->placements,
                   p->canvas_base, p->jobs, p->canvas_jobs, p->ranges, p->gather_units,
                   p->id_state};
@@ -673,6 +673,7 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
     return cudaMalloc(reinterpret_cast<void**>(ptr), std::max<size_t>(1, count) * sizeof(**ptr));
   };
   cudaError_t e = cudaSuccess;
+  if (!e) e = alloc(&p->raw, F * q.height * p->mask_words);
   if (!e) e = alloc(&p->cells, F * cx * cy);
   if (!e) e = alloc(&p->active, F * cy * p->act_words);
   if (!e && q.keep_mask) e = alloc(&p->mask, F * q.height * p->mask_words);
@@ -707,7 +708,7 @@ tg_status tg_pipeline_stage_mask(tg_pipeline* p, int32_t n_frames, const uint8_t
   if (n_frames < 0 || n_frames > p->p.max_frames)
     return fail(TG_ERR_INVALID_ARGUMENT, "n_frames must be in [0, max_frames]");
   TG_CUDA(launch_mask_cells(d_cur, d_prev, n_frames, p->p.width, p->p.height, p->p.pitch,
-                            p->p.threshold, p->p.dilate_radius, p->cells, p->active,
+                            p->p.threshold, p->p.dilate_radius, p->raw, p->cells, p->active,
                             p->p.keep_mask ? p->mask : nullptr, p->ctx->sms,
                             pick(p->ctx, stream)));
   p->last_frames = n_frames;

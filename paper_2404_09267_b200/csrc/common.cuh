@@ -10,7 +10,7 @@ namespace tg {
 
 constexpr int kCell = TG_CELL_SIZE;   // 16x16-pixel patch-grid cells
 constexpr int kMaxZones = 64;         // X*Y supported by the device partitioner
-constexpr int kMaxRadius = 8;         // dilation radius bound (K1 ring sizing)
+constexpr int kMaxRadius = 8;         // dilation radius bound (K1b register window)
 
 // Device-side error latch (first error wins), read back at sync points.
 struct DevError {
@@ -93,6 +93,22 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
+}
+
+// Wait with a suspend-time hint: the warp sleeps in the barrier unit until
+// the phase completes (or the hint expires) instead of spinning on issue
+// slots its producer needs.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+  } while (!ok);
 }
 
 // Global -> shared bulk copy completing on an mbarrier (UBLKCP in SASS).

@@ -8,8 +8,8 @@ namespace tg {
 // ---- K1 (k_mask.cu) --------------------------------------------------------
 cudaError_t launch_mask_cells(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                               int n_frames, int W, int H, int pitch, int threshold, int radius,
-                              uint32_t* d_cells, uint32_t* d_active, uint32_t* d_mask, int sms,
-                              cudaStream_t stream);
+                              uint32_t* d_raw, uint32_t* d_cells, uint32_t* d_active,
+                              uint32_t* d_mask, int sms, cudaStream_t stream);
 
 // ---- K2-K4 per-frame planner + scan (k_plan.cu) ----------------------------
 struct PlanArgs {
