@@ -197,9 +197,14 @@ tg_status tg_pipeline_run(tg_pipeline* p, int32_t n_frames, const uint8_t* const
                           const int64_t* d_gen_us, uint64_t first_patch_id,
                           uint8_t* d_canvases, void* stream);
 
-/* The same stages one by one (parity tests, profiling). */
+/* The same stages one by one (parity tests, profiling).  stage_mask =
+ * stage_mask_fg (K1: raw foreground bitmap) + stage_mask_cells (K1b:
+ * dilation + cell summaries). */
 tg_status tg_pipeline_stage_mask(tg_pipeline* p, int32_t n_frames, const uint8_t* const* d_cur,
                                  const uint8_t* const* d_prev, void* stream);
+tg_status tg_pipeline_stage_mask_fg(tg_pipeline* p, int32_t n_frames, const uint8_t* const* d_cur,
+                                    const uint8_t* const* d_prev, void* stream);
+tg_status tg_pipeline_stage_mask_cells(tg_pipeline* p, int32_t n_frames, void* stream);
 tg_status tg_pipeline_stage_plan(tg_pipeline* p, int32_t n_frames, const uint64_t* d_frame_ids,
                                  const int64_t* d_gen_us, uint64_t first_patch_id, void* stream);
 tg_status tg_pipeline_stage_gather(tg_pipeline* p, int32_t n_frames,

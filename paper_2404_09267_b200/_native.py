@@ -138,6 +138,8 @@ SIGNATURES = {
     "tg_pipeline_destroy": (None, [vp]),
     "tg_pipeline_run": (st, [vp, i32, vp, vp, vp, vp, u64, vp, vp]),
     "tg_pipeline_stage_mask": (st, [vp, i32, vp, vp, vp]),
+    "tg_pipeline_stage_mask_fg": (st, [vp, i32, vp, vp, vp]),
+    "tg_pipeline_stage_mask_cells": (st, [vp, i32, vp]),
     "tg_pipeline_stage_plan": (st, [vp, i32, vp, vp, u64, vp]),
     "tg_pipeline_stage_gather": (st, [vp, i32, vp, vp, vp]),
     "tg_pipeline_graph_create": (st, [vp, i32, vp, vp, vp, vp, u64, vp, vp, P(vp)]),

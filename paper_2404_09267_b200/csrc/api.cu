@@ -701,18 +701,36 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
   return TG_OK;
 }
 
-tg_status tg_pipeline_stage_mask(tg_pipeline* p, int32_t n_frames, const uint8_t* const* d_cur,
-                                 const uint8_t* const* d_prev, void* stream) {
+tg_status tg_pipeline_stage_mask_fg(tg_pipeline* p, int32_t n_frames, const uint8_t* const* d_cur,
+                                    const uint8_t* const* d_prev, void* stream) {
   tg_status s = use_device(p->ctx);
   if (s) return s;
   if (n_frames < 0 || n_frames > p->p.max_frames)
     return fail(TG_ERR_INVALID_ARGUMENT, "n_frames must be in [0, max_frames]");
-  TG_CUDA(launch_mask_cells(d_cur, d_prev, n_frames, p->p.width, p->p.height, p->p.pitch,
-                            p->p.threshold, p->p.dilate_radius, p->raw, p->cells, p->active,
-                            p->p.keep_mask ? p->mask : nullptr, p->ctx->sms,
-                            pick(p->ctx, stream)));
+  if (n_frames > 0 && (!d_cur || !d_prev))
+    return fail(TG_ERR_INVALID_ARGUMENT, "null frame pointer table");
+  TG_CUDA(launch_mask_fg(d_cur, d_prev, n_frames, p->p.width, p->p.height, p->p.pitch,
+                         p->p.threshold, p->raw, p->ctx->sms, pick(p->ctx, stream)));
+  return TG_OK;
+}
+
+tg_status tg_pipeline_stage_mask_cells(tg_pipeline* p, int32_t n_frames, void* stream) {
+  tg_status s = use_device(p->ctx);
+  if (s) return s;
+  if (n_frames < 0 || n_frames > p->p.max_frames)
+    return fail(TG_ERR_INVALID_ARGUMENT, "n_frames must be in [0, max_frames]");
+  TG_CUDA(launch_dilate_cells(p->raw, n_frames, p->p.width, p->p.height, p->p.dilate_radius,
+                              p->cells, p->active, p->p.keep_mask ? p->mask : nullptr,
+                              pick(p->ctx, stream)));
   p->last_frames = n_frames;
   return TG_OK;
+}
+
+tg_status tg_pipeline_stage_mask(tg_pipeline* p, int32_t n_frames, const uint8_t* const* d_cur,
+                                 const uint8_t* const* d_prev, void* stream) {
+  tg_status s = tg_pipeline_stage_mask_fg(p, n_frames, d_cur, d_prev, stream);
+  if (!s) s = tg_pipeline_stage_mask_cells(p, n_frames, stream);
+  return s;
 }
 
 tg_status tg_pipeline_stage_plan(tg_pipeline* p, int32_t n_frames, const uint64_t* d_frame_ids,

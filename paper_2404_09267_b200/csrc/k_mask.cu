@@ -312,6 +312,19 @@ __global__ void __launch_bounds__(256) dilate_cells_kernel(const DilateArgs a) {
       for (int i = 2 * R; i < kWin; ++i) win[i] = raw_row(yb0 - R + i);
     }
     const int nrow = min(kCell, a.H - yb0);
+    uint32_t any = 0;
+#pragma unroll
+    for (int i = 0; i < kWin; ++i) any |= win[i];
+    if (!a.mask_out && !__any_sync(0xffffffffu, any != 0)) {  // empty band tile: zero cells
+      if (owns) {
+        const size_t cbase = (static_cast<size_t>(f) * a.cells_y + cy0 + bi) * a.cells_x;
+        a.cells[cbase + 2 * w] = 0u;
+        if (2 * w + 1 < a.cells_x) a.cells[cbase + 2 * w + 1] = 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < 2 * R; ++i) win[i] = win[kCell + i];
+      continue;
+    }
     int occ = 0, occ_hi = 0;
     uint32_t cols = 0, row_lo = 0, row_hi = 0;
 #pragma unroll
@@ -359,10 +372,9 @@ static int env_int(const char* name, int dflt) {
   return e ? std::atoi(e) : dflt;
 }
 
-cudaError_t launch_mask_cells(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
-                              int n_frames, int W, int H, int pitch, int threshold, int radius,
-                              uint32_t* d_raw, uint32_t* d_cells, uint32_t* d_active,
-                              uint32_t* d_mask, int sms, cudaStream_t stream) {
+cudaError_t launch_mask_fg(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
+                           int n_frames, int W, int H, int pitch, int threshold, uint32_t* d_raw,
+                           int sms, cudaStream_t stream) {
   if (n_frames <= 0) return cudaSuccess;
   MaskArgs a;
   a.cur = d_cur;
@@ -402,14 +414,18 @@ cudaError_t launch_mask_cells(const uint8_t* const* d_cur, const uint8_t* const*
     mask_fg_kernel<true><<<grid, kK1Threads, smem, stream>>>(a);
   else
     mask_fg_kernel<false><<<grid, kK1Threads, smem, stream>>>(a);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
 
+cudaError_t launch_dilate_cells(const uint32_t* d_raw, int n_frames, int W, int H, int radius,
+                                uint32_t* d_cells, uint32_t* d_active, uint32_t* d_mask,
+                                cudaStream_t stream) {
+  if (n_frames <= 0) return cudaSuccess;
   DilateArgs d;
   d.raw = d_raw;
   d.H = H;
   d.W = W;
-  d.nwords = a.nwords;
+  d.nwords = ceil_div(W, 32);
   d.cells_x = ceil_div(W, kCell);
   d.cells_y = ceil_div(H, kCell);
   d.act_words = ceil_div(d.cells_x, 32);
@@ -417,7 +433,7 @@ cudaError_t launch_mask_cells(const uint8_t* const* d_cur, const uint8_t* const*
   d.cells = d_cells;
   d.active = d_active;
   d.mask_out = d_mask;
-  const int dwarps = ceil_div(a.nwords, kK1GroupWords);
+  const int dwarps = ceil_div(d.nwords, kK1GroupWords);
   const dim3 dg(n_frames * ceil_div(d.cells_y, kK1bBands)), db(dwarps * 32);
   switch (radius) {
 #define TG_DILATE_CASE(R) \

@@ -6,10 +6,12 @@
 namespace tg {
 
 // ---- K1 (k_mask.cu) --------------------------------------------------------
-cudaError_t launch_mask_cells(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
-                              int n_frames, int W, int H, int pitch, int threshold, int radius,
-                              uint32_t* d_raw, uint32_t* d_cells, uint32_t* d_active,
-                              uint32_t* d_mask, int sms, cudaStream_t stream);
+cudaError_t launch_mask_fg(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
+                           int n_frames, int W, int H, int pitch, int threshold, uint32_t* d_raw,
+                           int sms, cudaStream_t stream);
+cudaError_t launch_dilate_cells(const uint32_t* d_raw, int n_frames, int W, int H, int radius,
+                                uint32_t* d_cells, uint32_t* d_active, uint32_t* d_mask,
+                                cudaStream_t stream);
 
 // ---- K2-K4 per-frame planner + scan (k_plan.cu) ----------------------------
 struct PlanArgs {

@@ -35,7 +35,8 @@ def launches():
                       h.index("ID"))
     d = defaultdict(dict)
     for r in rows[hdr + 1:]:
-        d[(int(r[ii]), r[ki].split("(")[0])][r[mi]] = float(r[vi].replace(",", ""))
+        name = r[ki].split("(")[0].replace("void ", "")
+        d[(int(r[ii]), name)][r[mi]] = float(r[vi].replace(",", ""))
     return d
 
 
@@ -87,12 +88,12 @@ def main(tag):
         wr = sum(m["dram__bytes_write.sum"] for m in ms) / len(ms)
         lines.append(f"| {name} | {len(ms)} | {t:.4f} | {rd/1e9:.3f} | {wr/1e9:.3f} | "
                      f"{(rd+wr)/t/1e6:.0f} |")
-        if name == "mask_cells_kernel":
+        if name.startswith("mask_fg_kernel"):
             k1 = dict(ms=t, read=rd, write=wr)
     total = sum(sum(m["gpu__time_duration.sum"] for m in ms) / len(ms)
                 for n, ms in per.items() if not n.startswith("synth"))
     lines += ["", f"Step total (sum of mean kernel times): {total/1e6:.4f} ms", ""]
-    for kern in ("mask_cells", "plan_kernel", "gather_kernel"):
+    for kern in ("mask_fg", "dilate", "plan_kernel", "gather_kernel"):
         rep = os.path.join(OUT, f"prof_{kern}.ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -110,9 +111,10 @@ def main(tag):
         f.write("\n".join(lines) + "\n")
     if k1:
         traffic = k1["read"] + k1["write"]
-        json.dump({"kernel": "mask_cells_kernel", "frames_per_launch": FRAMES,
+        raw = 2160 * 120 * 4
+        json.dump({"kernel": "mask_fg_kernel", "frames_per_launch": FRAMES,
                    "dram_bytes_per_launch": traffic, "dram_bytes_per_frame": traffic / FRAMES,
-                   "algorithmic_bytes_per_frame": 2 * FRAME_BYTES,
+                   "algorithmic_bytes_per_launch": (FRAMES + 1) * FRAME_BYTES + FRAMES * raw,
                    "source": f"profiles/{tag}_launches.csv"},
                   open(os.path.join(PROF, "k1_traffic.json"), "w"), indent=1)
     print("\n".join(lines))
