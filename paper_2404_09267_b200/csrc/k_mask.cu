@@ -273,7 +273,7 @@ __device__ __forceinline__ uint32_t pack_cell(int occ, uint32_t cols, uint32_t r
 constexpr int kK1bBands = 4;  // cell bands per K1b CTA (a 64-row strip)
 
 template <int R>  // dilation radius
-__global__ void __launch_bounds__(256) dilate_cells_kernel(const DilateArgs a) {
+__global__ void __launch_bounds__(320) dilate_cells_kernel(const DilateArgs a) {  // W <= 8192: <= 9 warps
   __shared__ uint32_t act_s[kK1bBands][kK1MaxActWords];
   const int strips = ceil_div(a.cells_y, kK1bBands);
   const int f = blockIdx.x / strips, cy0 = (blockIdx.x - f * strips) * kK1bBands;

@@ -346,6 +346,8 @@ def test_round_trip_fixture(ctx):
     dict(W=1280, H=720, n=4, zones=(8, 8)),
     dict(W=1280, H=720, n=4, zones=(3, 5), canvas=(300, 200)),
     dict(W=640, H=352, n=3, pitch=640 * 3 + 64),       # padded rows
+    dict(W=8192, H=48, n=3),                           # 4 K1 parts per row, 2 rows per item
+    dict(W=2080, H=70, n=5),                           # 65 words: two uneven K1 parts
     dict(W=1920, H=1080, n=6, trace_kw=dict(roi_proportion_mean=0.59, roi_max_dim=1080,
                                             roi_count_max=30)),  # dense, oversize patches
 ])
@@ -357,6 +359,40 @@ def test_pipeline_edge_cases(ctx, case):
     gpu = run.run()
     orc = run.oracle()
     _compare_full(run, gpu, orc)
+    run.close()
+
+
+def test_pipeline_broken_frame_chains(ctx):
+    """prev[i] need not be cur[i-1]: K1 restarts its frame chain wherever the
+    pointer tables break it (a prev that is some other frame, the frame itself,
+    the background slot)."""
+    W, H, n = 1280, 720, 7
+    run = GpuRun(ctx, W, H, n, seed=11, trace_kw=dict(roi_max_dim=400))
+    slots = run.ring.slots
+    cur_slot = [i + 1 for i in range(n)]
+    prev_slot = [0, 1, 0, 3, 5, 5, 2]  # chain, chain, break, chain, self, chain, break
+    d_cur, d_prev = ctx.malloc(8 * n), ctx.malloc(8 * n)
+    ctx.upload(d_cur, np.array([slots[s] for s in cur_slot], np.uint64))
+    ctx.upload(d_prev, np.array([slots[s] for s in prev_slot], np.uint64))
+    run.pipe.run(n, d_cur, d_prev, run.d_ids, run.d_gen, 0, run.d_canvases)
+    gpu = run.pipe.results(n)
+    frames = run.host_frames()
+    gm = run.pipe.mask(n)
+    for i in range(n):
+        om = O.mask(frames[cur_slot[i]], frames[prev_slot[i]], W, H, run.threshold, run.radius)
+        assert np.array_equal(gm[i], om), f"mask frame {i}"
+    params = oracle_params(W, H, run.radius, run.threshold, run.zones, run.canvas, run.max_rois,
+                           pitch=run.ring.pitch)
+    orc = O.process_frames(params, [frames[s] for s in cur_slot], [frames[s] for s in prev_slot],
+                           list(range(n)), run.t_us, 0, want_canvases=True, want_cells=True)
+    assert np.array_equal(run.pipe.cells(n), orc["cells"])
+    assert patch_tuples(gpu["patch_list"]) == oracle_patch_tuples(orc["patch_list"])
+    assert gpu["placement_list"] == orc["placement_list"]
+    assert gpu["total_canvases"] == orc["total_canvases"]
+    got = ctx.download(run.d_canvases, (gpu["total_canvases"], 1024, 3072), np.uint8)
+    assert np.array_equal(got, orc["canvases"][:orc["total_canvases"]])
+    for d in (d_cur, d_prev):
+        ctx.free(d)
     run.close()
 
 
