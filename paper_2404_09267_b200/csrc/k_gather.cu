@@ -114,10 +114,16 @@ __device__ __forceinline__ uint4 window16(uintptr_t p, int need_lo, int need_hi)
   return realign(v0, use1 ? ldg128(q + 16) : z, s);
 }
 
-// 16 bytes at ring offset aa (may be up to 15 below the item start).
+// 16 bytes at ring offset aa (may be up to 15 below the item start): five
+// word loads from the 4-byte-aligned address + four funnel shifts (fewer
+// instructions than two aligned LDS.128 + word selects; the 4-way bank
+// conflict of 16-byte-strided lanes is affordable at this byte rate).
 __device__ __forceinline__ uint4 ring16(const uint8_t* ring, int aa) {
-  const uint8_t* p0 = ring + (aa & ~15);
-  return realign(lds128(p0), lds128(p0 + 16), aa & 15);
+  const uint32_t* p = reinterpret_cast<const uint32_t*>(ring + (aa & ~3));
+  const int sh = 8 * (aa & 3);
+  const uint32_t w0 = p[0], w1 = p[1], w2 = p[2], w3 = p[3], w4 = p[4];
+  return make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh),
+                    __funnelshift_r(w2, w3, sh), __funnelshift_r(w3, w4, sh));
 }
 
 // x << n with n >= 32 giving 0 (PTX shl clamps the shift amount).
