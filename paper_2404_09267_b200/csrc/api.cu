@@ -69,6 +69,7 @@ struct tg_pipeline {
   tg_pipeline_params p{};
   int zones = 0, cells_x = 0, cells_y = 0, act_words = 0, mask_words = 0, job_cap = 0, nbands = 0;
   uint32_t *raw = nullptr, *cells = nullptr, *active = nullptr, *mask = nullptr;
+  uint32_t* mask_sync = nullptr;  // fused K1/K1b launch: item counters + task queue
   int32_t *n_rois = nullptr, *n_patches = nullptr, *n_placements = nullptr, *n_canvases = nullptr;
   tg_rect* rois = nullptr;
   tg_patch_meta* patches = nullptr;
@@ -624,7 +625,7 @@ tg_status tg_pipeline_params_default(int32_t width, int32_t height, tg_pipeline_
 void tg_pipeline_destroy(tg_pipeline* p) {
   if (!p) return;
   cudaSetDevice(p->ctx->device);
-  void* bufs[] = {p->raw, p->cells, p->active, p->mask, p->n_rois, p->n_patches, p->n_placements,
+  void* bufs[] = {p->raw, p->mask_sync, p->cells, p->active, p->mask, p->n_rois, p->n_patches, p->n_placements,
                   p->n_canvases, p->rois, p->patches, p->admitted, p->placements,
                   p->canvas_base, p->jobs, p->canvas_jobs, p->ranges, p->gather_units,
                   p->id_state};
@@ -674,6 +675,7 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
   };
   cudaError_t e = cudaSuccess;
   if (!e) e = alloc(&p->raw, F * q.height * p->mask_words);
+  if (!e) e = alloc(&p->mask_sync, mask_sync_words(q.height, ctx->sms));
   if (!e) e = alloc(&p->cells, F * cx * cy);
   if (!e) e = alloc(&p->active, F * cy * p->act_words);
   if (!e && q.keep_mask) e = alloc(&p->mask, F * q.height * p->mask_words);
@@ -728,7 +730,26 @@ tg_status tg_pipeline_stage_mask_cells(tg_pipeline* p, int32_t n_frames, void* s
 
 tg_status tg_pipeline_stage_mask(tg_pipeline* p, int32_t n_frames, const uint8_t* const* d_cur,
                                  const uint8_t* const* d_prev, void* stream) {
-  tg_status s = tg_pipeline_stage_mask_fg(p, n_frames, d_cur, d_prev, stream);
+  tg_status s = use_device(p->ctx);
+  if (s) return s;
+  if (n_frames < 0 || n_frames > p->p.max_frames)
+    return fail(TG_ERR_INVALID_ARGUMENT, "n_frames must be in [0, max_frames]");
+  if (n_frames > 0 && (!d_cur || !d_prev))
+    return fail(TG_ERR_INVALID_ARGUMENT, "null frame pointer table");
+  // K1 + K1b in one cooperative launch; separate launches if the device
+  // cannot co-schedule one K1 CTA per SM (e.g. a shared GPU).
+  const cudaError_t e = launch_mask_fused(
+      d_cur, d_prev, n_frames, p->p.width, p->p.height, p->p.pitch, p->p.threshold,
+      p->p.dilate_radius, p->raw, p->cells, p->active, p->p.keep_mask ? p->mask : nullptr,
+      p->mask_sync, p->ctx->sms, pick(p->ctx, stream));
+  if (e == cudaSuccess) {
+    p->last_frames = n_frames;
+    return TG_OK;
+  }
+  if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported)
+    return cuda_fail(e, "launch_mask_fused");
+  cudaGetLastError();
+  s = tg_pipeline_stage_mask_fg(p, n_frames, d_cur, d_prev, stream);
   if (!s) s = tg_pipeline_stage_mask_cells(p, n_frames, stream);
   return s;
 }

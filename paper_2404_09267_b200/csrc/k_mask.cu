@@ -24,10 +24,19 @@
 //    PRMT planar regroup); this row stays in registers as the next `prev`.
 //  * Raw words go to global memory (1 bit/pixel: 1/24 of the frame bytes).
 //
-// K1b (dilate_cells_kernel) -- one CTA per (frame, 16-row cell band): vertical
-// OR over 2r+1 raw rows, horizontal funnel shifts with neighbour words from
-// adjacent lanes, per-cell popcounts and bbox bit-masks -> packed u32 cell
-// summaries plus an activity bitmask (and the dilated mask on request).
+// K1b (dilate_strip) -- per (frame, 64-row strip, 30-word column group) warp
+// task: vertical OR over 2r+1 raw rows, horizontal funnel shifts with
+// neighbour words from adjacent lanes, per-cell popcounts and bbox bit-masks
+// -> packed u32 cell summaries plus an activity bitmask (and the dilated mask
+// on request).
+//
+// Fused launch (launch_mask_fused, the pipeline's mask stage): K1 CTAs carry
+// 3 extra warps that run the K1b tasks while K1 streams.  K1 is HBM bound and
+// leaves issue slots idle; a task starts once every K1 item covering its rows
+// has published completion (per-item counters, release/acquire), reads the
+// freshly written raw rows from L2, and the last strips are finished by all
+// warps after the stream ends.  Cooperative launch guarantees that all CTAs
+// are co-resident, so waiting on other CTAs' items cannot deadlock.
 #include <algorithm>
 #include <cstdlib>
 
@@ -39,10 +48,139 @@ constexpr int kK1MaxPartWords = 64;     // 32-pixel words per unit (one per cons
 constexpr int kK1Group = 2;             // warps per consumer group
 constexpr int kK1Groups = 8;            // consumer groups (units per item)
 constexpr int kK1MaxSlots = 8;          // ring slots per group
-constexpr int kK1Threads = (kK1Groups * kK1Group + 1) * 32;
+constexpr int kK1DilateWarps = 3;       // fused launch: warps running K1b tasks (20 warps: 96 regs)
+constexpr int kK1Threads = (kK1Groups * kK1Group + 1 + kK1DilateWarps) * 32;
+constexpr int kK1bBands = 4;            // cell bands per K1b task (a 64-row strip)
 constexpr int kK1SmemBudget = 227 * 1024;
 constexpr int kK1GroupWords = 30;       // K1b: output words per warp (lanes 1..30)
 constexpr int kK1MaxActWords = 16;      // K1b: act words per cell row (W <= 8192)
+
+// ---- K1b: dilation + cell summaries ---------------------------------------
+struct DilateArgs {
+  const uint32_t* raw;
+  int H, W, nwords, cells_x, cells_y, act_words;
+  uint32_t* cells;
+  uint32_t* active;
+  uint32_t* mask_out;
+};
+
+__device__ __forceinline__ uint32_t pack_cell(int occ, uint32_t cols, uint32_t rows) {
+  if (occ == 0) return 0u;
+  const uint32_t x0 = __ffs(cols) - 1, x1 = 31 - __clz(cols);
+  const uint32_t y0 = __ffs(rows) - 1, y1 = 31 - __clz(rows);
+  return static_cast<uint32_t>(occ) | x0 << 9 | x1 << 13 | y0 << 17 | y1 << 21;
+}
+
+// One warp: frame f, cell rows cy0 .. cy0+3, words [30*wi - 1, 30*wi + 31)
+// (lanes 1..30 own a word, lanes 0/31 are the neighbours).  kFused: raw rows
+// were written by other SMs during this launch -> L2 loads (ld.cg), activity
+// bits straight to global (zeroed before the launch); otherwise the CTA's
+// act_s collects them.
+template <int R, bool kFused>
+__device__ __forceinline__ void dilate_strip(const DilateArgs& a, int f, int cy0, int wi, int lane,
+                                             uint32_t (*act_s)[kK1MaxActWords]) {
+  const int nb = min(kK1bBands, a.cells_y - cy0);
+  const uint32_t lastmask = (a.W & 31) ? ((1u << (a.W & 31)) - 1u) : 0xffffffffu;
+  const int w = wi * kK1GroupWords + lane - 1;
+  const bool col_ok = w >= 0 && w < a.nwords;
+  const bool owns = lane >= 1 && lane <= kK1GroupWords && col_ok;
+  // bits this lane keeps: its own word, minus pixels past the frame edge
+  const uint32_t keep = owns ? (w == a.nwords - 1 ? lastmask : 0xffffffffu) : 0u;
+  const int wc = min(max(w, 0), a.nwords - 1);  // clamped column: loads stay in bounds
+  const uint32_t cmask = col_ok ? 0xffffffffu : 0u;
+  const uint32_t* fr = a.raw + static_cast<size_t>(f) * a.H * a.nwords + wc;
+  auto ld = [](const uint32_t* q) -> uint32_t { return kFused ? __ldcg(q) : __ldg(q); };
+  // rows outside [0, H) read a clamped row and are masked to zero
+  auto raw_row = [&](int yy) -> uint32_t {
+    const uint32_t m = (yy >= 0 && yy < a.H) ? cmask : 0u;
+    return ld(fr + static_cast<size_t>(min(max(yy, 0), a.H - 1)) * a.nwords) & m;
+  };
+  // window of raw rows yb0 - R .. yb0 + 15 + R; consecutive bands share 2R rows
+  constexpr int kWin = kCell + 2 * R;
+  uint32_t win[kWin];
+#pragma unroll
+  for (int i = 0; i < 2 * R; ++i) win[i] = raw_row(cy0 * kCell - R + i);
+  for (int bi = 0; bi < nb; ++bi) {
+    const int yb0 = (cy0 + bi) * kCell, cy = cy0 + bi;
+    const bool interior = yb0 + kCell + R <= a.H;  // uniform: no row past the frame
+    if (interior) {
+      const uint32_t* q = fr + static_cast<size_t>(yb0 + R) * a.nwords;
+#pragma unroll
+      for (int i = 2 * R; i < kWin; ++i) win[i] = ld(q + static_cast<size_t>(i - 2 * R) * a.nwords) & cmask;
+    } else {
+#pragma unroll
+      for (int i = 2 * R; i < kWin; ++i) win[i] = raw_row(yb0 - R + i);
+    }
+    const int nrow = min(kCell, a.H - yb0);
+    const size_t cbase = (static_cast<size_t>(f) * a.cells_y + cy) * a.cells_x;
+    uint32_t any = 0;
+#pragma unroll
+    for (int i = 0; i < kWin; ++i) any |= win[i];
+    if (!a.mask_out && !__any_sync(0xffffffffu, any != 0)) {  // empty band tile: zero cells
+      if (owns) {
+        a.cells[cbase + 2 * w] = 0u;
+        if (2 * w + 1 < a.cells_x) a.cells[cbase + 2 * w + 1] = 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < 2 * R; ++i) win[i] = win[kCell + i];
+      continue;
+    }
+    int occ = 0, occ_hi = 0;
+    uint32_t cols = 0, row_lo = 0, row_hi = 0;
+#pragma unroll
+    for (int ly = 0; ly < kCell; ++ly) {
+      uint32_t v = win[ly];
+#pragma unroll
+      for (int k = 1; k <= 2 * R; ++k) v |= win[ly + k];
+      const uint32_t vm = __shfl_up_sync(0xffffffffu, v, 1);
+      const uint32_t vp = __shfl_down_sync(0xffffffffu, v, 1);
+      uint32_t d = v;
+#pragma unroll
+      for (int k = 1; k <= R; ++k) d |= __funnelshift_r(v, vp, k) | __funnelshift_l(vm, v, k);
+      d &= ly < nrow ? keep : 0u;
+      if (a.mask_out && owns && ly < nrow)
+        a.mask_out[(static_cast<size_t>(f) * a.H + yb0 + ly) * a.nwords + w] = d;
+      const uint32_t dh = d >> 16;
+      occ += __popc(d);
+      occ_hi += __popc(dh);
+      cols |= d;
+      row_lo += min(d & 0xffffu, 1u) << ly;
+      row_hi += min(dh, 1u) << ly;
+    }
+#pragma unroll
+    for (int i = 0; i < 2 * R; ++i) win[i] = win[kCell + i];
+    if (owns) {
+      const int cx = 2 * w;
+      const int occ_lo = occ - occ_hi;
+      a.cells[cbase + cx] = pack_cell(occ_lo, cols & 0xffffu, row_lo);
+      if (cx + 1 < a.cells_x) a.cells[cbase + cx + 1] = pack_cell(occ_hi, cols >> 16, row_hi);
+      const uint32_t bits = (occ_lo > 0 ? 1u : 0u) | (occ_hi > 0 ? 2u : 0u);
+      if (bits) {
+        if (kFused)
+          atomicOr(&a.active[(static_cast<size_t>(f) * a.cells_y + cy) * a.act_words + (cx >> 5)],
+                   bits << (cx & 31));
+        else
+          atomicOr(&act_s[bi][cx >> 5], bits << (cx & 31));
+      }
+    }
+  }
+}
+
+template <int R>  // dilation radius
+__global__ void __launch_bounds__(320) dilate_cells_kernel(const DilateArgs a) {  // W <= 8192: <= 9 warps
+  __shared__ uint32_t act_s[kK1bBands][kK1MaxActWords];
+  const int strips = ceil_div(a.cells_y, kK1bBands);
+  const int f = blockIdx.x / strips, cy0 = (blockIdx.x - f * strips) * kK1bBands;
+  const int nb = min(kK1bBands, a.cells_y - cy0);
+  for (int i = threadIdx.x; i < kK1bBands * kK1MaxActWords; i += blockDim.x) (&act_s[0][0])[i] = 0;
+  __syncthreads();
+  dilate_strip<R, false>(a, f, cy0, threadIdx.x >> 5, threadIdx.x & 31, act_s);
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb * a.act_words; i += blockDim.x) {
+    const int bi = i / a.act_words, aw = i - bi * a.act_words;
+    a.active[(static_cast<size_t>(f) * a.cells_y + cy0 + bi) * a.act_words + aw] = act_s[bi][aw];
+  }
+}
 
 struct MaskArgs {
   const uint8_t* const* cur;
@@ -56,6 +194,11 @@ struct MaskArgs {
   int nslots;         // ring slots per group
   int slot_bytes;
   uint32_t* raw;      // [F][H][nwords] raw foreground bits
+  // fused launch only (item_done == nullptr otherwise)
+  uint32_t* item_done;  // [total_items] warps done per item (zeroed)
+  uint32_t* task_next;  // K1b task queue head (zeroed)
+  int radius, dgroups, strips, n_tasks;
+  DilateArgs d;
 };
 
 // Per-byte "d > T" flag in bit 7 of each byte, SWAR without cross-byte
@@ -155,6 +298,48 @@ __device__ __forceinline__ ItemK1 load_item(const MaskArgs& a, int item) {
   return it;
 }
 
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Fused launch: K1b tasks (strip, frame, column group) in strip order, each
+// after the K1 items that write its rows have published completion.
+__device__ void run_dilate_tasks(const MaskArgs& a, int lane) {
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = static_cast<int>(atomicAdd(a.task_next, 1u));
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= a.n_tasks) return;
+    const int wi = t % a.dgroups, sf = t / a.dgroups;
+    const int f = sf % a.n_frames, sg = sf / a.n_frames;
+    const int cy0 = sg * kK1bBands;
+    const int y_lo = max(0, cy0 * kCell - a.radius);
+    const int y_hi = min(a.H, (cy0 + kK1bBands) * kCell + a.radius) - 1;
+    const int run = f / a.kf;
+    for (int rb = y_lo / a.rows_per_item + lane; rb <= y_hi / a.rows_per_item; rb += 32) {
+      const int rows = min(a.rows_per_item, a.H - rb * a.rows_per_item);
+      const uint32_t want = static_cast<uint32_t>(kK1Group * a.nparts * rows);
+      const uint32_t* flag = a.item_done + rb * a.ntg + run;
+      while (ld_acquire(flag) < want) __nanosleep(256);
+    }
+    __syncwarp();
+    __threadfence();
+    switch (a.radius) {
+#define TG_DILATE_TASK(R) \
+  case R:                 \
+    dilate_strip<R, true>(a.d, f, cy0, wi, lane, nullptr); \
+    break;
+      TG_DILATE_TASK(0) TG_DILATE_TASK(1) TG_DILATE_TASK(2) TG_DILATE_TASK(3) TG_DILATE_TASK(4)
+      TG_DILATE_TASK(5) TG_DILATE_TASK(6) TG_DILATE_TASK(7) TG_DILATE_TASK(8)
+#undef TG_DILATE_TASK
+      default:
+        break;
+    }
+  }
+}
+
 template <bool kLow>
 __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -174,7 +359,12 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
   }
   __syncthreads();
   const int part_bytes = a.part_words * 96;
+  const bool fused = a.item_done != nullptr;
 
+  if (warp > kK1Groups * kK1Group) {  // K1b task warps (fused launch)
+    if (fused) run_dilate_tasks(a, lane);
+    return;
+  }
   if (warp == kK1Groups * kK1Group) {
     // ===== producer: lane g streams group g's unit down the frame chain =====
     const int g = lane;
@@ -210,6 +400,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
         if (!__any_sync(0xffffffffu, issued)) __nanosleep(64);
       }
     }
+    if (fused) run_dilate_tasks(a, lane);
     return;
   }
 
@@ -222,8 +413,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
   const bool in_slot = 96 * (col + 1) <= a.slot_bytes;  // lane's bytes inside a slot
   uint32_t fpar = 0;  // bit k: parity of the next full phase of ring slot k
   int k = 0;
-  if (g >= units) return;
-  for (int item = blockIdx.x; item < a.total_items; item += gridDim.x) {
+  for (int item = blockIdx.x; g < units && item < a.total_items; item += gridDim.x) {
     const ItemK1 it = load_item(a, item);
     const int row = it.y0 + g / a.nparts, part = g % a.nparts;
     if (row >= a.H) continue;
@@ -251,119 +441,13 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
 #pragma unroll
       for (int q = 0; q < 6; ++q) P[q] = C[q];
     }
-  }
-}
-
-// ---- K1b: dilation + cell summaries ---------------------------------------
-struct DilateArgs {
-  const uint32_t* raw;
-  int H, W, nwords, cells_x, cells_y, act_words;
-  uint32_t* cells;
-  uint32_t* active;
-  uint32_t* mask_out;
-};
-
-__device__ __forceinline__ uint32_t pack_cell(int occ, uint32_t cols, uint32_t rows) {
-  if (occ == 0) return 0u;
-  const uint32_t x0 = __ffs(cols) - 1, x1 = 31 - __clz(cols);
-  const uint32_t y0 = __ffs(rows) - 1, y1 = 31 - __clz(rows);
-  return static_cast<uint32_t>(occ) | x0 << 9 | x1 << 13 | y0 << 17 | y1 << 21;
-}
-
-constexpr int kK1bBands = 4;  // cell bands per K1b CTA (a 64-row strip)
-
-template <int R>  // dilation radius
-__global__ void __launch_bounds__(320) dilate_cells_kernel(const DilateArgs a) {  // W <= 8192: <= 9 warps
-  __shared__ uint32_t act_s[kK1bBands][kK1MaxActWords];
-  const int strips = ceil_div(a.cells_y, kK1bBands);
-  const int f = blockIdx.x / strips, cy0 = (blockIdx.x - f * strips) * kK1bBands;
-  const int nb = min(kK1bBands, a.cells_y - cy0);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < kK1bBands * kK1MaxActWords; i += blockDim.x) (&act_s[0][0])[i] = 0;
-  __syncthreads();
-  const uint32_t lastmask = (a.W & 31) ? ((1u << (a.W & 31)) - 1u) : 0xffffffffu;
-  const int w = warp * kK1GroupWords + lane - 1;
-  const bool col_ok = w >= 0 && w < a.nwords;
-  const bool owns = lane >= 1 && lane <= kK1GroupWords && col_ok;
-  // bits this lane keeps: its own word, minus pixels past the frame edge
-  const uint32_t keep = owns ? (w == a.nwords - 1 ? lastmask : 0xffffffffu) : 0u;
-  const int wc = min(max(w, 0), a.nwords - 1);  // clamped column: loads stay in bounds
-  const uint32_t cmask = col_ok ? 0xffffffffu : 0u;
-  const uint32_t* fr = a.raw + static_cast<size_t>(f) * a.H * a.nwords + wc;
-  // rows outside [0, H) read a clamped row and are masked to zero
-  auto raw_row = [&](int yy) -> uint32_t {
-    const uint32_t m = (yy >= 0 && yy < a.H) ? cmask : 0u;
-    return __ldg(fr + static_cast<size_t>(min(max(yy, 0), a.H - 1)) * a.nwords) & m;
-  };
-  // window of raw rows yb0 - R .. yb0 + 15 + R; consecutive bands share 2R rows
-  constexpr int kWin = kCell + 2 * R;
-  uint32_t win[kWin];
-#pragma unroll
-  for (int i = 0; i < 2 * R; ++i) win[i] = raw_row(cy0 * kCell - R + i);
-  for (int bi = 0; bi < nb; ++bi) {
-    const int yb0 = (cy0 + bi) * kCell;
-    const bool interior = yb0 + kCell + R <= a.H;  // uniform: no row past the frame
-    if (interior) {
-      const uint32_t* p = fr + static_cast<size_t>(yb0 + R) * a.nwords;
-#pragma unroll
-      for (int i = 2 * R; i < kWin; ++i) win[i] = __ldg(p + static_cast<size_t>(i - 2 * R) * a.nwords) & cmask;
-    } else {
-#pragma unroll
-      for (int i = 2 * R; i < kWin; ++i) win[i] = raw_row(yb0 - R + i);
-    }
-    const int nrow = min(kCell, a.H - yb0);
-    uint32_t any = 0;
-#pragma unroll
-    for (int i = 0; i < kWin; ++i) any |= win[i];
-    if (!a.mask_out && !__any_sync(0xffffffffu, any != 0)) {  // empty band tile: zero cells
-      if (owns) {
-        const size_t cbase = (static_cast<size_t>(f) * a.cells_y + cy0 + bi) * a.cells_x;
-        a.cells[cbase + 2 * w] = 0u;
-        if (2 * w + 1 < a.cells_x) a.cells[cbase + 2 * w + 1] = 0u;
-      }
-#pragma unroll
-      for (int i = 0; i < 2 * R; ++i) win[i] = win[kCell + i];
-      continue;
-    }
-    int occ = 0, occ_hi = 0;
-    uint32_t cols = 0, row_lo = 0, row_hi = 0;
-#pragma unroll
-    for (int ly = 0; ly < kCell; ++ly) {
-      uint32_t v = win[ly];
-#pragma unroll
-      for (int k = 1; k <= 2 * R; ++k) v |= win[ly + k];
-      const uint32_t vm = __shfl_up_sync(0xffffffffu, v, 1);
-      const uint32_t vp = __shfl_down_sync(0xffffffffu, v, 1);
-      uint32_t d = v;
-#pragma unroll
-      for (int k = 1; k <= R; ++k) d |= __funnelshift_r(v, vp, k) | __funnelshift_l(vm, v, k);
-      d &= ly < nrow ? keep : 0u;
-      if (a.mask_out && owns && ly < nrow)
-        a.mask_out[(static_cast<size_t>(f) * a.H + yb0 + ly) * a.nwords + w] = d;
-      const uint32_t dh = d >> 16;
-      occ += __popc(d);
-      occ_hi += __popc(dh);
-      cols |= d;
-      row_lo += min(d & 0xffffu, 1u) << ly;
-      row_hi += min(dh, 1u) << ly;
-    }
-#pragma unroll
-    for (int i = 0; i < 2 * R; ++i) win[i] = win[kCell + i];
-    if (owns) {
-      const int cx = 2 * w, cy = cy0 + bi;
-      const int occ_lo = occ - occ_hi;
-      const size_t cbase = (static_cast<size_t>(f) * a.cells_y + cy) * a.cells_x;
-      a.cells[cbase + cx] = pack_cell(occ_lo, cols & 0xffffu, row_lo);
-      if (cx + 1 < a.cells_x) a.cells[cbase + cx + 1] = pack_cell(occ_hi, cols >> 16, row_hi);
-      const uint32_t bits = (occ_lo > 0 ? 1u : 0u) | (occ_hi > 0 ? 2u : 0u);
-      if (bits) atomicOr(&act_s[bi][cx >> 5], bits << (cx & 31));
+    if (fused) {  // publish: this warp's raw words of the item are written
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(&a.item_done[item], 1u);
     }
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < nb * a.act_words; i += blockDim.x) {
-    const int bi = i / a.act_words, aw = i - bi * a.act_words;
-    a.active[(static_cast<size_t>(f) * a.cells_y + cy0 + bi) * a.act_words + aw] = act_s[bi][aw];
-  }
+  if (fused) run_dilate_tasks(a, lane);
 }
 
 // ---- host launcher ---------------------------------------------------------
@@ -372,11 +456,27 @@ static int env_int(const char* name, int dflt) {
   return e ? std::atoi(e) : dflt;
 }
 
-cudaError_t launch_mask_fg(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
+static DilateArgs dilate_args(const uint32_t* d_raw, int W, int H, uint32_t* d_cells,
+                              uint32_t* d_active, uint32_t* d_mask) {
+  DilateArgs d;
+  d.raw = d_raw;
+  d.H = H;
+  d.W = W;
+  d.nwords = ceil_div(W, 32);
+  d.cells_x = ceil_div(W, kCell);
+  d.cells_y = ceil_div(H, kCell);
+  d.act_words = ceil_div(d.cells_x, 32);
+  d.cells = d_cells;
+  d.active = d_active;
+  d.mask_out = d_mask;
+  return d;
+}
+
+// K1 work decomposition (items, ring slots) for one launch.
+static cudaError_t plan_k1(MaskArgs& a, const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                            int n_frames, int W, int H, int pitch, int threshold, uint32_t* d_raw,
-                           int sms, cudaStream_t stream) {
-  if (n_frames <= 0) return cudaSuccess;
-  MaskArgs a;
+                           int sms, size_t* smem) {
+  a = MaskArgs{};
   a.cur = d_cur;
   a.prev = d_prev;
   a.n_frames = n_frames;
@@ -401,38 +501,82 @@ cudaError_t launch_mask_fg(const uint8_t* const* d_cur, const uint8_t* const* d_
   a.ntg = ceil_div(n_frames, a.kf);
   a.total_items = a.ntg * a.nrb;
   a.raw = d_raw;
-  const size_t smem = static_cast<size_t>(kK1Groups) * a.nslots * (a.slot_bytes + 16);
-  if (smem > static_cast<size_t>(kK1SmemBudget)) return cudaErrorInvalidConfiguration;
+  *smem = static_cast<size_t>(kK1Groups) * a.nslots * (a.slot_bytes + 16);
+  if (*smem > static_cast<size_t>(kK1SmemBudget)) return cudaErrorInvalidConfiguration;
+  const bool low = threshold <= 127;
+  return cudaFuncSetAttribute(low ? mask_fg_kernel<true> : mask_fg_kernel<false>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(*smem));
+}
+
+cudaError_t launch_mask_fg(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
+                           int n_frames, int W, int H, int pitch, int threshold, uint32_t* d_raw,
+                           int sms, cudaStream_t stream) {
+  if (n_frames <= 0) return cudaSuccess;
+  MaskArgs a;
+  size_t smem = 0;
+  cudaError_t e = plan_k1(a, d_cur, d_prev, n_frames, W, H, pitch, threshold, d_raw, sms, &smem);
+  if (e != cudaSuccess) return e;
   int grid = std::min(a.total_items, sms);
   grid = std::max(1, std::min(a.total_items, env_int("TG_K1_GRID", grid)));
-  const bool low = threshold <= 127;
-  cudaError_t e = cudaFuncSetAttribute(low ? mask_fg_kernel<true> : mask_fg_kernel<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  if (low)
+  if (threshold <= 127)
     mask_fg_kernel<true><<<grid, kK1Threads, smem, stream>>>(a);
   else
     mask_fg_kernel<false><<<grid, kK1Threads, smem, stream>>>(a);
   return cudaGetLastError();
 }
 
+size_t mask_sync_words(int H, int sms) { return static_cast<size_t>(8) * sms + H + 2; }
+
+cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
+                              int n_frames, int W, int H, int pitch, int threshold, int radius,
+                              uint32_t* d_raw, uint32_t* d_cells, uint32_t* d_active,
+                              uint32_t* d_mask, uint32_t* d_sync, int sms, cudaStream_t stream) {
+  if (n_frames <= 0) return cudaSuccess;
+  if (radius < 0 || radius > kMaxRadius) return cudaErrorInvalidValue;
+  MaskArgs a;
+  size_t smem = 0;
+  cudaError_t e = plan_k1(a, d_cur, d_prev, n_frames, W, H, pitch, threshold, d_raw, sms, &smem);
+  if (e != cudaSuccess) return e;
+  a.d = dilate_args(d_raw, W, H, d_cells, d_active, d_mask);
+  if (a.d.act_words > kK1MaxActWords) return cudaErrorInvalidConfiguration;
+  if (static_cast<size_t>(a.total_items) + 1 > mask_sync_words(H, sms))
+    return cudaErrorInvalidConfiguration;
+  a.radius = radius;
+  a.dgroups = ceil_div(a.nwords, kK1GroupWords);
+  a.strips = ceil_div(a.d.cells_y, kK1bBands);
+  a.n_tasks = a.strips * n_frames * a.dgroups;
+  a.task_next = d_sync;
+  a.item_done = d_sync + 1;
+  e = cudaMemsetAsync(d_sync, 0, sizeof(uint32_t) * (a.total_items + 1), stream);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(d_active, 0,
+                      sizeof(uint32_t) * n_frames * a.d.cells_y * a.d.act_words, stream);
+  if (e != cudaSuccess) return e;
+  // every CTA must be resident: task warps wait on items of other CTAs
+  const int grid = std::min(a.total_items, sms);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kK1Threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (threshold <= 127)
+    e = cudaLaunchKernelEx(&cfg, mask_fg_kernel<true>, a);
+  else
+    e = cudaLaunchKernelEx(&cfg, mask_fg_kernel<false>, a);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 cudaError_t launch_dilate_cells(const uint32_t* d_raw, int n_frames, int W, int H, int radius,
                                 uint32_t* d_cells, uint32_t* d_active, uint32_t* d_mask,
                                 cudaStream_t stream) {
   if (n_frames <= 0) return cudaSuccess;
-  DilateArgs d;
-  d.raw = d_raw;
-  d.H = H;
-  d.W = W;
-  d.nwords = ceil_div(W, 32);
-  d.cells_x = ceil_div(W, kCell);
-  d.cells_y = ceil_div(H, kCell);
-  d.act_words = ceil_div(d.cells_x, 32);
+  const DilateArgs d = dilate_args(d_raw, W, H, d_cells, d_active, d_mask);
   if (d.act_words > kK1MaxActWords) return cudaErrorInvalidConfiguration;
-  d.cells = d_cells;
-  d.active = d_active;
-  d.mask_out = d_mask;
   const int dwarps = ceil_div(d.nwords, kK1GroupWords);
   const dim3 dg(n_frames * ceil_div(d.cells_y, kK1bBands)), db(dwarps * 32);
   switch (radius) {
