@@ -655,7 +655,8 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
   if (q.max_frames < 1 || q.max_rois_per_frame < 1 || q.max_canvases < 0)
     return fail(TG_ERR_INVALID_ARGUMENT, "capacities must be positive");
   const int cx = q.width / kCell, cy = ceil_div(q.height, kCell);
-  if (static_cast<long long>(cx) * cy > 65535)
+  if (static_cast<long long>(cx) * cy > 65535 ||
+      static_cast<long long>(ceil_div(cx, 32)) * cy * 16 > 65536)  // 16-bit CCL run slots
     return fail(TG_ERR_INVALID_ARGUMENT, "frame has more than 65535 %dx%d cells", kCell, kCell);
   if (plan_smem_bytes(cx, cy, q.max_rois_per_frame) > 200 * 1024)
     return fail(TG_ERR_INVALID_ARGUMENT, "max_rois_per_frame too large for this frame size");

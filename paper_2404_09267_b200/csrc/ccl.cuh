@@ -2,13 +2,17 @@
 // of one frame, one CTA, everything in shared memory.
 //
 // Run-based union-find: a horizontal run of active cells is labelled by its
-// first cell (bit tricks on the activity bitmask, no atomics), so unions are
-// only needed between runs of adjacent rows that touch diagonally or
-// vertically.  Links always point from the larger to the smaller cell index
-// (16-bit atomic-CAS min), so every root is its component's first cell in
-// raster order -- the oracle's component order (orc_extract_rois).  Finds use
-// path halving.  Each run then folds its pixel-tight extent (from the cell
-// summaries K1 wrote) into its component's box.
+// head (bit tricks on the activity bitmask, no atomics), so unions are only
+// needed between runs of adjacent rows that touch diagonally or vertically.
+// A run's label slot is (its activity word) * 16 + (its ordinal among the
+// word's run heads): a word holds at most 16 heads, slots are in raster
+// order, and the label array is 16 u16 per 32 cells instead of one per cell
+// (small enough for three planner CTAs per SM).  Links always point from the
+// larger to the smaller slot (16-bit atomic-CAS min), so every root is its
+// component's first run in raster order -- the oracle's component order
+// (orc_extract_rois).  Finds use path halving.  Each run then folds its
+// pixel-tight extent (from the cell summaries K1b wrote) into its
+// component's box.
 #pragma once
 
 #include <climits>
@@ -130,13 +134,21 @@ __device__ int block_exclusive_scan(int* v, int n, int* warp_tmp) {
   return carry;
 }
 
+constexpr int kHeadsPerWord = 16;  // run heads in a 32-cell activity word
+
 struct CclSmem {
-  uint32_t* act;    // [ncw] activity bits (copied from K1's bitmask)
-  uint32_t* rootm;  // [ncw] root-run heads
+  uint32_t* act;    // [ncw] activity bits (copied from K1b's bitmask)
+  uint32_t* rootm;  // [ncw] root runs, by head ordinal within the word
   int* wpre;        // [ncw + 1] exclusive prefix of popc(rootm)
   int *bx0, *by0, *bx1, *by1;  // [max_rois]
-  uint16_t* L;      // [cells] labels (run heads only)
+  uint16_t* L;      // [ncw * 16] run labels by slot
 };
+
+// Slot of the run whose head is bit b of activity word `word` (index wi of
+// its row `row`).
+__device__ __forceinline__ int head_slot(const uint32_t* row, int wi, int word, int b) {
+  return word * kHeadsPerWord + __popc(run_heads(row, wi) & ((1u << b) - 1u));
+}
 
 // Returns the number of RoIs (components), boxes in bx0..by1 (inclusive
 // pixel bounds), ranked by root cell.  Latches kErrRoiCapacity and clamps.
@@ -150,13 +162,8 @@ __device__ int ccl_frame(const uint32_t* gact, const uint32_t* gcells, int cx_n,
   // labels of run heads
   for (int i = tid; i < ncw; i += nt) {
     const int cy = i / aw, wi = i - cy * aw;
-    uint32_t h = run_heads(s.act + cy * aw, wi);
-    while (h) {
-      const int b = __ffs(h) - 1;
-      h &= h - 1;
-      const int idx = cy * cx_n + (wi << 5) + b;
-      s.L[idx] = static_cast<uint16_t>(idx);
-    }
+    const int nh = __popc(run_heads(s.act + cy * aw, wi));
+    for (int k = 0; k < nh; ++k) s.L[i * kHeadsPerWord + k] = static_cast<uint16_t>(i * kHeadsPerWord + k);
   }
   __syncthreads();
   // unions between each run and the runs it touches in the row above
@@ -166,12 +173,12 @@ __device__ int ccl_frame(const uint32_t* gact, const uint32_t* gcells, int cx_n,
     const uint32_t* row = s.act + cy * aw;
     const uint32_t* up = row - aw;
     uint32_t h = run_heads(row, wi);
-    while (h) {
+    for (int k = 0; h; ++k) {
       const int b = __ffs(h) - 1;
       h &= h - 1;
       const int a0 = (wi << 5) + b;
       const int e = run_end(row, a0, aw);
-      const int head = cy * cx_n + a0;
+      const int head = i * kHeadsPerWord + k;
       int x = max(a0 - 1, 0);
       const int xe = min(e + 1, cx_n - 1);
       while (x <= xe) {
@@ -181,34 +188,33 @@ __device__ int ccl_frame(const uint32_t* gact, const uint32_t* gcells, int cx_n,
         if (!m) break;
         x = (uw << 5) + __ffs(m) - 1;
         if (x > xe) break;
-        uf_merge(s.L, head, (cy - 1) * cx_n + run_start(up, x));
+        const int us = run_start(up, x);
+        uf_merge(s.L, head, head_slot(up, us >> 5, i - aw - wi + (us >> 5), us & 31));
         x = run_end(up, x, aw) + 2;
       }
     }
   }
   __syncthreads();
-  // roots (compressing every head's label to its root)
+  // roots
   for (int i = tid; i < ncw; i += nt) {
     const int cy = i / aw, wi = i - cy * aw;
-    uint32_t h = run_heads(s.act + cy * aw, wi), roots = 0;
-    while (h) {
-      const int b = __ffs(h) - 1;
-      h &= h - 1;
-      const int idx = cy * cx_n + (wi << 5) + b;
-      if (uf_find_ro(s.L, idx) == idx) roots |= 1u << b;
+    const int nh = __popc(run_heads(s.act + cy * aw, wi));
+    uint32_t roots = 0;
+    for (int k = 0; k < nh; ++k) {
+      const int sl = i * kHeadsPerWord + k;
+      if (uf_find_ro(s.L, sl) == sl) roots |= 1u << k;
     }
     s.rootm[i] = roots;
     s.wpre[i] = __popc(roots);
   }
   __syncthreads();
+  // compress every head's label to its root
   for (int i = tid; i < ncw; i += nt) {
     const int cy = i / aw, wi = i - cy * aw;
-    uint32_t h = run_heads(s.act + cy * aw, wi);
-    while (h) {
-      const int b = __ffs(h) - 1;
-      h &= h - 1;
-      const int idx = cy * cx_n + (wi << 5) + b;
-      s.L[idx] = static_cast<uint16_t>(uf_find_ro(s.L, idx));
+    const int nh = __popc(run_heads(s.act + cy * aw, wi));
+    for (int k = 0; k < nh; ++k) {
+      const int sl = i * kHeadsPerWord + k;
+      s.L[sl] = static_cast<uint16_t>(uf_find_ro(s.L, sl));
     }
   }
   const int ncomp = block_exclusive_scan(s.wpre, ncw, warp_tmp);
@@ -235,15 +241,14 @@ __device__ int ccl_frame(const uint32_t* gact, const uint32_t* gcells, int cx_n,
     const int cy = i / aw, wi = i - cy * aw;
     const uint32_t* row = s.act + cy * aw;
     uint32_t h = run_heads(row, wi);
-    while (h) {
+    for (int k = 0; h; ++k) {
       const int b = __ffs(h) - 1;
       h &= h - 1;
       const int a0 = (wi << 5) + b;
       const int e = run_end(row, a0, aw);
-      const int root = s.L[cy * cx_n + a0];
-      const int rcy = root / cx_n, rcx = root - rcy * cx_n;
-      const int rw = rcy * aw + (rcx >> 5);
-      const int rank = s.wpre[rw] + __popc(s.rootm[rw] & ((1u << (rcx & 31)) - 1u));
+      const int root = s.L[i * kHeadsPerWord + k];
+      const int rw = root / kHeadsPerWord, ro = root - rw * kHeadsPerWord;
+      const int rank = s.wpre[rw] + __popc(s.rootm[rw] & ((1u << ro) - 1u));
       if (rank >= nr) continue;
       const uint32_t* crow = gcells + static_cast<size_t>(cy) * cx_n;
       const uint32_t va = crow[a0], ve = crow[e];

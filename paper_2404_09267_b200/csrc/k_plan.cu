@@ -35,16 +35,26 @@ __device__ __forceinline__ void sort_jobs_by_x(const Job* tmp, int n, Job* out, 
   }
 }
 
+// K3/K4 working set; aliases the K2 (CCL) region of dynamic smem once the
+// RoI boxes are out, so three planner CTAs fit on an SM.
+struct PlanTail {
+  tg_patch_meta spatch[kMaxZones];
+  FreeRect freel[2 * kMaxZones + 2];
+  StitchOut souts[kMaxZones];
+  Job sjobs[3 * kMaxZones];
+};
+
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ ZoneAcc zacc;
-  __shared__ tg_patch_meta spatch[kMaxZones];
   __shared__ int adm_w[kMaxZones], adm_h[kMaxZones], adm_idx[kMaxZones];
-  __shared__ FreeRect freel[2 * kMaxZones + 2];
-  __shared__ StitchOut souts[kMaxZones];
-  __shared__ Job sjobs[3 * kMaxZones];
   __shared__ int warp_tmp[32];
   __shared__ int s_nrois;
+  PlanTail& T = *reinterpret_cast<PlanTail*>(dsm);
+  tg_patch_meta* spatch = T.spatch;
+  FreeRect* freel = T.freel;
+  StitchOut* souts = T.souts;
+  Job* sjobs = T.sjobs;
 
   const int f = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const int cx_n = a.cells_x, cy_n = a.cells_y, aw = a.act_words, ncw = cy_n * aw;
@@ -292,8 +302,9 @@ __global__ void __launch_bounds__(128) stitch_batch_kernel(const StitchBatchArgs
 size_t plan_smem_bytes(int cells_x, int cells_y, int max_rois) {
   const int aw = ceil_div(cells_x, 32);
   const size_t ncw = static_cast<size_t>(cells_y) * aw;
-  return ncw * 4 * 2 + (ncw + 1) * 4 + static_cast<size_t>(max_rois) * 16 +
-         static_cast<size_t>(cells_x) * cells_y * 2 + 16;
+  const size_t ccl = ncw * 4 * 2 + (ncw + 1) * 4 + static_cast<size_t>(max_rois) * 16 +
+                     ncw * kHeadsPerWord * 2 + 16;
+  return ccl > sizeof(PlanTail) ? ccl : sizeof(PlanTail);
 }
 
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
