@@ -676,7 +676,7 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
   };
   cudaError_t e = cudaSuccess;
   if (!e) e = alloc(&p->raw, F * q.height * p->mask_words);
-  if (!e) e = alloc(&p->mask_sync, mask_sync_words(q.height, ctx->sms));
+  if (!e) e = alloc(&p->mask_sync, mask_sync_words(q.height, q.max_frames));
   if (!e) e = alloc(&p->cells, F * cx * cy);
   if (!e) e = alloc(&p->active, F * cy * p->act_words);
   if (!e && q.keep_mask) e = alloc(&p->mask, F * q.height * p->mask_words);

@@ -525,7 +525,8 @@ cudaError_t launch_mask_fg(const uint8_t* const* d_cur, const uint8_t* const* d_
   return cudaGetLastError();
 }
 
-size_t mask_sync_words(int H, int sms) { return static_cast<size_t>(8) * sms + H + 2; }
+// item counters (<= frames x row blocks) + the task queue head
+size_t mask_sync_words(int H, int max_frames) { return static_cast<size_t>(max_frames) * H + 2; }
 
 cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                               int n_frames, int W, int H, int pitch, int threshold, int radius,
@@ -539,7 +540,7 @@ cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const*
   if (e != cudaSuccess) return e;
   a.d = dilate_args(d_raw, W, H, d_cells, d_active, d_mask);
   if (a.d.act_words > kK1MaxActWords) return cudaErrorInvalidConfiguration;
-  if (static_cast<size_t>(a.total_items) + 1 > mask_sync_words(H, sms))
+  if (static_cast<size_t>(a.total_items) + 1 > mask_sync_words(H, n_frames))
     return cudaErrorInvalidConfiguration;
   a.radius = radius;
   a.dgroups = ceil_div(a.nwords, kK1GroupWords);
