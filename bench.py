@@ -86,6 +86,10 @@ class Clocks:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()  # the timed region starts once samples are flowing
+            while not self.rows and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.005)
+            self.rows = []
         except Exception:
             self.proc = None
 
@@ -208,8 +212,9 @@ def run_ours(args):
     # algorithmic bytes.  Path: B_run = 2*W*H*C per frame +
     # admitted patch bytes + every canvas byte.  K1 (the dominant kernel,
     # launched fused with K1b): the frames it must read -- the n frames plus
-    # the first frame's prev, each once -- and the cell grids it writes (the
-    # raw bitmap between K1 and K1b is an intermediate, not credited).
+    # the first frame's prev, each once -- the raw foreground bitmap's one
+    # HBM round trip (written by K1, read back by the K1b tasks) and the cell
+    # grids it writes.
     adm_bytes = 0
     for f in range(n):
         for j, p in enumerate(res["patch_list"][f]):
@@ -219,7 +224,7 @@ def run_ours(args):
     raw_bytes = n * H * ((W + 31) // 32) * 4
     cx, cy = (W + 15) // 16, (H + 15) // 16
     cell_bytes = n * cy * (cx + (cx + 31) // 32) * 4
-    k1_bytes = (n + 1) * FRAME_BYTES + cell_bytes
+    k1_bytes = (n + 1) * FRAME_BYTES + 2 * raw_bytes + cell_bytes
     b_run = n * 2 * FRAME_BYTES + adm_bytes + ncanv * pipe.canvas_bytes
     b_unique = (n + 1) * FRAME_BYTES + 2 * raw_bytes + adm_bytes + ncanv * pipe.canvas_bytes
     peak, peak_src = peaks()

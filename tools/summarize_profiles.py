@@ -93,7 +93,7 @@ def main(tag):
     total = sum(sum(m["gpu__time_duration.sum"] for m in ms) / len(ms)
                 for n, ms in per.items() if not n.startswith("synth"))
     lines += ["", f"Step total (sum of mean kernel times): {total/1e6:.4f} ms", ""]
-    for kern in ("mask_fg", "dilate", "plan_kernel", "gather_kernel"):
+    for kern in ("mask_fg", "plan_kernel", "gather_kernel"):
         rep = os.path.join(OUT, f"prof_{kern}.ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -112,9 +112,11 @@ def main(tag):
     if k1:
         traffic = k1["read"] + k1["write"]
         raw = 2160 * 120 * 4
-        json.dump({"kernel": "mask_fg_kernel", "frames_per_launch": FRAMES,
+        cells = 135 * (240 + 8) * 4
+        json.dump({"kernel": "mask_fg_kernel (K1, K1b fused)", "frames_per_launch": FRAMES,
                    "dram_bytes_per_launch": traffic, "dram_bytes_per_frame": traffic / FRAMES,
-                   "algorithmic_bytes_per_launch": (FRAMES + 1) * FRAME_BYTES + FRAMES * raw,
+                   "algorithmic_bytes_per_launch":
+                       (FRAMES + 1) * FRAME_BYTES + FRAMES * (2 * raw + cells),
                    "source": f"profiles/{tag}_launches.csv"},
                   open(os.path.join(PROF, "k1_traffic.json"), "w"), indent=1)
     print("\n".join(lines))
