@@ -124,27 +124,30 @@ struct Choice {
 // BSSF over every free rect of every open canvas; ties by canvas, y, x
 // (candidate_better, stitch.hpp:72-81).
 Choice choose(const Packing& st, int w, int h, int M, int N) {
-  Choice best{-1, -1, tg_rect{0, 0, 0, 0}};
-  int bs = 0;
+  // One 64-bit key per candidate, (score, canvas, y, x) from the top 16 bits
+  // down (all < 2^16), so the minimum key is the candidate_better winner;
+  // infeasible rects get ~0.  Branch-free inner loop.
+  uint64_t best = ~0ull;
+  int bfi = -1;
   for (int ci = 0; ci < static_cast<int>(st.canvases.size()); ++ci) {
     const auto& fr = st.canvases[ci].free;
+    const uint64_t cbits = static_cast<uint64_t>(ci) << 32;
     for (int fi = 0; fi < static_cast<int>(fr.size()); ++fi) {
       const tg_rect& c = fr[fi];
-      if (c.w < w || c.h < h) continue;
-      const int s = std::min(c.w - w, c.h - h);
-      bool better;
-      if (best.canvas < 0) better = true;
-      else if (s != bs) better = s < bs;
-      else if (ci != best.canvas) better = ci < best.canvas;
-      else better = c.y != best.chosen.y ? c.y < best.chosen.y : c.x < best.chosen.x;
-      if (better) {
-        best = Choice{ci, fi, c};
-        bs = s;
+      const bool ok = c.w >= w && c.h >= h;
+      const uint64_t s = static_cast<uint64_t>(std::min(c.w - w, c.h - h));
+      const uint64_t key = ok ? (s << 48 | cbits | static_cast<uint64_t>(c.y) << 16 |
+                                 static_cast<uint64_t>(c.x))
+                              : ~0ull;
+      if (key < best) {
+        best = key;
+        bfi = fi;
       }
     }
   }
-  if (best.canvas < 0) best = Choice{static_cast<int>(st.canvases.size()), -1, tg_rect{0, 0, M, N}};
-  return best;
+  if (bfi < 0) return Choice{static_cast<int>(st.canvases.size()), -1, tg_rect{0, 0, M, N}};
+  const int ci = static_cast<int>(best >> 32 & 0xffff);
+  return Choice{ci, bfi, st.canvases[ci].free[bfi]};
 }
 
 void commit(Packing& st, const Choice& ch, const tg_patch_meta& p, int queue_index, int M, int N) {

@@ -175,11 +175,12 @@ def schedule_descriptors(sched, desc: np.ndarray, cameras, n_frames: int, bandwi
     d = np.array(desc, copy=True)
     d["patch"]["patch_id"] = np.arange(len(d), dtype=np.uint64)
     adm = d[d["admitted"] != 0]
-    cams = list(cameras)
+    cams = np.asarray(list(cameras), np.int64)
+    lut = np.full(int(cams.max()) + 1 if len(cams) else 1, -1, np.int32)
+    lut[cams] = np.arange(len(cams), dtype=np.int32)
+    cam_slot = lut[adm["camera"]]
     offs = np.zeros(len(cams) + 1, np.int32)
-    offs[1:] = np.cumsum([(adm["camera"] == c).sum() for c in cams])
-    slot_of_cam = {c: k for k, c in enumerate(cams)}
-    cam_slot = np.array([slot_of_cam[c] for c in adm["camera"]], np.int32)
+    offs[1:] = np.cumsum(np.bincount(cam_slot, minlength=len(cams)))
     src = (cam_slot * (n_frames + 1) + adm["frame"] + 1).astype(np.int32)
     patches = np.ascontiguousarray(adm["patch"])
     arrival = np.zeros(max(1, len(patches)), np.int64)
