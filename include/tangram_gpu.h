@@ -338,6 +338,41 @@ tg_status tg_batcher_replay_links(tg_batcher* b, int32_t n_cams, const int32_t* 
                                   double bandwidth_mbps, int32_t per_camera_link,
                                   int64_t* arrival_us_out, int32_t* n_events);
 
+/* ---- multi-camera descriptors (configs 3/4, sim.hpp:249-262, 274-290) ----
+ * One record per patch of a camera shard: what ranks all-gather and what the
+ * batcher consumes.  Never pixels. */
+typedef struct {
+  tg_patch_meta patch;
+  int32_t camera;    /* camera id */
+  int32_t frame;     /* frame index within the camera */
+  int32_t admitted;  /* w <= M && h <= N (sim.hpp:262) */
+  int32_t pad;
+} tg_descriptor;     /* 80 B */
+/* Compacts a pipeline's per-frame patch slots (patches[F][zones],
+ * n_patches[F], admitted[F][zones], as tg_pipeline_views lays them out) into
+ * descriptors, frame order then zone order.  Pipeline frame f is frame
+ * f % frames_per_camera of camera cameras[f / frames_per_camera]
+ * (F = n_cams * frames_per_camera).  TG_ERR_CAPACITY if cap is too small. */
+tg_status tg_descriptors_compact(const tg_patch_meta* patches, const int32_t* n_patches,
+                                 const uint8_t* admitted, int32_t zones, const int32_t* cameras,
+                                 int32_t n_cams, int32_t frames_per_camera, tg_descriptor* out,
+                                 int64_t cap, int64_t* n_out);
+/* Host half of configs 3/4.  `desc` is camera-major (each camera's records
+ * in frame, zone order) -- a shard's own list or the all-gathered list of
+ * every shard.  Record i gets patch id i (sim.hpp:249-251: ids over every
+ * camera of the job); records of cameras outside cameras[0..n_cams) take
+ * their id and are skipped; the admitted ones (sim.hpp:262) of the listed
+ * cameras, which must appear in `cameras` order, go through
+ * tg_batcher_replay_links with pixels at d_frames index
+ * slot * (frames_per_camera + 1) + frame + 1 for camera cameras[slot].
+ * Optional outputs per admitted patch, in order: its renumbered meta,
+ * source frame index and arrival time. */
+tg_status tg_batcher_schedule(tg_batcher* b, const tg_descriptor* desc, int64_t n,
+                              const int32_t* cameras, int32_t n_cams, int32_t frames_per_camera,
+                              double bandwidth_mbps, int32_t per_camera_link,
+                              tg_patch_meta* admitted_out, int32_t* src_frames_out,
+                              int64_t* arrival_us_out, int64_t* n_admitted, int32_t* n_events);
+
 /* ---- synthetic workload (fixture source; not part of the timed path) -----
  * trace.hpp:145-231 generate_trace, restated (std::mt19937_64 + the
  * reference's hand-rolled distributions).  Writes t_us[n_frames],

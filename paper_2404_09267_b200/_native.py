@@ -165,6 +165,9 @@ SIGNATURES = {
     "tg_batcher_gather_all": (st, [vp, vp, vp, i32, vp, i64, P(i64), vp]),
     "tg_batcher_replay": (st, [vp, P(tg_patch_meta), P(i32), P(i64), i32, P(i32)]),
     "tg_batcher_replay_links": (st, [vp, i32, vp, vp, vp, C.c_double, i32, vp, P(i32)]),
+    "tg_descriptors_compact": (st, [vp, vp, vp, i32, vp, i32, i32, vp, i64, P(i64)]),
+    "tg_batcher_schedule": (st, [vp, vp, i64, vp, i32, i32, C.c_double, i32, vp, vp, vp, P(i64),
+                                 P(i32)]),
     "tg_workload_default": (st, [P(tg_workload_config)]),
     "tg_derive_seed": (u64, [u64, C.c_char_p]),
     "tg_generate_trace": (st, [P(tg_workload_config), P(i64), P(i32), P(tg_rect), i64, P(i64)]),

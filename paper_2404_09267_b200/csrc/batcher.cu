@@ -16,7 +16,6 @@
 #include <cstdarg>
 #include <cstdio>
 #include <optional>
-#include <queue>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -114,6 +113,18 @@ struct CanvasSt {
 
 struct Packing {
   std::vector<CanvasSt> canvases;
+  // per canvas (max free-rect width) << 16 | (max free-rect height), kept
+  // contiguous so choose() skips canvases nothing fits in without touching them
+  std::vector<uint32_t> bound;
+
+  void refresh_bound(int ci) {
+    int mw = 0, mh = 0;
+    for (const tg_rect& r : canvases[ci].free) {
+      mw = std::max(mw, r.w);
+      mh = std::max(mh, r.h);
+    }
+    bound[ci] = static_cast<uint32_t>(mw) << 16 | static_cast<uint32_t>(mh);
+  }
 };
 
 struct Choice {
@@ -126,34 +137,41 @@ struct Choice {
 Choice choose(const Packing& st, int w, int h, int M, int N) {
   // One 64-bit key per candidate, (score, canvas, y, x) from the top 16 bits
   // down (all < 2^16), so the minimum key is the candidate_better winner;
-  // infeasible rects get ~0.  Branch-free inner loop.
+  // infeasible rects get ~0.  The scan is a branch-free min; free rects of a
+  // canvas are disjoint, so (canvas, y, x) names the winner, found again in
+  // its canvas's list afterwards.
   uint64_t best = ~0ull;
-  int bfi = -1;
   for (int ci = 0; ci < static_cast<int>(st.canvases.size()); ++ci) {
-    const auto& fr = st.canvases[ci].free;
+    const uint32_t bd = st.bound[ci];
+    if (static_cast<int>(bd >> 16) < w || static_cast<int>(bd & 0xffff) < h) continue;
+    const tg_rect* fr = st.canvases[ci].free.data();
+    const int nf = static_cast<int>(st.canvases[ci].free.size());
     const uint64_t cbits = static_cast<uint64_t>(ci) << 32;
-    for (int fi = 0; fi < static_cast<int>(fr.size()); ++fi) {
-      const tg_rect& c = fr[fi];
-      const bool ok = c.w >= w && c.h >= h;
-      const uint64_t s = static_cast<uint64_t>(std::min(c.w - w, c.h - h));
-      const uint64_t key = ok ? (s << 48 | cbits | static_cast<uint64_t>(c.y) << 16 |
-                                 static_cast<uint64_t>(c.x))
-                              : ~0ull;
-      if (key < best) {
-        best = key;
-        bfi = fi;
-      }
+    for (int fi = 0; fi < nf; ++fi) {
+      const tg_rect c = fr[fi];
+      const int dw = c.w - w, dh = c.h - h;
+      // all ones when the patch does not fit (dw or dh negative): no branch
+      const uint64_t bad = static_cast<uint64_t>(static_cast<int64_t>(dw | dh) >> 63);
+      const uint64_t s = static_cast<uint64_t>(static_cast<uint32_t>(dw < dh ? dw : dh));
+      const uint64_t key = (s << 48 | cbits | static_cast<uint64_t>(c.y) << 16 |
+                            static_cast<uint64_t>(c.x)) | bad;
+      best = key < best ? key : best;
     }
   }
-  if (bfi < 0) return Choice{static_cast<int>(st.canvases.size()), -1, tg_rect{0, 0, M, N}};
+  if (best == ~0ull) return Choice{static_cast<int>(st.canvases.size()), -1, tg_rect{0, 0, M, N}};
   const int ci = static_cast<int>(best >> 32 & 0xffff);
-  return Choice{ci, bfi, st.canvases[ci].free[bfi]};
+  const int by = static_cast<int>(best >> 16 & 0xffff), bx = static_cast<int>(best & 0xffff);
+  const auto& fr = st.canvases[ci].free;
+  int fi = 0;
+  while (fr[fi].x != bx || fr[fi].y != by) ++fi;
+  return Choice{ci, fi, fr[fi]};
 }
 
 void commit(Packing& st, const Choice& ch, const tg_patch_meta& p, int queue_index, int M, int N) {
   if (ch.fi < 0) {
     st.canvases.emplace_back();
     st.canvases.back().free.push_back(tg_rect{0, 0, M, N});
+    st.bound.push_back(0);
   }
   CanvasSt& cv = st.canvases[ch.canvas];
   const int fi = ch.fi < 0 ? 0 : ch.fi;
@@ -170,6 +188,7 @@ void commit(Packing& st, const Choice& ch, const tg_patch_meta& p, int queue_ind
   }
   if (a.w > 0 && a.h > 0) cv.free.push_back(a);
   if (b.w > 0 && b.h > 0) cv.free.push_back(b);
+  st.refresh_bound(ch.canvas);
   tg_placement pl;
   pl.patch_id = p.patch_id;
   pl.canvas_index = ch.canvas;
@@ -491,32 +510,39 @@ tg_status tg_batcher_gather_all(tg_ctx* ctx, tg_batcher* b, const uint8_t* const
 tg_status tg_batcher_replay(tg_batcher* b, const tg_patch_meta* patches, const int32_t* src_frames,
                             const int64_t* arrival_us, int32_t n, int32_t* n_events) {
   // sim.hpp:334-342 (arrival seqs first, scene-major), 392-400 (timer pushed
-  // when its epoch is new), 425-458 (heap by (t, seq)).
-  struct Ev {
-    int64_t t;
-    uint64_t seq;
-    int kind;  // 0 arrival, 1 timer
-    uint64_t a;
-    bool operator>(const Ev& o) const { return std::tie(t, seq) > std::tie(o.t, o.seq); }
-  };
-  std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> heap;
-  uint64_t seq = 0;
-  for (int i = 0; i < n; ++i) heap.push(Ev{arrival_us[i], seq++, 0, static_cast<uint64_t>(i)});
+  // when its epoch is new), 425-458 (heap by (t, seq)).  The reference's heap
+  // is replayed without one: arrivals hold seqs 0..n-1, so they pop in
+  // (t, index) order -- one sort -- and precede any timer at equal t (timer
+  // seqs are >= n).  Only the newest timer can fire: an older epoch's timer
+  // pops as a no-op (scheduler.hpp:130-135), so a single pending (t, epoch)
+  // stands in for the heap's timer entries.
+  std::vector<std::pair<int64_t, int32_t>> order(static_cast<size_t>(n));
+  bool sorted = true;
+  for (int i = 0; i < n; ++i) {
+    order[i] = {arrival_us[i], i};
+    if (i && order[i] < order[i - 1]) sorted = false;
+  }
+  if (!sorted) std::sort(order.begin(), order.end());
   std::vector<Event> all;
-  uint64_t pushed_epoch = 0;
-  while (!heap.empty()) {
-    const Ev ev = heap.top();
-    heap.pop();
+  bool timer_pending = false;
+  int64_t timer_t = 0;
+  uint64_t timer_ep = 0, pushed_epoch = 0;
+  size_t next = 0;
+  while (next < order.size() || timer_pending) {
     b->events.clear();
-    if (ev.kind == 0) {
-      const tg_status s = b->arrival(patches[ev.a], src_frames ? src_frames[ev.a] : -1, ev.t);
+    if (next < order.size() && (!timer_pending || order[next].first <= timer_t)) {
+      const int i = order[next++].second;
+      const tg_status s = b->arrival(patches[i], src_frames ? src_frames[i] : -1, arrival_us[i]);
       if (s) return s;
       if (b->has_timer && b->timer_epoch != pushed_epoch) {
-        heap.push(Ev{b->timer_at, seq++, 1, b->timer_epoch});
+        timer_pending = true;
+        timer_t = b->timer_at;
+        timer_ep = b->timer_epoch;
         pushed_epoch = b->timer_epoch;
       }
     } else {
-      b->timer(ev.t, ev.a);
+      timer_pending = false;
+      b->timer(timer_t, timer_ep);
     }
     for (auto& e : b->events) all.push_back(std::move(e));
   }
@@ -554,6 +580,89 @@ tg_status tg_batcher_replay_links(tg_batcher* b, int32_t n_cams, const int32_t* 
   }
   if (arrival_us_out) std::copy(arrival.begin(), arrival.end(), arrival_us_out);
   return tg_batcher_replay(b, patches, src_frames, arrival.data(), n, n_events);
+}
+
+}  // extern "C"
+
+extern "C" {
+
+tg_status tg_descriptors_compact(const tg_patch_meta* patches, const int32_t* n_patches,
+                                 const uint8_t* admitted, int32_t zones, const int32_t* cameras,
+                                 int32_t n_cams, int32_t frames_per_camera, tg_descriptor* out,
+                                 int64_t cap, int64_t* n_out) {
+  *n_out = 0;
+  if (zones < 1 || n_cams < 0 || frames_per_camera < 0)
+    return bfail(TG_ERR_INVALID_ARGUMENT, "bad descriptor layout");
+  int64_t k = 0;
+  const int64_t F = static_cast<int64_t>(n_cams) * frames_per_camera;
+  for (int64_t f = 0; f < F; ++f) {
+    const int np = n_patches[f];
+    if (np < 0 || np > zones) return bfail(TG_ERR_INVALID_ARGUMENT, "bad patch count");
+    if (k + np > cap) return bfail(TG_ERR_CAPACITY, "descriptor capacity exceeded");
+    const int cam = cameras[f / frames_per_camera];
+    const int fr = static_cast<int>(f % frames_per_camera);
+    for (int j = 0; j < np; ++j) {
+      tg_descriptor& d = out[k++];
+      d.patch = patches[f * zones + j];
+      d.camera = cam;
+      d.frame = fr;
+      d.admitted = admitted[f * zones + j] ? 1 : 0;
+      d.pad = 0;
+    }
+  }
+  *n_out = k;
+  return TG_OK;
+}
+
+tg_status tg_batcher_schedule(tg_batcher* b, const tg_descriptor* desc, int64_t n,
+                              const int32_t* cameras, int32_t n_cams, int32_t frames_per_camera,
+                              double bandwidth_mbps, int32_t per_camera_link,
+                              tg_patch_meta* admitted_out, int32_t* src_frames_out,
+                              int64_t* arrival_us_out, int64_t* n_admitted, int32_t* n_events) {
+  *n_events = 0;
+  if (n_admitted) *n_admitted = 0;
+  if (n < 0 || n_cams < 0 || frames_per_camera < 0)
+    return bfail(TG_ERR_INVALID_ARGUMENT, "bad descriptor counts");
+  int32_t max_cam = -1;
+  for (int k = 0; k < n_cams; ++k) {
+    if (cameras[k] < 0) return bfail(TG_ERR_INVALID_ARGUMENT, "negative camera id");
+    max_cam = std::max(max_cam, cameras[k]);
+  }
+  std::vector<int32_t> slot_of(static_cast<size_t>(max_cam) + 1, -1);
+  for (int k = 0; k < n_cams; ++k) slot_of[cameras[k]] = k;
+  std::vector<tg_patch_meta> adm;
+  std::vector<int32_t> src;
+  std::vector<int32_t> count(static_cast<size_t>(n_cams), 0);
+  adm.reserve(static_cast<size_t>(n));
+  src.reserve(static_cast<size_t>(n));
+  int last_slot = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const tg_descriptor& d = desc[i];
+    const int slot = (d.camera >= 0 && d.camera <= max_cam) ? slot_of[d.camera] : -1;
+    if (slot < 0) continue;  // another shard's camera: it only takes its id
+    if (slot < last_slot)
+      return bfail(TG_ERR_INVALID_ARGUMENT,
+                   "descriptor %lld: camera %d out of the camera order", static_cast<long long>(i),
+                   d.camera);
+    last_slot = slot;
+    if (d.frame < 0 || d.frame >= frames_per_camera)
+      return bfail(TG_ERR_INVALID_ARGUMENT, "descriptor %lld: frame %d out of range",
+                   static_cast<long long>(i), d.frame);
+    if (!d.admitted) continue;
+    tg_patch_meta p = d.patch;
+    p.patch_id = static_cast<uint64_t>(i);
+    adm.push_back(p);
+    src.push_back(slot * (frames_per_camera + 1) + d.frame + 1);
+    ++count[slot];
+  }
+  std::vector<int32_t> offs(static_cast<size_t>(n_cams) + 1, 0);
+  for (int k = 0; k < n_cams; ++k) offs[k + 1] = offs[k] + count[k];
+  const int32_t na = static_cast<int32_t>(adm.size());
+  if (n_admitted) *n_admitted = na;
+  if (admitted_out) std::copy(adm.begin(), adm.end(), admitted_out);
+  if (src_frames_out) std::copy(src.begin(), src.end(), src_frames_out);
+  return tg_batcher_replay_links(b, n_cams, offs.data(), adm.data(), src.data(), bandwidth_mbps,
+                                 per_camera_link, arrival_us_out, n_events);
 }
 
 }  // extern "C"

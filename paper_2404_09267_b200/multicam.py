@@ -53,26 +53,32 @@ class MultiCameraPath:
         self.canvas = canvas
         self.bandwidth, self.per_camera_link = bandwidth_mbps, per_camera_link
         trace_kw = dict(trace_kw or {})
-        self.rings, self.pipes, self.tables, self.t_us, self.rects = [], [], [], [], []
-        self.d_ids, self.d_gen = [], []
+        self.rings, self.t_us, self.rects = [], [], []
         for c in self.cameras:
             t_us, rects = generate_trace(n_frames=n_frames, fps=fps, frame_width=width,
                                          frame_height=height, seed=1000 + c, **trace_kw)
             ring = FrameRing(ctx, width, height, n_frames)
             ring.synthesize(derive_seed(1000 + c, "pixels"), rects)
-            pipe = Pipeline(ctx, width, height, max_frames=n_frames, max_canvases=0, zones=zones,
-                            canvas=canvas, slo_us=slo_us)
             self.rings.append(ring)
-            self.pipes.append(pipe)
-            self.tables.append(ring.tables())
             self.t_us.append(t_us)
             self.rects.append(rects)
-            d_ids, d_gen = ctx.malloc(8 * n_frames), ctx.malloc(8 * n_frames)
-            ctx.upload(d_ids, np.arange(n_frames, dtype=np.uint64))
-            ctx.upload(d_gen, np.array(t_us, np.int64))
-            self.d_ids.append(d_ids)
-            self.d_gen.append(d_gen)
-        self.zones = self.pipes[0].zones if self.pipes else zones[0] * zones[1]
+        # ONE pipeline over the frames of every camera of the shard, camera-major:
+        # frame k*n + i is camera k's frame i, its predecessor that camera's slot i
+        # (K1 restarts the frame chain at each camera boundary), so the shard's
+        # masks, cells and plans take one K1 and one K2-K4 launch per step.
+        F = max(1, len(self.cameras) * n_frames)
+        self.pipe = Pipeline(ctx, width, height, max_frames=F, max_canvases=0, zones=zones,
+                             canvas=canvas, slo_us=slo_us)
+        cur = np.array([r.slots[1 + i] for r in self.rings for i in range(n_frames)], np.uint64)
+        prev = np.array([r.slots[i] for r in self.rings for i in range(n_frames)], np.uint64)
+        ids = np.tile(np.arange(n_frames, dtype=np.uint64), len(self.cameras))
+        gen = np.array([t for t_us in self.t_us for t in t_us], np.int64)
+        self.d_cur, self.d_prev, self.d_ids, self.d_gen = (ctx.malloc(8 * F) for _ in range(4))
+        if len(cur):
+            for d, a in ((self.d_cur, cur), (self.d_prev, prev), (self.d_ids, ids),
+                         (self.d_gen, gen)):
+                ctx.upload(d, a)
+        self.zones = self.pipe.zones
         # one device table of every frame of every camera: index cam*(n+1) + slot
         ptrs = np.array([s for ring in self.rings for s in ring.slots], np.uint64)
         self.d_frames = ctx.malloc(8 * max(1, len(ptrs)))
@@ -84,50 +90,54 @@ class MultiCameraPath:
         self.canvas_bytes = canvas[0] * canvas[1] * 3
         self.canvas_cap = canvas_capacity
         self.d_canvases = None
-        self.stream = ctx.new_stream()
-        self._pat = np.zeros(len(self.cameras) * n_frames * self.zones, PATCH_DTYPE)
-        self._adm = np.zeros(len(self.cameras) * n_frames * self.zones, np.uint8)
-        self._np = np.zeros(len(self.cameras) * n_frames, np.int32)
+        self.stream = ctx.new_stream()   # K1-K4 and the descriptor read-back
+        self.gstream = ctx.new_stream()  # K5 (event canvases)
+        self._gdone = ctx.event()
+        # pinned landing zone of the descriptor read-back: patches, admission, counts
+        nslot = len(self.cameras) * n_frames * self.zones
+        self._hbytes = nslot * 64 + nslot + 4 * len(self.cameras) * n_frames
+        self._h = ctx.malloc_host(max(1, self._hbytes))
+        self._cams = np.array(self.cameras, np.int32)
+        self._desc = np.zeros(max(1, nslot), DESC_DTYPE)
 
     def close(self):
-        for p in self.pipes:
-            p.close()
+        self.pipe.close()
         for r in self.rings:
             r.close()
-        for p in self.d_ids + self.d_gen + [self.d_frames]:
+        for p in (self.d_cur, self.d_prev, self.d_ids, self.d_gen, self.d_frames):
             self.ctx.free(p)
         if self.d_canvases:
             self.ctx.free(self.d_canvases)
+        self.ctx.free_host(self._h)
         self.sched.close()
 
     # ---- 1. device: K1-K4 for every camera --------------------------------
     def run_planes(self):
-        lib = N.lib()
-        for k, pipe in enumerate(self.pipes):
-            d_cur, d_prev = self.tables[k]
-            check(lib.tg_pipeline_stage_mask(pipe.handle, self.n, d_cur, d_prev, self.stream))
-            check(lib.tg_pipeline_stage_plan(pipe.handle, self.n, self.d_ids[k], self.d_gen[k], 0,
-                                             self.stream))
+        if not self.cameras:
+            return
+        lib, F = N.lib(), len(self.cameras) * self.n
+        check(lib.tg_pipeline_stage_mask(self.pipe.handle, F, self.d_cur, self.d_prev, self.stream))
+        check(lib.tg_pipeline_stage_plan(self.pipe.handle, F, self.d_ids, self.d_gen, 0,
+                                         self.stream))
 
     # ---- 2. descriptors to the host ----------------------------------------
     def descriptors(self) -> np.ndarray:
         """DESC_DTYPE records of every patch of the shard, camera-major,
-        frame order, zone order (ids still camera-local)."""
-        n, Z = self.n, self.zones
-        for k, pipe in enumerate(self.pipes):
-            v = pipe.views
-            self.ctx.memcpy(self._pat[k * n * Z:].ctypes.data, v.patches, n * Z * 64, 1, self.stream)
-            self.ctx.memcpy(self._adm[k * n * Z:].ctypes.data, v.admitted, n * Z, 1, self.stream)
-            self.ctx.memcpy(self._np[k * n:].ctypes.data, v.n_patches, n * 4, 1, self.stream)
+        frame order, zone order (ids numbered over the shard; `schedule`
+        renumbers them over the whole camera set).  Waits for the planes."""
+        Z, F = self.zones, len(self.cameras) * self.n
+        if not F:
+            return self._desc[:0]
+        v, h = self.pipe.views, self._h
+        self.ctx.memcpy(h, v.patches, F * Z * 64, 1, self.stream)
+        self.ctx.memcpy(h + F * Z * 64, v.admitted, F * Z, 1, self.stream)
+        self.ctx.memcpy(h + F * Z * 65, v.n_patches, F * 4, 1, self.stream)
         self.ctx.stream_sync(self.stream)
-        counts = self._np.reshape(len(self.pipes), n)
-        valid = (np.arange(Z)[None, None, :] < counts[:, :, None]).reshape(-1)
-        out = np.zeros(int(valid.sum()), DESC_DTYPE)
-        out["patch"] = self._pat[valid]
-        cams = np.repeat(np.array(self.cameras, np.int32), n * Z)[valid]
-        frames = np.tile(np.repeat(np.arange(n, dtype=np.int32), Z), len(self.pipes))[valid]
-        out["camera"], out["frame"], out["admitted"] = cams, frames, self._adm[valid]
-        return out
+        n = C.c_int64()
+        check(N.lib().tg_descriptors_compact(h, h + F * Z * 65, h + F * Z * 64, Z,
+                                             self._cams.ctypes.data, len(self.cameras), self.n,
+                                             self._desc.ctypes.data, len(self._desc), C.byref(n)))
+        return self._desc[:n.value]
 
     # ---- 3. host: ids, admission, links, batcher ----------------------------
     def schedule(self, desc: np.ndarray):
@@ -138,7 +148,9 @@ class MultiCameraPath:
         return self._nev
 
     # ---- 4. device: every event's canvases ----------------------------------
-    def gather(self) -> int:
+    def gather(self, join: bool = True) -> int:
+        """Writes every event's canvases (one K5 launch on `gstream`); with
+        `join`, `stream` waits for them (so syncing `stream` covers them)."""
         if self.d_canvases is None:
             cap = self.canvas_cap or max(1, len(self._last["patches"]))
             self.canvas_cap = cap
@@ -146,8 +158,36 @@ class MultiCameraPath:
         n = C.c_int64()
         check(N.lib().tg_batcher_gather_all(self.ctx.handle, self.sched.handle, self.d_frames,
                                             3 * self.W, self.d_canvases, self.canvas_cap,
-                                            C.byref(n), self.stream))
+                                            C.byref(n), self.gstream))
+        if join:
+            self.join()
         return n.value
+
+    def join(self):
+        """Orders `stream` after every gather issued so far."""
+        self.ctx.record(self._gdone, self.gstream)
+        check(N.lib().tg_stream_wait_event(self.ctx.handle, self.stream, self._gdone))
+
+    def run_pipelined(self, steps: int, exchange=None) -> int:
+        """`steps` passes over the shard's frames with the host batcher of
+        pass i overlapping the device planes (K1-K4) of pass i+1; K5 of pass
+        i runs on `gstream`.  `exchange(desc) -> desc` (e.g. the NCCL
+        descriptor all-gather) runs before each schedule.  Returns the last
+        pass's canvas count; `stream` is joined with every gather."""
+        n_canv = 0
+        self.run_planes()
+        desc = self.descriptors()
+        for i in range(steps):
+            if i + 1 < steps:
+                self.run_planes()
+            if exchange is not None:
+                desc = exchange(desc)
+            self.schedule(desc)
+            n_canv = self.gather(join=False)
+            if i + 1 < steps:
+                desc = self.descriptors()
+        self.join()
+        return n_canv
 
     def step(self):
         self.run_planes()
@@ -155,6 +195,14 @@ class MultiCameraPath:
         n_events = self.schedule(desc)
         n_canvases = self.gather()
         return desc, n_events, n_canvases
+
+    def camera_results(self, k: int) -> dict:
+        """Per-frame results (RoIs, patches, ...) of the shard's k-th camera
+        from the last step (blocking download)."""
+        n = self.n
+        res = self.pipe.results(len(self.cameras) * n, self.stream)
+        return {key: (val[k * n:(k + 1) * n] if isinstance(val, np.ndarray) else val)
+                for key, val in res.items() if key in ("n_rois", "rois", "n_patches", "admitted")}
 
     def events(self):
         """InvokeEvents of the last step (readable until the next batcher call)."""
@@ -167,29 +215,26 @@ class MultiCameraPath:
 
 def schedule_descriptors(sched, desc: np.ndarray, cameras, n_frames: int, bandwidth_mbps: float,
                          per_camera_link: bool = True):
-    """Host half of configs 3/4 on DESC_DTYPE records (camera-major, frame
-    and zone order): ids renumbered camera-major over all patches
-    (sim.hpp:249-251), admitted ones (sim.hpp:262) sent over the uplinks and
-    replayed through `sched` (an api.SloScheduler).  Returns (number of
-    events, arrival times of the admitted patches, plan dict)."""
-    d = np.array(desc, copy=True)
-    d["patch"]["patch_id"] = np.arange(len(d), dtype=np.uint64)
-    adm = d[d["admitted"] != 0]
-    cams = np.asarray(list(cameras), np.int64)
-    lut = np.full(int(cams.max()) + 1 if len(cams) else 1, -1, np.int32)
-    lut[cams] = np.arange(len(cams), dtype=np.int32)
-    cam_slot = lut[adm["camera"]]
-    offs = np.zeros(len(cams) + 1, np.int32)
-    offs[1:] = np.cumsum(np.bincount(cam_slot, minlength=len(cams)))
-    src = (cam_slot * (n_frames + 1) + adm["frame"] + 1).astype(np.int32)
-    patches = np.ascontiguousarray(adm["patch"])
-    arrival = np.zeros(max(1, len(patches)), np.int64)
-    n_ev = C.c_int32()
-    check(N.lib().tg_batcher_replay_links(sched.handle, len(cams), offs.ctypes.data,
-                                          patches.ctypes.data, src.ctypes.data,
-                                          float(bandwidth_mbps), int(per_camera_link),
-                                          arrival.ctypes.data, C.byref(n_ev)))
-    return n_ev.value, arrival[:len(patches)], dict(patches=patches, src=src, offs=offs)
+    """Host half of configs 3/4 on DESC_DTYPE records (camera-major in the
+    order of `cameras`, frame and zone order), tg_batcher_schedule: ids
+    renumbered over all patches (sim.hpp:249-251), admitted ones
+    (sim.hpp:262) sent over the uplinks and replayed through `sched` (an
+    api.SloScheduler).  Returns (number of events, arrival times of the
+    admitted patches, dict(patches=their renumbered metas, src=their frame
+    table indices))."""
+    desc = np.ascontiguousarray(desc, DESC_DTYPE)
+    cams = np.ascontiguousarray(list(cameras), np.int32)
+    n = len(desc)
+    patches = np.zeros(max(1, n), PATCH_DTYPE)
+    src = np.zeros(max(1, n), np.int32)
+    arrival = np.zeros(max(1, n), np.int64)
+    n_adm, n_ev = C.c_int64(), C.c_int32()
+    check(N.lib().tg_batcher_schedule(sched.handle, desc.ctypes.data, n, cams.ctypes.data,
+                                      len(cams), n_frames, float(bandwidth_mbps),
+                                      int(per_camera_link), patches.ctypes.data, src.ctypes.data,
+                                      arrival.ctypes.data, C.byref(n_adm), C.byref(n_ev)))
+    k = n_adm.value
+    return n_ev.value, arrival[:k], dict(patches=patches[:k], src=src[:k])
 
 
 def gather_descriptors(local: np.ndarray, dist, device=None) -> np.ndarray:

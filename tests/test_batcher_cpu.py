@@ -234,3 +234,37 @@ def test_multi_camera_stream_matches_reference_simulator(n_cams, W, H, bw, kw):
                e["patch_ids"]) for e in ref["events"]]
     assert ours == theirs
     assert len(ours) > 0
+
+
+def test_descriptor_compaction_layout():
+    """tg_descriptors_compact: pipeline slots [F][Z] -> camera-major records."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_2404_09267_b200 import _native as N
+    from paper_2404_09267_b200 import multicam as MC
+    rng = np.random.default_rng(5)
+    cams, n, Z = np.array([3, 7, 9], np.int32), 4, 16
+    F = len(cams) * n
+    pat = np.zeros(F * Z, MC.PATCH_DTYPE)
+    pat["patch_id"] = np.arange(F * Z)
+    pat["w"] = rng.integers(1, 2000, F * Z)
+    adm = rng.integers(0, 2, F * Z).astype(np.uint8)
+    cnt = rng.integers(0, Z + 1, F).astype(np.int32)
+    out = np.zeros(F * Z, MC.DESC_DTYPE)
+    k = C.c_int64()
+    A.check(N.lib().tg_descriptors_compact(pat.ctypes.data, cnt.ctypes.data, adm.ctypes.data, Z,
+                                           cams.ctypes.data, len(cams), n, out.ctypes.data,
+                                           len(out), C.byref(k)))
+    valid = (np.arange(Z)[None, :] < cnt[:, None]).reshape(-1)
+    assert k.value == int(valid.sum())
+    got = out[:k.value]
+    assert np.array_equal(got["patch"], pat[valid])
+    assert np.array_equal(got["admitted"], adm[valid].astype(np.int32))
+    assert np.array_equal(got["camera"], np.repeat(cams, n * Z)[valid])
+    assert np.array_equal(got["frame"], np.tile(np.repeat(np.arange(n), Z), len(cams))[valid])
+    with pytest.raises(A.CapacityError):
+        A.check(N.lib().tg_descriptors_compact(pat.ctypes.data, cnt.ctypes.data, adm.ctypes.data,
+                                               Z, cams.ctypes.data, len(cams), n, out.ctypes.data,
+                                               max(0, k.value - 1), C.byref(k)))

@@ -65,6 +65,15 @@ def _worker(rank, world, port, q):
         n_ev, arrival, _ = MC.schedule_descriptors(sched, local, mine, N_FRAMES, 40.0)
         evs = [(e.fire_time_us, e.trigger, e.batch_size, e.estimated_slack_us, e.patch_ids)
                for e in sched._events(n_ev)]
+        # the same shard scheduled from the all-gathered list: global ids
+        # (sim.hpp:249-251), other shards' records skipped -- same decisions
+        sched_g = A.SloScheduler(A.CanvasSpec(1024, 1024), A.LatencyProfile(1024, 1024, PROFILE),
+                                 A.max_canvases_per_batch(6.0, 2.0, 1.0))
+        n_g, _, _ = MC.schedule_descriptors(sched_g, glob, mine, N_FRAMES, 40.0)
+        off = int((glob["camera"] < mine[0]).sum())
+        evs_g = [(e.fire_time_us, e.trigger, e.batch_size, e.estimated_slack_us,
+                  [i - off for i in e.patch_ids]) for e in sched_g._events(n_g)]
+        same = same and evs_g == evs
         ref = None
         if O.have_ref():
             r = O.run_tangram([scene(c) for c in mine], W, H, PROFILE, bandwidth_mbps=40.0)

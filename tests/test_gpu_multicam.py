@@ -34,7 +34,7 @@ def test_multicam_events_and_canvases_match_reference(ctx, cams, W, H, n, bw, li
     # the GPU's RoIs, as the reference simulator's input scenes
     scenes, frames = [], []
     for k, c in enumerate(cams):
-        res = path.pipes[k].results(n)
+        res = path.camera_results(k)
         rois = [[tuple(r) for r in res["rois"][f, :res["n_rois"][f]].tolist()] for f in range(n)]
         scenes.append((path.t_us[k], rois))
         frames.append([path.rings[k].download_frame(s) for s in range(n + 1)])

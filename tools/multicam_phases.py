@@ -13,7 +13,7 @@ ctx = A.Context(0)
 path = MC.MultiCameraPath(ctx, list(range(ncam)), W, H, frames, bench.SIM_PROFILE,
                           bandwidth_mbps=bench.SIM_BANDWIDTH_MBPS, gpu_memory_gb=bench.SIM_GPU_MEMORY_GB,
                           model_size_gb=4.0, trace_kw=dict(roi_proportion_mean=0.10, roi_max_dim=480))
-for it in range(4):
+for it in range(6):
     t0 = time.perf_counter()
     path.run_planes()
     ctx.stream_sync(path.stream)
