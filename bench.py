@@ -52,6 +52,10 @@ def parse():
                     help="cfg2 (default, the headline): per-frame path, 1 camera x 300 frames per "
                          "GPU; cfg3: 5 cameras batched across cameras on 1 GPU; cfg4: 64 cameras "
                          "sharded over the ranks; cfg5: RoI-density sweep")
+    ap.add_argument("--global-batching", action="store_true",
+                    help="cfg3/cfg4 at N>1: one batcher over every camera (the reference's single "
+                         "scheduler), replicated per rank; rank r writes invoke events r, r+N, ... "
+                         "reading peer frames over CUDA IPC / NVLink (default: shard-local)")
     return ap.parse_args()
 
 
@@ -471,13 +475,17 @@ def run_multicam(args):
     frames = min(args.frames, 300 if args.config == "cfg3" else 30)
     cams = MC.shard_cameras(n_cams_total, world, rank)
     ctx = A.Context(local)
-    path = MC.MultiCameraPath(ctx, cams, W, H, frames, SIM_PROFILE,
-                              bandwidth_mbps=SIM_BANDWIDTH_MBPS,
-                              gpu_memory_gb=SIM_GPU_MEMORY_GB, model_size_gb=4.0,
-                              trace_kw=dict(roi_proportion_mean=0.10, roi_max_dim=480))
+    kw = dict(bandwidth_mbps=SIM_BANDWIDTH_MBPS, gpu_memory_gb=SIM_GPU_MEMORY_GB, model_size_gb=4.0,
+              trace_kw=dict(roi_proportion_mean=0.10, roi_max_dim=480))
+    glob = args.global_batching and dist is not None
+    if glob:
+        path = MC.GlobalCameraPath(ctx, n_cams_total, rank, world, dist, W, H, frames, SIM_PROFILE,
+                                   device=f"cuda:{local}", **kw)
+    else:
+        path = MC.MultiCameraPath(ctx, cams, W, H, frames, SIM_PROFILE, **kw)
     e0, e1 = ctx.event(), ctx.event()
     exchange = None
-    if dist is not None:
+    if dist is not None and not glob:
         # every rank schedules its shard from the all-gathered list (global ids)
         def exchange(desc):
             return MC.gather_descriptors(desc, dist, device=f"cuda:{local}")
@@ -511,7 +519,9 @@ def run_multicam(args):
         "data": "synthetic (generate_trace rects, frozen pixel spec, device-resident)",
         "config": {"workload": f"BASELINE configs[{2 if args.config == 'cfg3' else 3}]: "
                                f"{n_cams_total} synthetic 4K cameras, {frames} frames each, "
-                               "SLO batcher across cameras, shard-local canvases",
+                               "SLO batcher across cameras, " +
+                               ("one global batcher, events split over the ranks, peer frames "
+                                "over CUDA IPC" if glob else "shard-local canvases"),
                    "cameras_per_gpu": len(cams), "frames_per_camera": frames,
                    "bandwidth_mbps": SIM_BANDWIDTH_MBPS, "profile": SIM_PROFILE,
                    "max_canvases_per_batch": path.max_canvases,
@@ -519,7 +529,7 @@ def run_multicam(args):
                                   (", NCCL all-gather of patch descriptors" if world > 1 else ""),
                    "pipelining": "host batcher of pass i overlaps device K1-K4 of pass i+1; "
                                  "K5 on its own stream; timed region = K whole passes"},
-        "batching": {"events": n_events, "canvases": n_canv,
+        "batching": {"events": n_events, ("canvases_rank0" if glob else "canvases"): n_canv,
                      "patches_admitted": int(len(path._last["patches"]))},
         "clocks": clk, "gpu_launches": 4 * args.steps,  # K1, plan, scan, gather
     }

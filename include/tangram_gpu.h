@@ -115,6 +115,15 @@ tg_status tg_device_sm_count(tg_ctx* ctx, int32_t* sms);
 tg_status tg_malloc_device(tg_ctx* ctx, size_t bytes, void** d_ptr);
 tg_status tg_free_device(tg_ctx* ctx, void* d_ptr);
 tg_status tg_malloc_host(tg_ctx* ctx, size_t bytes, void** h_ptr); /* pinned */
+/* Cross-process device memory (global cross-camera mode): a
+ * rank exports the base of a tg_malloc_device allocation (its cameras'
+ * frame rings); peers import it as a device pointer they can read -- over
+ * NVLink from another GPU, or the same memory from another process on this
+ * one.  Imported pointers are released with tg_ipc_close. */
+typedef struct { uint8_t bytes[64]; } tg_ipc_handle;
+tg_status tg_ipc_export(tg_ctx* ctx, void* d_ptr, tg_ipc_handle* out);
+tg_status tg_ipc_import(tg_ctx* ctx, const tg_ipc_handle* handle, void** d_ptr);
+tg_status tg_ipc_close(tg_ctx* ctx, void* d_ptr);
 tg_status tg_free_host(tg_ctx* ctx, void* h_ptr);
 /* kind: 0 host->device, 1 device->host, 2 device->device; async on stream */
 tg_status tg_memcpy_async(tg_ctx* ctx, void* dst, const void* src, size_t bytes, int32_t kind,
@@ -322,6 +331,12 @@ tg_status tg_batcher_gather(tg_ctx* ctx, tg_batcher* b, int32_t i, const uint8_t
 tg_status tg_batcher_gather_all(tg_ctx* ctx, tg_batcher* b, const uint8_t* const* d_frames,
                                 int32_t pitch, uint8_t* d_canvases, int64_t canvas_cap,
                                 int64_t* n_canvases, void* stream);
+/* Same for the events i with i % stride == first (event order): how the
+ * ranks of the global cross-camera mode split the invokes between them. */
+tg_status tg_batcher_gather_events(tg_ctx* ctx, tg_batcher* b, int32_t first, int32_t stride,
+                                   const uint8_t* const* d_frames, int32_t pitch,
+                                   uint8_t* d_canvases, int64_t canvas_cap, int64_t* n_canvases,
+                                   void* stream);
 /* Offline driver of the reference event loop for the tangram policy
  * (sim.hpp:334-342, 425-458): arrivals ordered by (arrival_us, input order),
  * a timer is queued when its epoch is new and loses ties to arrivals.  All

@@ -84,6 +84,10 @@ class tg_gather_job(C.Structure):
                 ("src_y", C.c_int32)]
 
 
+class tg_ipc_handle(C.Structure):
+    _fields_ = [("bytes", C.c_uint8 * 64)]
+
+
 class tg_profile_entry(C.Structure):
     _fields_ = [("batch_size", C.c_int32), ("mu_ms", C.c_double), ("sigma_ms", C.c_double)]
 
@@ -115,6 +119,9 @@ SIGNATURES = {
     "tg_malloc_device": (st, [vp, sz, P(vp)]),
     "tg_free_device": (st, [vp, vp]),
     "tg_malloc_host": (st, [vp, sz, P(vp)]),
+    "tg_ipc_export": (st, [vp, vp, P(tg_ipc_handle)]),
+    "tg_ipc_import": (st, [vp, P(tg_ipc_handle), P(vp)]),
+    "tg_ipc_close": (st, [vp, vp]),
     "tg_free_host": (st, [vp, vp]),
     "tg_memcpy_async": (st, [vp, vp, vp, sz, i32, vp]),
     "tg_memset_async": (st, [vp, vp, i32, sz, vp]),
@@ -163,6 +170,7 @@ SIGNATURES = {
                               P(tg_free_rect)]),
     "tg_batcher_gather": (st, [vp, vp, i32, vp, i32, vp, vp]),
     "tg_batcher_gather_all": (st, [vp, vp, vp, i32, vp, i64, P(i64), vp]),
+    "tg_batcher_gather_events": (st, [vp, vp, i32, i32, vp, i32, vp, i64, P(i64), vp]),
     "tg_batcher_replay": (st, [vp, P(tg_patch_meta), P(i32), P(i64), i32, P(i32)]),
     "tg_batcher_replay_links": (st, [vp, i32, vp, vp, vp, C.c_double, i32, vp, P(i32)]),
     "tg_descriptors_compact": (st, [vp, vp, vp, i32, vp, i32, i32, vp, i64, P(i64)]),

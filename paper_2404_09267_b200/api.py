@@ -233,6 +233,22 @@ class Context:
     def free_host(self, ptr: int) -> None:
         check(self._lib.tg_free_host(self.handle, ptr))
 
+    def ipc_export(self, dptr: int) -> bytes:
+        """64-byte handle of a device allocation for other processes."""
+        h = N.tg_ipc_handle()
+        check(self._lib.tg_ipc_export(self.handle, dptr, C.byref(h)))
+        return bytes(h.bytes)
+
+    def ipc_import(self, handle: bytes) -> int:
+        h = N.tg_ipc_handle()
+        C.memmove(h.bytes, handle, 64)
+        p = C.c_void_p()
+        check(self._lib.tg_ipc_import(self.handle, C.byref(h), C.byref(p)))
+        return p.value
+
+    def ipc_close(self, dptr: int) -> None:
+        check(self._lib.tg_ipc_close(self.handle, dptr))
+
     def memcpy(self, dst: int, src: int, nbytes: int, kind: int, stream=None) -> None:
         check(self._lib.tg_memcpy_async(self.handle, dst, src, nbytes, kind, stream))
 

@@ -297,6 +297,33 @@ tg_status tg_malloc_host(tg_ctx* ctx, size_t bytes, void** h_ptr) {
   return TG_OK;
 }
 
+tg_status tg_ipc_export(tg_ctx* ctx, void* d_ptr, tg_ipc_handle* out) {
+  tg_status s = use_device(ctx);
+  if (s) return s;
+  static_assert(sizeof(cudaIpcMemHandle_t) <= sizeof(tg_ipc_handle), "ipc handle size");
+  cudaIpcMemHandle_t h;
+  TG_CUDA(cudaIpcGetMemHandle(&h, d_ptr));
+  memset(out, 0, sizeof(*out));
+  memcpy(out->bytes, &h, sizeof(h));
+  return TG_OK;
+}
+
+tg_status tg_ipc_import(tg_ctx* ctx, const tg_ipc_handle* handle, void** d_ptr) {
+  tg_status s = use_device(ctx);
+  if (s) return s;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle->bytes, sizeof(h));
+  TG_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return TG_OK;
+}
+
+tg_status tg_ipc_close(tg_ctx* ctx, void* d_ptr) {
+  tg_status s = use_device(ctx);
+  if (s) return s;
+  TG_CUDA(cudaIpcCloseMemHandle(d_ptr));
+  return TG_OK;
+}
+
 tg_status tg_free_host(tg_ctx* ctx, void* h_ptr) {
   tg_status s = use_device(ctx);
   if (s) return s;

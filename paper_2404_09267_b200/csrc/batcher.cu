@@ -489,13 +489,17 @@ tg_status tg_batcher_gather(tg_ctx* ctx, tg_batcher* b, int32_t i, const uint8_t
                                 d_canvases, stream);
 }
 
-tg_status tg_batcher_gather_all(tg_ctx* ctx, tg_batcher* b, const uint8_t* const* d_frames,
-                                int32_t pitch, uint8_t* d_canvases, int64_t canvas_cap,
-                                int64_t* n_canvases, void* stream) {
+tg_status tg_batcher_gather_events(tg_ctx* ctx, tg_batcher* b, int32_t first, int32_t stride,
+                                   const uint8_t* const* d_frames, int32_t pitch,
+                                   uint8_t* d_canvases, int64_t canvas_cap, int64_t* n_canvases,
+                                   void* stream) {
+  *n_canvases = 0;
+  if (stride < 1 || first < 0 || first >= stride)
+    return bfail(TG_ERR_INVALID_ARGUMENT, "event subset needs 0 <= first < stride");
   std::vector<Job> jobs;
   std::vector<uint2> ranges;
-  for (const Event& ev : b->events) {
-    const tg_status s = append_event_plan(ev, jobs, ranges);
+  for (size_t e = static_cast<size_t>(first); e < b->events.size(); e += static_cast<size_t>(stride)) {
+    const tg_status s = append_event_plan(b->events[e], jobs, ranges);
     if (s) return s;
   }
   *n_canvases = static_cast<int64_t>(ranges.size());
@@ -505,6 +509,13 @@ tg_status tg_batcher_gather_all(tg_ctx* ctx, tg_batcher* b, const uint8_t* const
   return tg_internal_run_gather(ctx, jobs.data(), static_cast<int32_t>(jobs.size()), ranges.data(),
                                 static_cast<int32_t>(ranges.size()), b->spec, d_frames, pitch,
                                 d_canvases, stream);
+}
+
+tg_status tg_batcher_gather_all(tg_ctx* ctx, tg_batcher* b, const uint8_t* const* d_frames,
+                                int32_t pitch, uint8_t* d_canvases, int64_t canvas_cap,
+                                int64_t* n_canvases, void* stream) {
+  return tg_batcher_gather_events(ctx, b, 0, 1, d_frames, pitch, d_canvases, canvas_cap,
+                                  n_canvases, stream);
 }
 
 tg_status tg_batcher_replay(tg_batcher* b, const tg_patch_meta* patches, const int32_t* src_frames,

@@ -213,6 +213,84 @@ class MultiCameraPath:
                                  np.uint8, self.stream)
 
 
+class GlobalCameraPath(MultiCameraPath):
+    """Global cross-camera mode: ONE batcher over every camera
+    of the job -- the reference's single SloScheduler over all scenes
+    (sim.hpp:392) -- replicated on every rank from the all-gathered
+    descriptors, so all ranks take the same decisions without a broadcast.
+    Rank r writes the canvases of invoke events r, r+G, r+2G, ...; patches
+    of other ranks' cameras are read straight from their frame rings through
+    CUDA IPC (peer reads over NVLink; on one GPU, the same memory).  Each
+    rank still runs K1-K4 only on its own cameras.
+
+    `dist` is torch.distributed (gloo or NCCL): it exchanges the rings' IPC
+    handles once, here, and the descriptors every pass (`exchange`)."""
+
+    def __init__(self, ctx: Context, n_cameras: int, rank: int, world: int, dist, width, height,
+                 n_frames, profile, device=None, **kw):
+        super().__init__(ctx, shard_cameras(n_cameras, world, rank), width, height, n_frames,
+                         profile, **kw)
+        self.all_cameras = list(range(n_cameras))
+        self.rank, self.world, self.dist, self.device = rank, world, dist, device
+        mine = [(c, ctx.ipc_export(r.base)) for c, r in zip(self.cameras, self.rings)]
+        every = [None] * world
+        dist.all_gather_object(every, mine)
+        base, self._imported = {}, []
+        for r, owned in enumerate(every):
+            for c, h in owned:
+                if r == rank:
+                    base[c] = self.rings[self.cameras.index(c)].base
+                else:
+                    base[c] = ctx.ipc_import(h)
+                    self._imported.append(base[c])
+        fb = self.rings[0].frame_bytes if self.rings else 3 * width * height
+        ptrs = np.array([base[c] + s * fb for c in self.all_cameras for s in range(n_frames + 1)],
+                        np.uint64)
+        self.d_frames_global = ctx.malloc(8 * max(1, len(ptrs)))
+        ctx.upload(self.d_frames_global, ptrs)
+        self.frame_base = base
+
+    def close(self):
+        for p in self._imported:
+            self.ctx.ipc_close(p)
+        self._imported = []
+        self.ctx.free(self.d_frames_global)
+        super().close()
+
+    def exchange(self, desc: np.ndarray) -> np.ndarray:
+        return gather_descriptors(desc, self.dist, device=self.device)
+
+    def schedule(self, desc: np.ndarray):
+        """`desc`: the all-gathered list of every camera."""
+        self._nev, self.arrival, self._last = schedule_descriptors(
+            self.sched, desc, self.all_cameras, self.n, self.bandwidth, self.per_camera_link)
+        return self._nev
+
+    def gather(self, join: bool = True) -> int:
+        if self.d_canvases is None:
+            cap = self.canvas_cap or max(1, len(self._last["patches"]))
+            self.canvas_cap = cap
+            self.d_canvases = self.ctx.malloc(cap * self.canvas_bytes)
+        n = C.c_int64()
+        check(N.lib().tg_batcher_gather_events(self.ctx.handle, self.sched.handle, self.rank,
+                                               self.world, self.d_frames_global, 3 * self.W,
+                                               self.d_canvases, self.canvas_cap, C.byref(n),
+                                               self.gstream))
+        if join:
+            self.join()
+        return n.value
+
+    def step(self):
+        self.run_planes()
+        desc = self.exchange(self.descriptors())
+        n_events = self.schedule(desc)
+        n_canvases = self.gather()
+        return desc, n_events, n_canvases
+
+    def run_pipelined(self, steps: int, exchange=None) -> int:
+        return super().run_pipelined(steps, exchange or self.exchange)
+
+
 def schedule_descriptors(sched, desc: np.ndarray, cameras, n_frames: int, bandwidth_mbps: float,
                          per_camera_link: bool = True):
     """Host half of configs 3/4 on DESC_DTYPE records (camera-major in the

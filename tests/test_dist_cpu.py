@@ -74,12 +74,24 @@ def _worker(rank, world, port, q):
         evs_g = [(e.fire_time_us, e.trigger, e.batch_size, e.estimated_slack_us,
                   [i - off for i in e.patch_ids]) for e in sched_g._events(n_g)]
         same = same and evs_g == evs
+        # global cross-camera mode: every rank replays ONE batcher over all
+        # cameras from the gathered list -- the reference's single scheduler
+        sched_all = A.SloScheduler(A.CanvasSpec(1024, 1024),
+                                   A.LatencyProfile(1024, 1024, PROFILE),
+                                   A.max_canvases_per_batch(6.0, 2.0, 1.0))
+        n_all, _, _ = MC.schedule_descriptors(sched_all, glob, range(N_CAMS), N_FRAMES, 40.0)
+        evs_all = [(e.fire_time_us, e.trigger, e.batch_size, e.estimated_slack_us, e.patch_ids)
+                   for e in sched_all._events(n_all)]
         ref = None
         if O.have_ref():
             r = O.run_tangram([scene(c) for c in mine], W, H, PROFILE, bandwidth_mbps=40.0)
             names = {0: "deadline_timer", 1: "infeasible_arrival", 2: "memory_cap"}
             ref = [(e["fire_time_us"], names[e["trigger"]], e["batch_size"], e["estimated_slack_us"],
                     e["patch_ids"]) for e in r["events"]]
+            r = O.run_tangram([scene(c) for c in range(N_CAMS)], W, H, PROFILE, bandwidth_mbps=40.0)
+            ref_all = [(e["fire_time_us"], names[e["trigger"]], e["batch_size"],
+                        e["estimated_slack_us"], e["patch_ids"]) for e in r["events"]]
+            same = same and evs_all == ref_all
         q.put((rank, mine, same, len(glob), evs, ref))
         dist.destroy_process_group()
     except Exception as e:  # surface worker failures in the parent
@@ -114,7 +126,8 @@ def test_two_rank_descriptor_allgather_and_shard_batching():
         p.join(timeout=60)
     for rank, mine, same, n_glob, evs, ref in res:
         assert mine is not None, same
-        assert same is True, f"rank {rank}: gathered descriptors differ from the global list"
+        assert same is True, (f"rank {rank}: gathered list, shard-from-gathered schedule or global "
+                              "batching differs")
         assert n_glob == len(descriptors(range(N_CAMS)))
         assert evs, rank
         if ref is not None:
