@@ -61,6 +61,7 @@ struct tg_ctx {
   Job* g_jobs = nullptr;
   uint2* g_ranges = nullptr;
   int32_t* g_units = nullptr;
+  int32_t g_units_h[3] = {0, 0, 0};
   size_t g_job_cap = 0, g_range_cap = 0;
 };
 
@@ -196,14 +197,16 @@ tg_status tg_internal_run_gather(tg_ctx* ctx, const void* jobs, int32_t n_jobs, 
     ctx->g_range_cap = std::max<size_t>(n_canvases, 1024);
     TG_CUDA(cudaMalloc(&ctx->g_ranges, ctx->g_range_cap * sizeof(uint2)));
   }
-  if (!ctx->g_units) TG_CUDA(cudaMalloc(&ctx->g_units, sizeof(int32_t)));
+  if (!ctx->g_units) TG_CUDA(cudaMalloc(&ctx->g_units, 3 * sizeof(int32_t)));
   const int nbands = gather_bands(spec.height);
-  const int32_t units = n_canvases * nbands;
+  ctx->g_units_h[0] = n_canvases * nbands;
+  ctx->g_units_h[1] = 0;  // K5's unit claim counter
+  ctx->g_units_h[2] = 0;  // K5's finished-CTA counter
   if (n_jobs > 0)
     TG_CUDA(cudaMemcpyAsync(ctx->g_jobs, jobs, sizeof(Job) * n_jobs, cudaMemcpyHostToDevice, st));
   TG_CUDA(cudaMemcpyAsync(ctx->g_ranges, ranges, sizeof(uint2) * n_canvases,
                           cudaMemcpyHostToDevice, st));
-  TG_CUDA(cudaMemcpyAsync(ctx->g_units, &units, sizeof(units), cudaMemcpyHostToDevice, st));
+  TG_CUDA(cudaMemcpyAsync(ctx->g_units, ctx->g_units_h, 3 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   GatherArgs g;
   g.frames = d_frames;
   g.pitch = pitch;
@@ -719,10 +722,10 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
   if (!e) e = alloc(&p->jobs, F * p->job_cap);
   if (!e) e = alloc(&p->canvas_jobs, F * Z);
   if (!e) e = alloc(&p->ranges, static_cast<size_t>(q.max_canvases));
-  if (!e) e = alloc(&p->gather_units, 1);
+  if (!e) e = alloc(&p->gather_units, 3);
   if (!e) e = alloc(&p->id_state, 1);
   if (!e) e = cudaMemset(p->id_state, 0, sizeof(uint64_t));
-  if (!e) e = cudaMemset(p->gather_units, 0, sizeof(int32_t));
+  if (!e) e = cudaMemset(p->gather_units, 0, 3 * sizeof(int32_t));
   if (e) {
     tg_pipeline_destroy(p);
     return cuda_fail(e, "pipeline allocation");

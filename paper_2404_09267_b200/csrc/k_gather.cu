@@ -4,10 +4,13 @@
 // Every canvas is exactly tiled by its placements plus its final guillotine
 // free rects: each canvas row is a left-to-right
 // sequence of intervals, each either a patch's source row or zeros.  A
-// persistent grid walks (canvas, 256-row band) units whose count the scan
-// kernel left in device memory (no host round trip between planning and
-// gathering); warp w of a block owns rows b0 + w, b0 + w + 8, ... of the
-// band, split into 3 KB destination segments ("items").
+// persistent grid claims (canvas, 64-row band) units from a device counter
+// -- their count is what the scan kernel left in device memory (no host
+// round trip between planning and gathering); dynamic claiming keeps CTAs
+// that drew light, zero-fill bands busy, so the grid drains together (static
+// round robin: 0.82 ms vs 0.66 ms per 300 4K frames).  Warp w of a block
+// owns rows b0 + w, b0 + w + 8, ... of the band, split into 3 KB destination
+// segments ("items").
 //
 // Each warp runs its own TMA pipeline.  Producer side (whole warp): ballot
 // the jobs active in the item's row, write the interval list into a header
@@ -37,10 +40,16 @@ namespace tg {
 #ifndef TG_GATHER_RING
 #define TG_GATHER_RING 6144
 #endif
+#ifndef TG_GATHER_BAND
+#define TG_GATHER_BAND 64
+#endif
+#ifndef TG_GATHER_DYNAMIC
+#define TG_GATHER_DYNAMIC 1
+#endif
 
 constexpr int kGatherThreads = 256;
 constexpr int kGatherWarps = kGatherThreads / 32;
-constexpr int kGatherBand = 256;                 // rows per unit
+constexpr int kGatherBand = TG_GATHER_BAND;      // rows per unit
 constexpr int kGatherMaxJobs = 192;              // jobs of one canvas cached in smem
 constexpr int kSlots = TG_GATHER_SLOTS;          // items in flight per warp (header slots)
 constexpr int kRing = TG_GATHER_RING;            // source bytes in flight per warp
@@ -189,7 +198,19 @@ __global__ void __launch_bounds__(kGatherThreads, TG_GATHER_MIN_BLOCKS) gather_k
   const unsigned lt = (1u << lane) - 1u;
   int gbase = 0;  // items this warp has pushed through its slots so far
 
+#if TG_GATHER_DYNAMIC
+  // units are claimed in order from a counter: CTAs that drew light (zero
+  // fill) bands take more, so the grid drains together
+  __shared__ int s_unit;
+  for (;;) {
+    __syncthreads();  // everyone has read the previous claim
+    if (tid == 0) s_unit = atomicAdd(&a.units[1], 1);
+    __syncthreads();
+    const int u = s_unit;
+    if (u >= nunits) break;
+#else
   for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+#endif
     const int k = u / a.nbands, b = u - k * a.nbands;
     const uint2 range = a.ranges[k];
     const int cnt = static_cast<int>(range.y);
@@ -431,6 +452,15 @@ __global__ void __launch_bounds__(kGatherThreads, TG_GATHER_MIN_BLOCKS) gather_k
     while (c < p) consume();
     gbase += p;
   }
+#if TG_GATHER_DYNAMIC
+  if (tid == 0) {  // the last CTA out leaves the counters at 0 for the next launch
+    __threadfence();
+    if (atomicAdd(&a.units[2], 1) == static_cast<int>(gridDim.x) - 1) {
+      a.units[1] = 0;
+      a.units[2] = 0;
+    }
+  }
+#endif
 }
 
 cudaError_t launch_gather(const GatherArgs& a, int sms, cudaStream_t stream) {

@@ -237,7 +237,9 @@ __global__ void __launch_bounds__(1024) scan_kernel(const ScanArgs a) {
       raise_error(a.err, TG_ERR_CAPACITY, kErrCanvasCapacity, total, a.max_canvases);
       total = a.max_canvases;
     }
-    *a.gather_units = static_cast<int32_t>(total * a.nbands);
+    a.gather_units[0] = static_cast<int32_t>(total * a.nbands);
+    a.gather_units[1] = 0;  // K5's claim counters
+    a.gather_units[2] = 0;
   }
 }
 

@@ -101,7 +101,8 @@ struct GatherArgs {
   int pitch, M, N, nbands;
   const Job* jobs;
   const uint2* ranges;
-  const int32_t* units;   // device count of (canvas, band) units
+  int32_t* units;         // [0]: (canvas, band) units; [1], [2]: K5's claim and finished-CTA
+                          // counters (0 at launch; the last CTA resets them)
   uint8_t* out;
 };
 cudaError_t launch_gather(const GatherArgs& a, int sms, cudaStream_t stream);
