@@ -251,10 +251,24 @@ __device__ int ccl_frame(const uint32_t* gact, const uint32_t* gcells, int cx_n,
       const int rank = s.wpre[rw] + __popc(s.rootm[rw] & ((1u << ro) - 1u));
       if (rank >= nr) continue;
       const uint32_t* crow = gcells + static_cast<size_t>(cy) * cx_n;
-      const uint32_t va = crow[a0], ve = crow[e];
+      const uint32_t va = __ldg(crow + a0), ve = __ldg(crow + e);
+      // y extent over the run's cell summaries (global, L2): eight loads in
+      // flight per step -- a run can span a whole cell row, and one thread's
+      // serial load chain would gate the CTA at the next barrier
       int y0 = INT_MAX, y1 = INT_MIN;
-      for (int cx = a0; cx <= e; ++cx) {
-        const uint32_t v = crow[cx];
+      int cx = a0;
+      for (; cx + 8 <= e + 1; cx += 8) {
+        uint32_t v[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[t] = __ldg(crow + cx + t);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          y0 = min(y0, static_cast<int>(v[t] >> 17 & 15u));
+          y1 = max(y1, static_cast<int>(v[t] >> 21 & 15u));
+        }
+      }
+      for (; cx <= e; ++cx) {
+        const uint32_t v = __ldg(crow + cx);
         y0 = min(y0, static_cast<int>(v >> 17 & 15u));
         y1 = max(y1, static_cast<int>(v >> 21 & 15u));
       }
