@@ -30,13 +30,18 @@
 // -> packed u32 cell summaries plus an activity bitmask (and the dilated mask
 // on request).
 //
-// Fused launch (launch_mask_fused, the pipeline's mask stage): K1 CTAs carry
-// 3 extra warps that run the K1b tasks while K1 streams.  K1 is HBM bound and
-// leaves issue slots idle; a task starts once every K1 item covering its rows
-// has published completion (per-item counters, release/acquire), reads the
-// freshly written raw rows from L2, and the last strips are finished by all
-// warps after the stream ends.  Cooperative launch guarantees that all CTAs
-// are co-resident, so waiting on other CTAs' items cannot deadlock.
+// Fused launch (launch_mask_fused, the pipeline's mask stage): once a K1
+// CTA's items are streamed, all its warps take K1b tasks from a queue in
+// strip order; a task starts once every K1 item covering its rows has
+// published completion (per-item counters, release/acquire), so the early
+// strips run on CTAs that finish first while others still stream.
+// Cooperative launch guarantees that all CTAs are co-resident, so waiting on
+// other CTAs' items cannot deadlock.  Measured alternatives (300 4K frames,
+// mask stage): 1 / 3 / 5 extra warps running K1b tasks beside the stream
+// 1.29 / 1.31 / 1.46 ms vs 1.27 ms without (TG_K1_DILATE_WARPS) -- the task
+// warps slow the stream more than they hide; L2 evict_first on the frame
+// stream + evict_last on the raw words (TG_K1_L2HINTS) cut DRAM reads by
+// 0.14 GB but not time (1.28 ms).
 #include <algorithm>
 #include <cstdlib>
 
@@ -44,11 +49,21 @@
 
 namespace tg {
 
+#ifndef TG_K1_L2HINTS
+#define TG_K1_L2HINTS 0
+#endif
+#ifndef TG_K1_TASKS_REVERSED
+#define TG_K1_TASKS_REVERSED 0
+#endif
+
 constexpr int kK1MaxPartWords = 64;     // 32-pixel words per unit (one per consumer lane)
 constexpr int kK1Group = 2;             // warps per consumer group
 constexpr int kK1Groups = 8;            // consumer groups (units per item)
 constexpr int kK1MaxSlots = 8;          // ring slots per group
-constexpr int kK1DilateWarps = 3;       // fused launch: warps running K1b tasks (20 warps: 96 regs)
+#ifndef TG_K1_DILATE_WARPS
+#define TG_K1_DILATE_WARPS 0
+#endif
+constexpr int kK1DilateWarps = TG_K1_DILATE_WARPS;  // fused launch: extra warps running K1b tasks
 constexpr int kK1Threads = (kK1Groups * kK1Group + 1 + kK1DilateWarps) * 32;
 constexpr int kK1bBands = 4;            // cell bands per K1b task (a 64-row strip)
 constexpr int kK1SmemBudget = 227 * 1024;
@@ -312,6 +327,9 @@ __device__ void run_dilate_tasks(const MaskArgs& a, int lane) {
     if (lane == 0) t = static_cast<int>(atomicAdd(a.task_next, 1u));
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= a.n_tasks) return;
+#if TG_K1_TASKS_REVERSED
+    t = a.n_tasks - 1 - t;  // last-written strips first: their raw rows may still be in L2
+#endif
     const int wi = t % a.dgroups, sf = t / a.dgroups;
     const int f = sf % a.n_frames, sg = sf / a.n_frames;
     const int cy0 = sg * kK1bBands;
@@ -370,6 +388,9 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
     const int g = lane;
     const bool mine = g < units;
     uint32_t used = 0, fills = 0;  // per ring slot: filled before; fill-count parity
+#if TG_K1_L2HINTS
+    const uint64_t pol_stream = l2_evict_first();
+#endif
     int k = 0;                     // ring slot of the next stage
     for (int item = blockIdx.x; item < a.total_items; item += gridDim.x) {
       const ItemK1 it = load_item(a, item);
@@ -389,7 +410,15 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
             int out;
             const uint8_t* src = ch.next(a, &out) + off;
             mbar_arrive_expect_tx(&full[slot], bytes);
-            bulk_g2s(slots + static_cast<size_t>(slot) * a.slot_bytes, src, bytes, &full[slot]);
+#if TG_K1_L2HINTS
+            // frames stream through once: keep L2 for the raw bitmap the K1b
+            // tasks read back
+            if (fused)
+              bulk_g2s_hint(slots + static_cast<size_t>(slot) * a.slot_bytes, src, bytes,
+                            &full[slot], pol_stream);
+            else
+#endif
+              bulk_g2s(slots + static_cast<size_t>(slot) * a.slot_bytes, src, bytes, &full[slot]);
             used |= bit;
             fills ^= bit;
             if (++k == S) k = 0;
@@ -412,6 +441,9 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
   const int col = (warp - g * kK1Group) * 32 + lane;  // word within the part
   const bool in_slot = 96 * (col + 1) <= a.slot_bytes;  // lane's bytes inside a slot
   uint32_t fpar = 0;  // bit k: parity of the next full phase of ring slot k
+#if TG_K1_L2HINTS
+  const uint64_t pol_keep = l2_evict_last();  // raw words: read back by K1b soon
+#endif
   int k = 0;
   for (int item = blockIdx.x; g < units && item < a.total_items; item += gridDim.x) {
     const ItemK1 it = load_item(a, item);
@@ -436,7 +468,16 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
       if (f >= 0) {
         uint32_t fw = fg_word<kLow>(C, P, t1);
         if (w == a.nwords - 1) fw &= lastmask;
+#if TG_K1_L2HINTS
+        if (valid) {
+          if (fused)
+            st_hint(out + static_cast<size_t>(f) * fstride, fw, pol_keep);
+          else
+            out[static_cast<size_t>(f) * fstride] = fw;
+        }
+#else
         if (valid) out[static_cast<size_t>(f) * fstride] = fw;
+#endif
       }
 #pragma unroll
       for (int q = 0; q < 6; ++q) P[q] = C[q];
