@@ -195,28 +195,23 @@ __device__ int ccl_frame(const uint32_t* gact, const uint32_t* gcells, int cx_n,
     }
   }
   __syncthreads();
-  // roots
+  // roots, and every head's label compressed to its root in the same pass:
+  // the unions are over, so a stored root is final and concurrent finds
+  // through this slot just arrive sooner
   for (int i = tid; i < ncw; i += nt) {
     const int cy = i / aw, wi = i - cy * aw;
     const int nh = __popc(run_heads(s.act + cy * aw, wi));
     uint32_t roots = 0;
     for (int k = 0; k < nh; ++k) {
       const int sl = i * kHeadsPerWord + k;
-      if (uf_find_ro(s.L, sl) == sl) roots |= 1u << k;
+      const int r = uf_find_ro(s.L, sl);
+      if (r == sl) roots |= 1u << k;
+      else s.L[sl] = static_cast<uint16_t>(r);
     }
     s.rootm[i] = roots;
     s.wpre[i] = __popc(roots);
   }
   __syncthreads();
-  // compress every head's label to its root
-  for (int i = tid; i < ncw; i += nt) {
-    const int cy = i / aw, wi = i - cy * aw;
-    const int nh = __popc(run_heads(s.act + cy * aw, wi));
-    for (int k = 0; k < nh; ++k) {
-      const int sl = i * kHeadsPerWord + k;
-      s.L[sl] = static_cast<uint16_t>(uf_find_ro(s.L, sl));
-    }
-  }
   const int ncomp = block_exclusive_scan(s.wpre, ncw, warp_tmp);
   if (tid == 0) {
     s.wpre[ncw] = ncomp;
@@ -236,47 +231,58 @@ __device__ int ccl_frame(const uint32_t* gact, const uint32_t* gcells, int cx_n,
     s.by1[r] = INT_MIN;
   }
   __syncthreads();
-  // every run folds its pixel extent into its component's box
-  for (int i = tid; i < ncw; i += nt) {
-    const int cy = i / aw, wi = i - cy * aw;
-    const uint32_t* row = s.act + cy * aw;
-    uint32_t h = run_heads(row, wi);
-    for (int k = 0; h; ++k) {
-      const int b = __ffs(h) - 1;
-      h &= h - 1;
-      const int a0 = (wi << 5) + b;
-      const int e = run_end(row, a0, aw);
-      const int root = s.L[i * kHeadsPerWord + k];
-      const int rw = root / kHeadsPerWord, ro = root - rw * kHeadsPerWord;
-      const int rank = s.wpre[rw] + __popc(s.rootm[rw] & ((1u << ro) - 1u));
-      if (rank >= nr) continue;
-      const uint32_t* crow = gcells + static_cast<size_t>(cy) * cx_n;
-      const uint32_t va = __ldg(crow + a0), ve = __ldg(crow + e);
-      // y extent over the run's cell summaries (global, L2): eight loads in
-      // flight per step -- a run can span a whole cell row, and one thread's
-      // serial load chain would gate the CTA at the next barrier
-      int y0 = INT_MAX, y1 = INT_MIN;
-      int cx = a0;
-      for (; cx + 8 <= e + 1; cx += 8) {
-        uint32_t v[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) v[t] = __ldg(crow + cx + t);
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          y0 = min(y0, static_cast<int>(v[t] >> 17 & 15u));
-          y1 = max(y1, static_cast<int>(v[t] >> 21 & 15u));
+  // Boxes.  x: every run's end cells.  y: only the component's top cell row
+  // (its root's row) can hold the box's top pixel and only its bottom row the
+  // bottom one, so just those runs scan their cells' y extents.  Pass 1 also
+  // raises by1 to 16 * (bottom cell row); pass 2 keeps it in [16 * row,
+  // 16 * row + 15], so by1 >> 4 names the bottom row throughout.
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int i = tid; i < ncw; i += nt) {
+      const int cy = i / aw, wi = i - cy * aw;
+      const uint32_t* row = s.act + cy * aw;
+      uint32_t h = run_heads(row, wi);
+      for (int k = 0; h; ++k) {
+        const int b = __ffs(h) - 1;
+        h &= h - 1;
+        const int a0 = (wi << 5) + b;
+        const int e = run_end(row, a0, aw);
+        const int root = s.L[i * kHeadsPerWord + k];
+        const int rw = root / kHeadsPerWord, ro = root - rw * kHeadsPerWord;
+        const int rank = s.wpre[rw] + __popc(s.rootm[rw] & ((1u << ro) - 1u));
+        if (rank >= nr) continue;
+        const uint32_t* crow = gcells + static_cast<size_t>(cy) * cx_n;
+        if (pass == 0) {
+          const uint32_t va = __ldg(crow + a0), ve = __ldg(crow + e);
+          atomicMin(&s.bx0[rank], a0 * kCell + static_cast<int>(va >> 9 & 15u));
+          atomicMax(&s.bx1[rank], e * kCell + static_cast<int>(ve >> 13 & 15u));
+          atomicMax(&s.by1[rank], cy * kCell);
+          continue;
         }
+        const bool top = rw / aw == cy, bottom = (s.by1[rank] >> 4) == cy;
+        if (!top && !bottom) continue;
+        // y extent over the run's cell summaries: eight loads in flight per step
+        int y0 = INT_MAX, y1 = INT_MIN;
+        int cx = a0;
+        for (; cx + 8 <= e + 1; cx += 8) {
+          uint32_t v[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) v[t] = __ldg(crow + cx + t);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            y0 = min(y0, static_cast<int>(v[t] >> 17 & 15u));
+            y1 = max(y1, static_cast<int>(v[t] >> 21 & 15u));
+          }
+        }
+        for (; cx <= e; ++cx) {
+          const uint32_t v = __ldg(crow + cx);
+          y0 = min(y0, static_cast<int>(v >> 17 & 15u));
+          y1 = max(y1, static_cast<int>(v >> 21 & 15u));
+        }
+        if (top) atomicMin(&s.by0[rank], cy * kCell + y0);
+        if (bottom) atomicMax(&s.by1[rank], cy * kCell + y1);
       }
-      for (; cx <= e; ++cx) {
-        const uint32_t v = __ldg(crow + cx);
-        y0 = min(y0, static_cast<int>(v >> 17 & 15u));
-        y1 = max(y1, static_cast<int>(v >> 21 & 15u));
-      }
-      atomicMin(&s.bx0[rank], a0 * kCell + static_cast<int>(va >> 9 & 15u));
-      atomicMax(&s.bx1[rank], e * kCell + static_cast<int>(ve >> 13 & 15u));
-      atomicMin(&s.by0[rank], cy * kCell + y0);
-      atomicMax(&s.by1[rank], cy * kCell + y1);
     }
+    __syncthreads();
   }
   __syncthreads();
   return nr;
