@@ -65,3 +65,48 @@ def test_multicam_events_and_canvases_match_reference(ctx, cams, W, H, n, bw, li
             k += 1
     assert k == n_canvases
     path.close()
+
+
+def test_pipelined_passes_match_a_single_step(ctx):
+    """run_pipelined (host batcher of pass i beside the planes of pass i+1,
+    K5 on its own stream) leaves the same events and canvases as step()."""
+    cams = [0, 1, 2, 3]
+    path = MC.MultiCameraPath(ctx, cams, 1920, 1080, 8, PROFILE, bandwidth_mbps=40.0,
+                              trace_kw=dict(roi_proportion_mean=0.15))
+    _, n_events, n_canv = path.step()
+    ctx.stream_sync(path.stream)
+    want_ev = [(e.fire_time_us, e.trigger, e.batch_size, e.patch_ids) for e in path.events()]
+    want = path.canvases(n_canv)
+    got_n = path.run_pipelined(3)
+    ctx.stream_sync(path.stream)
+    assert got_n == n_canv
+    assert [(e.fire_time_us, e.trigger, e.batch_size, e.patch_ids) for e in path.events()] == want_ev
+    assert np.array_equal(path.canvases(n_canv), want)
+    path.close()
+
+
+def test_event_subsets_partition_the_canvases(ctx):
+    """tg_batcher_gather_events(first, stride) writes exactly the canvases of
+    events first, first+stride, ... in event order."""
+    import ctypes as C
+
+    from paper_2404_09267_b200 import _native as N
+    path = MC.MultiCameraPath(ctx, [0, 1, 2], 1920, 1080, 10, PROFILE, bandwidth_mbps=40.0,
+                              trace_kw=dict(roi_proportion_mean=0.2))
+    _, n_events, n_canv = path.step()
+    ctx.stream_sync(path.stream)
+    every = path.canvases(n_canv)
+    sizes = [e.batch_size for e in path.events()]
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    for stride in (2, 3):
+        for first in range(stride):
+            n = C.c_int64()
+            A.check(N.lib().tg_batcher_gather_events(ctx.handle, path.sched.handle, first, stride,
+                                                     path.d_frames, 3 * path.W, path.d_canvases,
+                                                     path.canvas_cap, C.byref(n), path.stream))
+            ctx.stream_sync(path.stream)
+            want = [every[offs[e]:offs[e + 1]] for e in range(first, len(sizes), stride)]
+            want = np.concatenate(want) if want else np.zeros((0,) + every.shape[1:], np.uint8)
+            assert n.value == len(want)
+            assert np.array_equal(path.canvases(n.value), want)
+    path.close()

@@ -449,3 +449,24 @@ def test_cpp_dropin_binary():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "ALL PASS" in out.stdout
+
+
+def test_gather_repeats_and_rewrites_every_byte(ctx):
+    """K5 claims units from a device counter that its last CTA resets: a
+    second gather after one plan (no scan in between) must rewrite every
+    canvas byte identically, including over garbage."""
+    from paper_2404_09267_b200 import _native as N
+    run = GpuRun(ctx, 1920, 1080, 12, seed=1004, trace_kw=dict(roi_proportion_mean=0.2))
+    run.run()
+    first = run.canvases()
+    total = run.res["total_canvases"]
+    assert total > 0
+    for _ in range(3):
+        run.ctx.memset(run.d_canvases, 0x5A, run.canvas_bytes * total)
+        A.check(N.lib().tg_pipeline_stage_gather(run.pipe.handle, run.n, run.d_cur,
+                                                 run.d_canvases, None))
+        run.ctx.stream_sync()
+        assert np.array_equal(run.canvases(), first)
+    orc = run.oracle()
+    assert np.array_equal(first, orc["canvases"][:total])
+    run.close()
