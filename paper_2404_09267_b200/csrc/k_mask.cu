@@ -41,7 +41,8 @@
 // 1.29 / 1.31 / 1.46 ms vs 1.27 ms without (TG_K1_DILATE_WARPS) -- the task
 // warps slow the stream more than they hide; L2 evict_first on the frame
 // stream + evict_last on the raw words (TG_K1_L2HINTS) cut DRAM reads by
-// 0.14 GB but not time (1.28 ms).
+// 0.14 GB but not time (1.28 ms); consumer warps taking up to 1/2/4/8 ready
+// tasks between their items (never waiting) 1.30/1.33/1.37/1.49 ms.
 #include <algorithm>
 #include <cstdlib>
 
@@ -51,9 +52,6 @@ namespace tg {
 
 #ifndef TG_K1_L2HINTS
 #define TG_K1_L2HINTS 0
-#endif
-#ifndef TG_K1_TASKS_REVERSED
-#define TG_K1_TASKS_REVERSED 0
 #endif
 
 constexpr int kK1MaxPartWords = 64;     // 32-pixel words per unit (one per consumer lane)
@@ -321,40 +319,49 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 
 // Fused launch: K1b tasks (strip, frame, column group) in strip order, each
 // after the K1 items that write its rows have published completion.
+// Waits until the K1 items writing the rows of task t have published.
+__device__ __forceinline__ void wait_dilate_task(const MaskArgs& a, int t, int lane) {
+  const int sf = t / a.dgroups;
+  const int f = sf % a.n_frames, sg = sf / a.n_frames;
+  const int cy0 = sg * kK1bBands;
+  const int y_lo = max(0, cy0 * kCell - a.radius);
+  const int y_hi = min(a.H, (cy0 + kK1bBands) * kCell + a.radius) - 1;
+  const int run = f / a.kf;
+  for (int rb = y_lo / a.rows_per_item + lane; rb <= y_hi / a.rows_per_item; rb += 32) {
+    const int rows = min(a.rows_per_item, a.H - rb * a.rows_per_item);
+    const uint32_t want = static_cast<uint32_t>(kK1Group * a.nparts * rows);
+    const uint32_t* flag = a.item_done + rb * a.ntg + run;
+    while (ld_acquire(flag) < want) __nanosleep(256);
+  }
+}
+
+__device__ __forceinline__ void run_dilate_task(const MaskArgs& a, int t, int lane) {
+  __syncwarp();
+  __threadfence();
+  const int wi = t % a.dgroups, sf = t / a.dgroups;
+  const int f = sf % a.n_frames, cy0 = sf / a.n_frames * kK1bBands;
+  switch (a.radius) {
+#define TG_DILATE_TASK(R) \
+  case R:                 \
+    dilate_strip<R, true>(a.d, f, cy0, wi, lane, nullptr); \
+    break;
+    TG_DILATE_TASK(0) TG_DILATE_TASK(1) TG_DILATE_TASK(2) TG_DILATE_TASK(3) TG_DILATE_TASK(4)
+    TG_DILATE_TASK(5) TG_DILATE_TASK(6) TG_DILATE_TASK(7) TG_DILATE_TASK(8)
+#undef TG_DILATE_TASK
+    default:
+      break;
+  }
+}
+
+// Drains the queue, waiting for each claimed task's items.
 __device__ void run_dilate_tasks(const MaskArgs& a, int lane) {
   for (;;) {
     int t = 0;
     if (lane == 0) t = static_cast<int>(atomicAdd(a.task_next, 1u));
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= a.n_tasks) return;
-#if TG_K1_TASKS_REVERSED
-    t = a.n_tasks - 1 - t;  // last-written strips first: their raw rows may still be in L2
-#endif
-    const int wi = t % a.dgroups, sf = t / a.dgroups;
-    const int f = sf % a.n_frames, sg = sf / a.n_frames;
-    const int cy0 = sg * kK1bBands;
-    const int y_lo = max(0, cy0 * kCell - a.radius);
-    const int y_hi = min(a.H, (cy0 + kK1bBands) * kCell + a.radius) - 1;
-    const int run = f / a.kf;
-    for (int rb = y_lo / a.rows_per_item + lane; rb <= y_hi / a.rows_per_item; rb += 32) {
-      const int rows = min(a.rows_per_item, a.H - rb * a.rows_per_item);
-      const uint32_t want = static_cast<uint32_t>(kK1Group * a.nparts * rows);
-      const uint32_t* flag = a.item_done + rb * a.ntg + run;
-      while (ld_acquire(flag) < want) __nanosleep(256);
-    }
-    __syncwarp();
-    __threadfence();
-    switch (a.radius) {
-#define TG_DILATE_TASK(R) \
-  case R:                 \
-    dilate_strip<R, true>(a.d, f, cy0, wi, lane, nullptr); \
-    break;
-      TG_DILATE_TASK(0) TG_DILATE_TASK(1) TG_DILATE_TASK(2) TG_DILATE_TASK(3) TG_DILATE_TASK(4)
-      TG_DILATE_TASK(5) TG_DILATE_TASK(6) TG_DILATE_TASK(7) TG_DILATE_TASK(8)
-#undef TG_DILATE_TASK
-      default:
-        break;
-    }
+    wait_dilate_task(a, t, lane);
+    run_dilate_task(a, t, lane);
   }
 }
 
