@@ -9,10 +9,17 @@
   (tools/tangram_main.cpp:225-248).
 * ``efficiency_summary`` -- mean / median canvas efficiency as the
   simulator's summary computes them (sim.hpp:540-550).
+* ``scene_from_rois`` -- the RoIs the device extracted from pixels as a
+  reference trace scene, so ``save_trace`` hands them to the reference's
+  own tools (``tangram simulate --trace``).
+* ``dump_canvases`` -- raw canvas dumps (HWC uint8) with a SHA-256 manifest
+  for cross-checking canvases between runs and builds.
 """
 from __future__ import annotations
 
+import hashlib
 import json
+import os
 from dataclasses import dataclass, field
 from typing import Iterable, TextIO
 
@@ -133,3 +140,57 @@ def efficiency_summary(stitches: Iterable[StitchResult]) -> dict:
     median = effs[mid] if len(effs) % 2 == 1 else 0.5 * (effs[mid - 1] + effs[mid])
     return {"canvases": len(effs), "mean_canvas_efficiency": total / len(effs),
             "median_canvas_efficiency": median}
+
+
+def scene_from_rois(scene_id: str, t_us, rois_per_frame, width: int, height: int,
+                    first_frame: int = 0) -> TraceScene:
+    """A trace scene (trace.hpp:39-50) of extracted RoIs: frame i has time
+    t_us[i] and the (x, y, w, h) boxes rois_per_frame[i]; validated like a
+    loaded trace."""
+    frames = [TraceFrame(first_frame + i, int(t), int(width), int(height),
+                         [r if isinstance(r, Rect) else Rect(*[int(v) for v in r]) for r in rois])
+              for i, (t, rois) in enumerate(zip(t_us, rois_per_frame))]
+    sc = TraceScene(str(scene_id), frames)
+    validate_scene(sc)
+    return sc
+
+
+def canvas_sha256(canvas) -> str:
+    """SHA-256 of a canvas's bytes (row-major HWC uint8, rows unpadded)."""
+    import numpy as np
+    return hashlib.sha256(np.ascontiguousarray(canvas, dtype=np.uint8).tobytes()).hexdigest()
+
+
+def dump_canvases(directory: str, canvases, prefix: str = "canvas") -> dict:
+    """Writes canvases[k] (N x 3M uint8 or N x M x 3) as <prefix>_<k>.rgb raw
+    files plus manifest.json {"canvases": [{"index", "file", "width",
+    "height", "sha256"}]}; returns the manifest."""
+    import numpy as np
+    os.makedirs(directory, exist_ok=True)
+    entries = []
+    for k, c in enumerate(canvases):
+        c = np.ascontiguousarray(c, dtype=np.uint8)
+        h = c.shape[0]
+        w = c.shape[1] if c.ndim == 3 else c.shape[1] // 3
+        name = f"{prefix}_{k:06d}.rgb"
+        with open(os.path.join(directory, name), "wb") as f:
+            f.write(c.tobytes())
+        entries.append({"index": k, "file": name, "width": int(w), "height": int(h),
+                        "sha256": canvas_sha256(c)})
+    manifest = {"format": "rgb8 HWC, rows unpadded", "canvases": entries}
+    with open(os.path.join(directory, "manifest.json"), "w") as f:
+        json.dump(manifest, f, indent=2, sort_keys=True)
+        f.write("\n")
+    return manifest
+
+
+def verify_canvas_dump(directory: str) -> list[int]:
+    """Indices of dumped canvases whose bytes no longer match the manifest."""
+    with open(os.path.join(directory, "manifest.json")) as f:
+        manifest = json.load(f)
+    bad = []
+    for e in manifest["canvases"]:
+        with open(os.path.join(directory, e["file"]), "rb") as f:
+            if hashlib.sha256(f.read()).hexdigest() != e["sha256"]:
+                bad.append(e["index"])
+    return bad

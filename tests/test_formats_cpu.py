@@ -69,3 +69,36 @@ def test_efficiency_summary_matches_reference_simulator():
     s = Fm.efficiency_summary(e.stitch for e in events)
     assert s["mean_canvas_efficiency"] == ref["mean_canvas_efficiency"]
     assert s["median_canvas_efficiency"] == ref["median_canvas_efficiency"]
+
+
+@need_ref
+def test_extracted_rois_export_as_reference_trace():
+    """scene_from_rois + save_trace: byte-identical to the reference's own
+    save_trace on the same RoIs, and loadable back."""
+    W, H = 1920, 1080
+    raw = scenes_for(2, 12, W, H)
+    scenes = [Fm.scene_from_rois(f"cam{s}", t_us, frames, W, H) for s, (t_us, frames) in
+              enumerate(raw)]
+    buf = io.StringIO()
+    Fm.save_trace(buf, scenes)
+    assert buf.getvalue() == O.save_trace_ref(raw, W, H)
+    back = Fm.load_trace(io.StringIO(buf.getvalue()))
+    assert [[f.rois for f in s.frames] for s in back] == [[f.rois for f in s.frames] for s in scenes]
+    with pytest.raises(A.InvalidArgument, match="roi outside frame"):
+        Fm.scene_from_rois("x", [0], [[(1900, 0, 40, 10)]], W, H)
+
+
+def test_canvas_dump_manifest(tmp_path):
+    import hashlib
+
+    import numpy as np
+    rng = np.random.default_rng(3)
+    canv = rng.integers(0, 256, (3, 64, 96 * 3), dtype=np.uint8)
+    man = Fm.dump_canvases(str(tmp_path), canv)
+    assert [e["sha256"] for e in man["canvases"]] == \
+        [hashlib.sha256(c.tobytes()).hexdigest() for c in canv]
+    assert man["canvases"][0]["width"] == 96 and man["canvases"][0]["height"] == 64
+    assert Fm.verify_canvas_dump(str(tmp_path)) == []
+    with open(tmp_path / man["canvases"][1]["file"], "r+b") as f:
+        f.write(b"\x00\x01")
+    assert Fm.verify_canvas_dump(str(tmp_path)) == [1]
