@@ -256,7 +256,7 @@ def run_ours(args):
                  "admitted": int(res["admitted"].sum()), "canvases": ncanv,
                  "canvas_efficiency_mean": round(adm_bytes / max(1, ncanv * pipe.canvas_bytes), 4)},
         "clocks": clk,
-        "gpu_launches": 4 * K,
+        "gpu_launches": 3 * K,  # K1 (+K1b), plan (+scan), gather
     }
 
     if not args.no_e2e:
@@ -517,7 +517,7 @@ def run_multicam(args):
                                  "K5 on its own stream; timed region = K whole passes"},
         "batching": {"events": n_events, ("canvases_rank0" if glob else "canvases"): n_canv,
                      "patches_admitted": int(len(path._last["patches"]))},
-        "clocks": clk, "gpu_launches": 4 * args.steps,  # K1, plan, scan, gather
+        "clocks": clk, "gpu_launches": 3 * args.steps,  # K1 (+K1b), plan (+scan), gather
     }
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -594,7 +594,7 @@ def run_density(args):
     peak, _ = peaks()
     out = {"metric": METRIC, "value": lines[2]["frames_per_s"], "unit": "frames/s", "n_gpus": 1,
            "steps": args.steps, "warmup": 3, "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "u8", "data": "synthetic", "gpu_launches_per_step": 4,
+           "vs_baseline": None, "dtype": "u8", "data": "synthetic", "gpu_launches_per_step": 3,
            "config": {"workload": "BASELINE configs[4]: RoI-density sweep, 8 synthetic 4K cameras, "
                                   f"{n} frames each, roi_max_dim 1024", "peak_GBps": peak},
            "sweep": lines}

@@ -82,6 +82,8 @@ struct tg_pipeline {
   uint2* ranges = nullptr;
   int32_t* gather_units = nullptr;
   uint64_t* id_state = nullptr;
+  uint64_t* look = nullptr;   // [F] plan look-back words
+  uint32_t* psync = nullptr;  // [3] plan frame ticket, finished CTAs, epoch
   int last_frames = 0;
 };
 
@@ -658,7 +660,7 @@ void tg_pipeline_destroy(tg_pipeline* p) {
   void* bufs[] = {p->raw, p->mask_sync, p->cells, p->active, p->mask, p->n_rois, p->n_patches, p->n_placements,
                   p->n_canvases, p->rois, p->patches, p->admitted, p->placements,
                   p->canvas_base, p->jobs, p->canvas_jobs, p->ranges, p->gather_units,
-                  p->id_state};
+                  p->id_state, p->look, p->psync};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete p;
@@ -690,6 +692,9 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
     return fail(TG_ERR_INVALID_ARGUMENT, "frame has more than 65535 %dx%d cells", kCell, kCell);
   if (plan_smem_bytes(cx, cy, q.max_rois_per_frame) > 200 * 1024)
     return fail(TG_ERR_INVALID_ARGUMENT, "max_rois_per_frame too large for this frame size");
+  // patch and canvas prefixes travel in 23-bit look-back fields
+  if (static_cast<long long>(q.max_frames) * q.partition.zones_x * q.partition.zones_y >= (1 << 23))
+    return fail(TG_ERR_INVALID_ARGUMENT, "max_frames x zones must be below 2^23");
   tg_pipeline* p = new tg_pipeline();
   p->ctx = ctx;
   p->p = q;
@@ -724,7 +729,11 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
   if (!e) e = alloc(&p->ranges, static_cast<size_t>(q.max_canvases));
   if (!e) e = alloc(&p->gather_units, 3);
   if (!e) e = alloc(&p->id_state, 1);
+  if (!e) e = alloc(&p->look, F);
+  if (!e) e = alloc(&p->psync, 3);
   if (!e) e = cudaMemset(p->id_state, 0, sizeof(uint64_t));
+  if (!e) e = cudaMemset(p->look, 0, F * sizeof(uint64_t));
+  if (!e) e = cudaMemset(p->psync, 0, 3 * sizeof(uint32_t));
   if (!e) e = cudaMemset(p->gather_units, 0, 3 * sizeof(int32_t));
   if (e) {
     tg_pipeline_destroy(p);
@@ -822,26 +831,16 @@ tg_status tg_pipeline_stage_plan(tg_pipeline* p, int32_t n_frames, const uint64_
   a.jobs = p->jobs;
   a.canvas_jobs = p->canvas_jobs;
   a.err = p->ctx->d_err;
+  a.first_id = first_patch_id;
+  a.max_canvases = p->p.max_canvases;
+  a.nbands = p->nbands;
+  a.canvas_base = p->canvas_base;
+  a.ranges = p->ranges;
+  a.gather_units = p->gather_units;
+  a.id_state = p->id_state;
+  a.look = p->look;
+  a.psync = p->psync;
   TG_CUDA(launch_plan(a, st));
-  ScanArgs sa;
-  sa.n_frames = n_frames;
-  sa.zones = p->zones;
-  sa.job_cap = p->job_cap;
-  sa.canvas_jobs = p->canvas_jobs;
-  sa.first_id = first_patch_id;
-  sa.max_canvases = p->p.max_canvases;
-  sa.nbands = p->nbands;
-  sa.n_patches = p->n_patches;
-  sa.n_placements = p->n_placements;
-  sa.n_canvases = p->n_canvases;
-  sa.patches = p->patches;
-  sa.placements = p->placements;
-  sa.canvas_base = p->canvas_base;
-  sa.ranges = p->ranges;
-  sa.gather_units = p->gather_units;
-  sa.id_state = p->id_state;
-  sa.err = p->ctx->d_err;
-  TG_CUDA(launch_scan(sa, st));
   p->last_frames = n_frames;
   return TG_OK;
 }

@@ -5,7 +5,7 @@
 // free rects: each canvas row is a left-to-right
 // sequence of intervals, each either a patch's source row or zeros.  A
 // persistent grid claims (canvas, 64-row band) units from a device counter
-// -- their count is what the scan kernel left in device memory (no host
+// -- their count is what the planner left in device memory (no host
 // round trip between planning and gathering); dynamic claiming keeps CTAs
 // that drew light, zero-fill bands busy, so the grid drains together (static
 // round robin: 0.82 ms vs 0.66 ms per 300 4K frames).  Warp w of a block

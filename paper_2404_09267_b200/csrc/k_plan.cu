@@ -8,9 +8,14 @@
 //   K3 partition() (partition.hpp:119-143) and admission (sim.hpp:262);
 //   K4 stitch_all() (stitch.hpp:108-146) on the frame's admitted patches
 //      (sim.hpp:302-332), one warp;
-// then the gather jobs: every placement plus every final free rect, which
-// tile each canvas exactly, grouped by canvas and sorted
-// by x so the gather can walk canvas rows left to right.
+// then the frame-order prefix of patch and canvas counts (global patch ids,
+// sim.hpp:249-251, and canvas numbering) by decoupled look-back between the
+// frames' CTAs -- frames are taken from a ticket counter, so every
+// predecessor of a frame is already running -- and the gather jobs: every
+// placement plus every final free rect, which tile each canvas exactly
+// (SURVEY Appendix P5), grouped by canvas and sorted by x so the gather can
+// walk canvas rows left to right.  The CTA of the last frame leaves the
+// totals (canvas count, K5 units, next patch id) in device memory.
 #include <algorithm>
 
 #include "ccl.cuh"
@@ -35,6 +40,85 @@ __device__ __forceinline__ void sort_jobs_by_x(const Job* tmp, int n, Job* out, 
   }
 }
 
+
+// ---- look-back words: epoch(16) | flag(2) | patches(23) | canvases(23) -----
+// flag 1: this frame's own counts, 2: inclusive prefix through this frame.
+// A word from an earlier launch carries another epoch and reads as absent.
+constexpr uint32_t kLookAgg = 1, kLookIncl = 2;
+constexpr uint64_t kLookMask = (1ull << 23) - 1;
+
+__device__ __forceinline__ uint64_t look_pack(uint32_t epoch, uint32_t flag, uint64_t p, uint64_t c) {
+  return static_cast<uint64_t>(epoch & 0xffffu) << 48 | static_cast<uint64_t>(flag) << 46 |
+         (p & kLookMask) << 23 | (c & kLookMask);
+}
+
+__device__ __forceinline__ void st_release64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_acquire64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ld_volatile32(const uint32_t* p) {
+  return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+// Warp 0 of frame f's CTA: publishes (np, nc), returns the exclusive prefix
+// over frames 0..f-1 and publishes the inclusive one.
+__device__ void look_back(const PlanArgs& a, int f, uint32_t epoch, uint64_t np, uint64_t nc,
+                          uint64_t* ex_p, uint64_t* ex_c, int lane) {
+  if (lane == 0) st_release64(&a.look[f], look_pack(epoch, f == 0 ? kLookIncl : kLookAgg, np, nc));
+  uint64_t sp = 0, sc = 0;
+  for (int j = f - 1; j >= 0; j -= 32) {
+    const int idx = j - lane;
+    uint64_t v = 0;
+    uint32_t flag = 0;
+    if (idx >= 0) {
+      for (;;) {
+        v = ld_acquire64(&a.look[idx]);
+        flag = static_cast<uint32_t>(v >> 46) & 3u;
+        if ((v >> 48) == (epoch & 0xffffu) && flag != 0) break;
+        __nanosleep(64);
+      }
+    }
+    const unsigned incl = __ballot_sync(0xffffffffu, flag == kLookIncl);
+    const int stop = incl ? __ffs(incl) - 1 : 31;  // nearest predecessor with a prefix
+    uint64_t vp = (idx >= 0 && lane <= stop) ? (v >> 23) & kLookMask : 0;
+    uint64_t vc = (idx >= 0 && lane <= stop) ? v & kLookMask : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      vp += __shfl_xor_sync(0xffffffffu, vp, o);
+      vc += __shfl_xor_sync(0xffffffffu, vc, o);
+    }
+    sp += vp;
+    sc += vc;
+    if (incl) break;
+  }
+  if (lane == 0 && f > 0) st_release64(&a.look[f], look_pack(epoch, kLookIncl, sp + np, sc + nc));
+  *ex_p = sp;
+  *ex_c = sc;
+}
+
+// Totals of the run, by the CTA that saw the inclusive prefix of the last frame.
+__device__ void plan_totals(const PlanArgs& a, uint64_t first_id, uint64_t total_p,
+                            long long total_c) {
+  *a.id_state = first_id + total_p;
+  a.canvas_base[a.n_frames] = total_c;
+  long long total = total_c;
+  if (a.max_canvases == 0) {
+    total = 0;  // planning only: per-frame canvases are not materialized
+  } else if (total > a.max_canvases) {
+    raise_error(a.err, TG_ERR_CAPACITY, kErrCanvasCapacity, total, a.max_canvases);
+    total = a.max_canvases;
+  }
+  a.gather_units[0] = static_cast<int32_t>(total * a.nbands);
+  a.gather_units[1] = 0;  // K5's claim counters
+  a.gather_units[2] = 0;
+}
+
 // K3/K4 working set; aliases the K2 (CCL) region of dynamic smem once the
 // RoI boxes are out, so three planner CTAs fit on an SM.
 struct PlanTail {
@@ -56,7 +140,24 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   StitchOut* souts = T.souts;
   Job* sjobs = T.sjobs;
 
-  const int f = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  __shared__ int s_f;
+  __shared__ uint32_t s_epoch;
+  __shared__ unsigned long long s_first;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) {
+    s_epoch = ld_volatile32(&a.psync[2]);
+    s_first = a.first_id == ~0ull ? *reinterpret_cast<const volatile uint64_t*>(a.id_state)
+                                   : a.first_id;
+    // frames in ticket order: a frame's predecessors are all running or done,
+    // so its look-back cannot wait on a CTA that is not resident
+    s_f = a.n_frames > 0 ? static_cast<int>(atomicAdd(&a.psync[0], 1u)) : 0;
+  }
+  __syncthreads();
+  if (a.n_frames == 0) {  // nothing planned: zero totals
+    if (tid == 0) plan_totals(a, s_first, 0, 0);
+    return;
+  }
+  const int f = s_f;
   const int cx_n = a.cells_x, cy_n = a.cells_y, aw = a.act_words, ncw = cy_n * aw;
   CclSmem cs;
   cs.act = reinterpret_cast<uint32_t*>(dsm);
@@ -121,125 +222,74 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     a.n_placements[f] = na;
     a.n_canvases[f] = nc < 0 ? 0 : nc;
   }
-  if (nc <= 0) return;
-  tg_placement* fpl = a.placements + static_cast<size_t>(f) * nz;
-  for (int k = lane; k < na; k += 32) {
-    tg_placement p;
-    p.patch_id = static_cast<uint64_t>(adm_idx[k]);  // frame-local; the scan makes it global
-    p.canvas_index = souts[k].canvas;
-    p.position = tg_rect{souts[k].x, souts[k].y, adm_w[k], adm_h[k]};
-    p.reserved = 0;
-    fpl[k] = p;
+  const int ncv = nc < 0 ? 0 : nc;
+  uint64_t ex_p, ex_c;
+  look_back(a, f, s_epoch, static_cast<uint64_t>(np), static_cast<uint64_t>(ncv), &ex_p, &ex_c,
+            lane);
+  const uint64_t id0 = s_first + ex_p;
+  const long long cb = static_cast<long long>(ex_c);
+  for (int j = lane; j < np; j += 32) a.patches[static_cast<size_t>(f) * nz + j].patch_id = id0 + j;
+  if (lane == 0) {
+    a.canvas_base[f] = cb;
+    if (f == a.n_frames - 1) plan_totals(a, s_first, ex_p + np, cb + ncv);
   }
-  // Gather jobs: placements and free rects grouped by canvas, sorted by x.
-  Job* fj = a.jobs + static_cast<size_t>(f) * a.job_cap;
-  uint32_t* fcj = a.canvas_jobs + static_cast<size_t>(f) * nz;
-  const int nitems = na + nfree;
-  int pos = 0;
-  for (int c = 0; c < nc; ++c) {
-    int cnt = 0;
-    for (int ib = 0; ib < nitems; ib += 32) {
-      const int it = ib + lane;
-      bool mine = false;
-      Job jb{};
-      if (it < na) {
-        mine = souts[it].canvas == c;
-        const tg_rect src = spatch[adm_idx[it]].rect;
-        jb = Job{static_cast<uint16_t>(souts[it].x), static_cast<uint16_t>(souts[it].y),
-                 static_cast<uint16_t>(src.w), static_cast<uint16_t>(src.h), f,
-                 static_cast<uint16_t>(src.x), static_cast<uint16_t>(src.y)};
-      } else if (it < nitems) {
-        const FreeRect fr = freel[it - na];
-        mine = fr.canvas == c;
-        jb = Job{static_cast<uint16_t>(fr.x), static_cast<uint16_t>(fr.y),
-                 static_cast<uint16_t>(fr.w), static_cast<uint16_t>(fr.h), -1,
-                 static_cast<uint16_t>(fr.seq & 0xffff), static_cast<uint16_t>(fr.seq >> 16)};
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, mine);
-      if (mine) sjobs[cnt + __popc(m & ((1u << lane) - 1u))] = jb;
-      cnt += __popc(m);
+  if (ncv > 0) {
+    tg_placement* fpl = a.placements + static_cast<size_t>(f) * nz;
+    for (int k = lane; k < na; k += 32) {
+      tg_placement p;
+      p.patch_id = id0 + static_cast<uint64_t>(adm_idx[k]);
+      p.canvas_index = souts[k].canvas;
+      p.position = tg_rect{souts[k].x, souts[k].y, adm_w[k], adm_h[k]};
+      p.reserved = 0;
+      fpl[k] = p;
     }
-    __syncwarp();
-    sort_jobs_by_x(sjobs, cnt, fj + pos, lane);
-    __syncwarp();
-    if (lane == 0) fcj[c] = static_cast<uint32_t>(pos) | static_cast<uint32_t>(cnt) << 16;
-    pos += cnt;
-  }
-}
-
-// ---- frame-order scan: global patch ids and canvas numbering -------------
-__global__ void __launch_bounds__(1024) scan_kernel(const ScanArgs a) {
-  __shared__ long long wtmp_p[32], wtmp_c[32];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nt = blockDim.x;
-  // ~0 = continue numbering where the previous run on this pipeline ended
-  // (streaming chunks without a host round trip).
-  const uint64_t first_id = a.first_id == ~0ull ? *a.id_state : a.first_id;
-  __syncthreads();
-  long long run_p = 0, run_c = 0;
-  for (int base = 0; base < a.n_frames; base += nt) {
-    const int f = base + tid;
-    const long long vp = f < a.n_frames ? a.n_patches[f] : 0;
-    const long long vc = f < a.n_frames ? a.n_canvases[f] : 0;
-    long long sp = vp, sc = vc;
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long yp = __shfl_up_sync(0xffffffffu, sp, o);
-      const long long yc = __shfl_up_sync(0xffffffffu, sc, o);
-      if (lane >= o) {
-        sp += yp;
-        sc += yc;
-      }
-    }
-    if (lane == 31) {
-      wtmp_p[wid] = sp;
-      wtmp_c[wid] = sc;
-    }
-    __syncthreads();
-    if (wid == 0) {
-      long long tp = lane < nt / 32 ? wtmp_p[lane] : 0, tc = lane < nt / 32 ? wtmp_c[lane] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        const long long yp = __shfl_up_sync(0xffffffffu, tp, o);
-        const long long yc = __shfl_up_sync(0xffffffffu, tc, o);
-        if (lane >= o) {
-          tp += yp;
-          tc += yc;
+    // Gather jobs: placements and free rects grouped by canvas, sorted by x.
+    Job* fj = a.jobs + static_cast<size_t>(f) * a.job_cap;
+    uint32_t* fcj = a.canvas_jobs + static_cast<size_t>(f) * nz;
+    const int nitems = na + nfree;
+    int pos = 0;
+    for (int c = 0; c < ncv; ++c) {
+      int cnt = 0;
+      for (int ib = 0; ib < nitems; ib += 32) {
+        const int it = ib + lane;
+        bool mine = false;
+        Job jb{};
+        if (it < na) {
+          mine = souts[it].canvas == c;
+          const tg_rect src = spatch[adm_idx[it]].rect;
+          jb = Job{static_cast<uint16_t>(souts[it].x), static_cast<uint16_t>(souts[it].y),
+                   static_cast<uint16_t>(src.w), static_cast<uint16_t>(src.h), f,
+                   static_cast<uint16_t>(src.x), static_cast<uint16_t>(src.y)};
+        } else if (it < nitems) {
+          const FreeRect fr = freel[it - na];
+          mine = fr.canvas == c;
+          jb = Job{static_cast<uint16_t>(fr.x), static_cast<uint16_t>(fr.y),
+                   static_cast<uint16_t>(fr.w), static_cast<uint16_t>(fr.h), -1,
+                   static_cast<uint16_t>(fr.seq & 0xffff), static_cast<uint16_t>(fr.seq >> 16)};
         }
+        const unsigned m = __ballot_sync(0xffffffffu, mine);
+        if (mine) sjobs[cnt + __popc(m & ((1u << lane) - 1u))] = jb;
+        cnt += __popc(m);
       }
-      wtmp_p[lane] = tp;
-      wtmp_c[lane] = tc;
-    }
-    __syncthreads();
-    const long long pb = run_p + (wid ? wtmp_p[wid - 1] : 0) + sp - vp;
-    const long long cb = run_c + (wid ? wtmp_c[wid - 1] : 0) + sc - vc;
-    if (f < a.n_frames) {
-      const uint64_t id0 = first_id + static_cast<uint64_t>(pb);
-      tg_patch_meta* fp = a.patches + static_cast<size_t>(f) * a.zones;
-      for (int j = 0; j < vp; ++j) fp[j].patch_id = id0 + static_cast<uint64_t>(j);
-      tg_placement* fl = a.placements + static_cast<size_t>(f) * a.zones;
-      for (int k = 0; k < a.n_placements[f]; ++k) fl[k].patch_id = id0 + fl[k].patch_id;
-      a.canvas_base[f] = cb;
-      const uint32_t* fcj = a.canvas_jobs + static_cast<size_t>(f) * a.zones;
-      for (int c = 0; c < vc; ++c)
+      __syncwarp();
+      sort_jobs_by_x(sjobs, cnt, fj + pos, lane);
+      __syncwarp();
+      if (lane == 0) {
+        fcj[c] = static_cast<uint32_t>(pos) | static_cast<uint32_t>(cnt) << 16;
         if (cb + c < a.max_canvases)
-          a.ranges[cb + c] = make_uint2(static_cast<uint32_t>(f) * a.job_cap + (fcj[c] & 0xffffu),
-                                        fcj[c] >> 16);
+          a.ranges[cb + c] = make_uint2(static_cast<uint32_t>(f) * a.job_cap + pos, cnt);
+      }
+      pos += cnt;
     }
-    run_p += wtmp_p[nt / 32 - 1];
-    run_c += wtmp_c[nt / 32 - 1];
-    __syncthreads();
   }
-  if (tid == 0) {
-    *a.id_state = first_id + static_cast<uint64_t>(run_p);
-    a.canvas_base[a.n_frames] = run_c;
-    long long total = run_c;
-    if (a.max_canvases == 0) {
-      total = 0;  // planning only: per-frame canvases are not materialized
-    } else if (total > a.max_canvases) {
-      raise_error(a.err, TG_ERR_CAPACITY, kErrCanvasCapacity, total, a.max_canvases);
-      total = a.max_canvases;
+  if (lane == 0) {  // the last CTA out resets the ticket and moves the epoch on
+    __threadfence();
+    if (atomicAdd(&a.psync[1], 1u) == static_cast<uint32_t>(a.n_frames) - 1) {
+      a.psync[0] = 0;
+      a.psync[1] = 0;
+      a.psync[2] = s_epoch + 1;
+      __threadfence();
     }
-    a.gather_units[0] = static_cast<int32_t>(total * a.nbands);
-    a.gather_units[1] = 0;  // K5's claim counters
-    a.gather_units[2] = 0;
   }
 }
 
@@ -310,19 +360,15 @@ size_t plan_smem_bytes(int cells_x, int cells_y, int max_rois) {
 }
 
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
-  if (a.n_frames <= 0) return cudaSuccess;
+  if (a.n_frames < 0) return cudaErrorInvalidValue;
   const size_t smem = plan_smem_bytes(a.cells_x, a.cells_y, a.max_rois);
   cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  plan_kernel<<<a.n_frames, kPlanThreads, smem, stream>>>(a);
+  plan_kernel<<<a.n_frames > 0 ? a.n_frames : 1, kPlanThreads, smem, stream>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream) {
-  scan_kernel<<<1, 1024, 0, stream>>>(a);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_partition_batch(const PartitionBatchArgs& a, cudaStream_t stream) {
   if (a.n_frames <= 0) return cudaSuccess;

@@ -40,24 +40,17 @@ struct PlanArgs {
   int32_t* n_canvases;
   Job* jobs;
   uint32_t* canvas_jobs;  // [F][Z] start | count << 16
-  DevError* err;
-};
-
-struct ScanArgs {
-  int n_frames, zones, job_cap;
-  uint64_t first_id;
+  // frame-order prefix (global patch ids, canvas numbering), by decoupled
+  // look-back between the frames' CTAs
+  uint64_t first_id;      // ~0: continue from *id_state
   int64_t max_canvases;
   int nbands;
-  const int32_t* n_patches;
-  const int32_t* n_placements;
-  const int32_t* n_canvases;
-  const uint32_t* canvas_jobs;  // [F][Z] local start | count << 16 (from the planner)
-  tg_patch_meta* patches;
-  tg_placement* placements;
-  int64_t* canvas_base;
+  int64_t* canvas_base;   // [F + 1]
   uint2* ranges;          // [max_canvases] (first job, job count) in the flat job array
-  int32_t* gather_units;  // out: min(total, cap) * nbands
-  uint64_t* id_state;     // next patch id after this run; read when first_id == ~0
+  int32_t* gather_units;  // out: [0] min(total, cap) * nbands; [1], [2] K5 counters := 0
+  uint64_t* id_state;     // next patch id after this run
+  uint64_t* look;         // [F] look-back words: epoch | flag | patches | canvases
+  uint32_t* psync;        // [3] frame ticket, finished CTAs, epoch
   DevError* err;
 };
 
@@ -89,7 +82,6 @@ struct StitchBatchArgs {
 
 size_t plan_smem_bytes(int cells_x, int cells_y, int max_rois);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
-cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream);
 cudaError_t launch_partition_batch(const PartitionBatchArgs& a, cudaStream_t stream);
 cudaError_t launch_stitch_batch(const StitchBatchArgs& a, cudaStream_t stream);
 
