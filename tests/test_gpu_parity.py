@@ -177,12 +177,13 @@ def test_synth_matches_oracle(ctx):
 
 def _compare_full(run, gpu, orc, check_canvases=True):
     n = run.n
-    # masks + cells
-    gm = run.pipe.mask(n)
-    frames = run.host_frames()
-    for i in range(n):
-        om = O.mask(frames[i + 1], frames[i], run.W, run.H, run.threshold, run.radius)
-        assert np.array_equal(gm[i], om), f"mask frame {i}"
+    # masks (when kept: the fused K1b then also writes the dilated mask) + cells
+    if run.pipe.params.keep_mask:
+        gm = run.pipe.mask(n)
+        frames = run.host_frames()
+        for i in range(n):
+            om = O.mask(frames[i + 1], frames[i], run.W, run.H, run.threshold, run.radius)
+            assert np.array_equal(gm[i], om), f"mask frame {i}"
     assert np.array_equal(run.pipe.cells(n), orc["cells"]), "cells"
     # RoIs in raster order of their first cell
     assert np.array_equal(gpu["n_rois"], orc["n_rois"])
@@ -213,10 +214,11 @@ def _compare_full(run, gpu, orc, check_canvases=True):
             assert np.array_equal(got[k], want[k]), f"canvas {k}"
 
 
-def test_pipeline_cfg1_bit_exact(ctx):
+@pytest.mark.parametrize("keep", [True, False])
+def test_pipeline_cfg1_bit_exact(ctx, keep):
     """BASELINE config 1: one 1920x1080 camera, 30 frames, 4x4 grid, 1024^2
     canvases -- every intermediate and every canvas byte."""
-    run = GpuRun(ctx, 1920, 1080, 30, seed=1000)
+    run = GpuRun(ctx, 1920, 1080, 30, seed=1000, keep_mask=keep)
     gpu = run.run()
     orc = run.oracle()
     _compare_full(run, gpu, orc)
@@ -238,10 +240,11 @@ def test_pipeline_cfg1_reference_rect_stages(ctx):
     run.close()
 
 
-def test_pipeline_cfg2_4k_bit_exact(ctx):
+@pytest.mark.parametrize("keep", [True, False])
+def test_pipeline_cfg2_4k_bit_exact(ctx, keep):
     """BASELINE config 2 geometry (3840x2160, moderate density), first 20
     frames, every byte."""
-    run = GpuRun(ctx, 3840, 2160, 20, seed=1000)
+    run = GpuRun(ctx, 3840, 2160, 20, seed=1000, keep_mask=keep)
     gpu = run.run()
     orc = run.oracle()
     _compare_full(run, gpu, orc)
@@ -351,11 +354,12 @@ def test_round_trip_fixture(ctx):
     dict(W=1920, H=1080, n=6, trace_kw=dict(roi_proportion_mean=0.59, roi_max_dim=1080,
                                             roi_count_max=30)),  # dense, oversize patches
 ])
-def test_pipeline_edge_cases(ctx, case):
+@pytest.mark.parametrize("keep", [True, False])
+def test_pipeline_edge_cases(ctx, case, keep):
     case = dict(case)
     W, H, n = case.pop("W"), case.pop("H"), case.pop("n")
     tk = case.pop("trace_kw", dict(roi_max_dim=min(480, W, H)))
-    run = GpuRun(ctx, W, H, n, seed=7, trace_kw=tk, **case)
+    run = GpuRun(ctx, W, H, n, seed=7, trace_kw=tk, keep_mask=keep, **case)
     gpu = run.run()
     orc = run.oracle()
     _compare_full(run, gpu, orc)

@@ -80,7 +80,7 @@ int main() {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  const int spans_S[] = {256, 512, 1024, 2048, 4096};
+  const int spans_S[] = {256, 512, 1024, 2048, 4096, 16384, 65536};
   for (int S : spans_S) {
     const int nspans = static_cast<int>((1ull << 30) / S) ;  // 1 GB read
     std::vector<uint64_t> h(nspans);
