@@ -7,8 +7,8 @@
  * the thin C layer underneath the C++ drop-in (include/tangram/[name].hpp), plus
  * the batched device entry points that carry the data-parallel hot path:
  *
- *   frames -> [K1 mask+cells] -> [K2 RoI boxes, K3 partition, K4 stitch plan]
- *          -> [scan] -> [K5 canvas gather]            (all stream-ordered)
+ *   frames -> [K1 mask+cells] -> [K2 RoI boxes, K3 partition, K4 stitch plan,
+ *              frame-order prefix] -> [K5 canvas gather]   (all stream-ordered)
  *
  * Conventions
  *   - Plain pointers and sizes only.  "d_" pointers are device memory,
@@ -19,7 +19,11 @@
  *   - Stream-ordered calls take a `void* stream` (a cudaStream_t; NULL = the
  *     context's own stream).  Device-side errors are latched in the context
  *     and reported by the next synchronizing call.
- *   - One context per device; a context is not thread-safe.
+ *   - One context per device; a context is not thread-safe.  Work that uses
+ *     a context's or a pipeline's device counters (a pipeline's stages; the
+ *     context's explicit-plan gathers tg_stitch_gather / tg_batcher_gather*)
+ *     must not run concurrently on two streams: each pipeline, and each
+ *     context's gathers, belong to one stream at a time.
  *   - There is no CPU fallback: without a CUDA device every compute call
  *     returns TG_ERR_NO_DEVICE.
  */
