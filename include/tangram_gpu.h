@@ -134,6 +134,9 @@ tg_status tg_memcpy_async(tg_ctx* ctx, void* dst, const void* src, size_t bytes,
                           void* stream);
 tg_status tg_memset_async(tg_ctx* ctx, void* d_ptr, int32_t value, size_t bytes, void* stream);
 tg_status tg_stream_create(tg_ctx* ctx, void** stream);
+/* high != 0: the device's greatest stream priority (its CTAs are scheduled
+ * ahead of pending CTAs of default-priority streams). */
+tg_status tg_stream_create_priority(tg_ctx* ctx, int32_t high, void** stream);
 tg_status tg_stream_destroy(tg_ctx* ctx, void* stream);
 tg_status tg_stream_synchronize(tg_ctx* ctx, void* stream);
 tg_status tg_event_create(tg_ctx* ctx, void** event);

@@ -126,6 +126,7 @@ SIGNATURES = {
     "tg_memcpy_async": (st, [vp, vp, vp, sz, i32, vp]),
     "tg_memset_async": (st, [vp, vp, i32, sz, vp]),
     "tg_stream_create": (st, [vp, P(vp)]),
+    "tg_stream_create_priority": (st, [vp, i32, P(vp)]),
     "tg_stream_destroy": (st, [vp, vp]),
     "tg_stream_synchronize": (st, [vp, vp]),
     "tg_event_create": (st, [vp, P(vp)]),

@@ -269,9 +269,12 @@ class Context:
     def stream_sync(self, stream=None) -> None:
         check(self._lib.tg_stream_synchronize(self.handle, stream))
 
-    def new_stream(self) -> int:
+    def new_stream(self, high_priority: bool = False) -> int:
         s = C.c_void_p()
-        check(self._lib.tg_stream_create(self.handle, C.byref(s)))
+        if high_priority:
+            check(self._lib.tg_stream_create_priority(self.handle, 1, C.byref(s)))
+        else:
+            check(self._lib.tg_stream_create(self.handle, C.byref(s)))
         return s.value
 
     def event(self) -> int:

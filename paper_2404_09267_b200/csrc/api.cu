@@ -363,6 +363,17 @@ tg_status tg_stream_create(tg_ctx* ctx, void** stream) {
   return TG_OK;
 }
 
+tg_status tg_stream_create_priority(tg_ctx* ctx, int32_t high, void** stream) {
+  tg_status s = use_device(ctx);
+  if (s) return s;
+  int least = 0, greatest = 0;
+  TG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  cudaStream_t st;
+  TG_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, high ? greatest : least));
+  *stream = st;
+  return TG_OK;
+}
+
 tg_status tg_stream_destroy(tg_ctx* ctx, void* stream) {
   tg_status s = use_device(ctx);
   if (s) return s;

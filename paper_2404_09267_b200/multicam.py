@@ -90,7 +90,10 @@ class MultiCameraPath:
         self.canvas_bytes = canvas[0] * canvas[1] * 3
         self.canvas_cap = canvas_capacity
         self.d_canvases = None
-        self.stream = ctx.new_stream()   # K1-K4 and the descriptor read-back
+        # K1-K4 and the descriptor read-back; high priority, so pass i+1's
+        # planner CTAs run ahead of pass i's pending K5 CTAs and the host gets
+        # the descriptors without waiting for the gather
+        self.stream = ctx.new_stream(high_priority=True)
         self.gstream = ctx.new_stream()  # K5 (event canvases)
         self._gdone = ctx.event()
         # pinned landing zone of the descriptor read-back: patches, admission, counts
