@@ -474,3 +474,20 @@ def test_gather_repeats_and_rewrites_every_byte(ctx):
     orc = run.oracle()
     assert np.array_equal(first, orc["canvases"][:total])
     run.close()
+
+
+def test_c07_granularity_on_device_partition(ctx):
+    """acceptance_test.cpp:310-347 with the device partition (drop-in
+    tg_partition): finer zone grids transmit no more bytes; and every frame's
+    patches equal the reference port's."""
+    from tests.test_geometry_cpu import c07_means, check_c07
+
+    def pb(i, W, H, t, z, rois):
+        got = A.partition(A.FrameSpec(i, W, H, t, 1_000_000), A.PartitionConfig(z, z),
+                          [A.Rect(*r) for r in rois], 1.5, 0, ctx=ctx)
+        if i % 17 == 0:  # sampled frames: field-for-field against the port
+            want = O.partition(i, W, H, t, 1_000_000, z, z, rois, 1.5, 0)
+            assert patch_tuples([got]) == oracle_patch_tuples([want])
+        return float(sum(p.size_bytes for p in got))
+
+    check_c07(*c07_means(pb))
