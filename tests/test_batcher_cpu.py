@@ -268,3 +268,75 @@ def test_descriptor_compaction_layout():
         A.check(N.lib().tg_descriptors_compact(pat.ctypes.data, cnt.ctypes.data, adm.ctypes.data,
                                                Z, cams.ctypes.data, len(cams), n, out.ctypes.data,
                                                max(0, k.value - 1), C.byref(k)))
+
+
+def test_infeasible_arrival_flushes_then_requeues():
+    """scheduler_test.cpp:133-162."""
+    s = sched(4)
+    a = full_patch(1, 0, 500_000)
+    a.rect = A.Rect(0, 0, 50, 100)
+    b = full_patch(2, 200_000, 260_000)
+    b.rect = A.Rect(50, 0, 50, 100)
+    assert s.on_patch_arrival(a, 0) == []
+    assert s.on_patch_arrival(b, 200_000) == []
+    assert s.current_canvas_count() == 1 and s.remaining_time_us() == 330_000
+    c = full_patch(3, 340_000, 140_000)
+    evs = s.on_patch_arrival(c, 340_000)
+    assert len(evs) == 1
+    assert (evs[0].trigger, evs[0].patch_ids, evs[0].batch_size) == ("infeasible_arrival", [1, 2], 1)
+    assert s.queue_size() == 1 and s.remaining_time_us() == 350_000
+    assert s.pending_timer().fire_at_us == 350_000
+
+
+def test_solo_infeasible_patch_dispatches_immediately():
+    """scheduler_test.cpp:164-177: SLO 120 ms < slack(1) = 130 ms."""
+    s = sched(2)
+    evs = s.on_patch_arrival(full_patch(1, 0, 120_000), 0)
+    assert [(e.trigger, e.fire_time_us, e.batch_size, e.patch_ids) for e in evs] == \
+        [("infeasible_arrival", 0, 1, [1])]
+    assert s.idle() and s.pending_timer() is None
+
+
+def test_flush_and_solo_dispatch_in_one_arrival():
+    """scheduler_test.cpp:179-195."""
+    s = sched(2)
+    s.on_patch_arrival(full_patch(1, 0, 500_000), 0)
+    evs = s.on_patch_arrival(full_patch(2, 300_000, 120_000), 300_000)
+    assert [(e.trigger, e.patch_ids, e.fire_time_us) for e in evs] == \
+        [("infeasible_arrival", [1], 300_000), ("infeasible_arrival", [2], 300_000)]
+    assert s.idle()
+
+
+def test_zero_remaining_time_still_feasible():
+    """scheduler_test.cpp:197-209: deadline == slack(1) -> timer at now."""
+    s = sched(2)
+    assert s.on_patch_arrival(full_patch(1, 0, 130_000), 0) == []
+    t = s.pending_timer()
+    assert t is not None and t.fire_at_us == 0
+    ev = s.on_timer(0, t.epoch)
+    assert ev is not None and ev.trigger == "deadline_timer"
+
+
+def test_timer_after_reset_is_ignored():
+    """scheduler_test.cpp:211-219."""
+    s = sched(2)
+    s.on_patch_arrival(full_patch(1, 0, 500_000), 0)
+    epoch = s.pending_timer().epoch
+    assert s.on_timer(370_000, epoch) is not None
+    assert s.on_timer(370_000, epoch) is None
+
+
+def test_transmission_known_answers():
+    """trace_test.cpp:243-275: 1 MB at 80 Mbps = 100 ms; FIFO link."""
+    def sized(pid, gen, nbytes):
+        return A.PatchMeta(pid, pid, A.Rect(0, 0, 1, 1), gen, 1_000_000, gen + 1_000_000, nbytes)
+
+    assert A.transmission_schedule([sized(0, 0, 1_000_000)], 80.0) == [100_000]
+    assert A.transmission_schedule([sized(0, 0, 2_000_000)], 80.0) == [200_000]
+    assert A.transmission_schedule([sized(0, 0, 0)], 80.0) == [0]
+    with pytest.raises(A.InvalidArgument):
+        A.transmission_schedule([sized(0, 0, 100)], 0.0)
+    assert A.transmission_schedule([sized(0, 0, 1_000_000), sized(1, 0, 1_000_000),
+                                    sized(2, 150_000, 1_000_000)], 80.0) == \
+        [100_000, 200_000, 300_000]
+    assert A.transmission_schedule([sized(0, 40_000, 250_000)], 80.0) == [65_000]
