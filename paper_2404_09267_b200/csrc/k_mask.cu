@@ -40,8 +40,10 @@
 // mask stage): 1 / 3 / 5 extra warps running K1b tasks beside the stream
 // 1.29 / 1.31 / 1.46 ms vs 1.27 ms without (TG_K1_DILATE_WARPS) -- the task
 // warps slow the stream more than they hide; L2 evict_first on the frame
-// stream + evict_last on the raw words (TG_K1_L2HINTS) cut DRAM reads by
-// 0.14 GB but not time (1.28 ms); consumer warps taking up to 1/2/4/8 ready
+// stream + evict_last on the raw words cut DRAM reads by 0.14 GB but not
+// time (1.28 ms); a sparse raw bitmap (only non-zero words written, plus
+// per-row ballot masks) saved K1 15 us but cost K1b 60 us (the mask loads
+// double its load instructions); consumer warps taking up to 1/2/4/8 ready
 // tasks between their items (never waiting) 1.30/1.33/1.37/1.49 ms.
 #include <algorithm>
 #include <cstdlib>
@@ -50,9 +52,6 @@
 
 namespace tg {
 
-#ifndef TG_K1_L2HINTS
-#define TG_K1_L2HINTS 0
-#endif
 
 constexpr int kK1MaxPartWords = 64;     // 32-pixel words per unit (one per consumer lane)
 constexpr int kK1Group = 2;             // warps per consumer group
@@ -395,9 +394,6 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
     const int g = lane;
     const bool mine = g < units;
     uint32_t used = 0, fills = 0;  // per ring slot: filled before; fill-count parity
-#if TG_K1_L2HINTS
-    const uint64_t pol_stream = l2_evict_first();
-#endif
     int k = 0;                     // ring slot of the next stage
     for (int item = blockIdx.x; item < a.total_items; item += gridDim.x) {
       const ItemK1 it = load_item(a, item);
@@ -417,15 +413,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
             int out;
             const uint8_t* src = ch.next(a, &out) + off;
             mbar_arrive_expect_tx(&full[slot], bytes);
-#if TG_K1_L2HINTS
-            // frames stream through once: keep L2 for the raw bitmap the K1b
-            // tasks read back
-            if (fused)
-              bulk_g2s_hint(slots + static_cast<size_t>(slot) * a.slot_bytes, src, bytes,
-                            &full[slot], pol_stream);
-            else
-#endif
-              bulk_g2s(slots + static_cast<size_t>(slot) * a.slot_bytes, src, bytes, &full[slot]);
+            bulk_g2s(slots + static_cast<size_t>(slot) * a.slot_bytes, src, bytes, &full[slot]);
             used |= bit;
             fills ^= bit;
             if (++k == S) k = 0;
@@ -448,9 +436,6 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
   const int col = (warp - g * kK1Group) * 32 + lane;  // word within the part
   const bool in_slot = 96 * (col + 1) <= a.slot_bytes;  // lane's bytes inside a slot
   uint32_t fpar = 0;  // bit k: parity of the next full phase of ring slot k
-#if TG_K1_L2HINTS
-  const uint64_t pol_keep = l2_evict_last();  // raw words: read back by K1b soon
-#endif
   int k = 0;
   for (int item = blockIdx.x; g < units && item < a.total_items; item += gridDim.x) {
     const ItemK1 it = load_item(a, item);
@@ -475,16 +460,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
       if (f >= 0) {
         uint32_t fw = fg_word<kLow>(C, P, t1);
         if (w == a.nwords - 1) fw &= lastmask;
-#if TG_K1_L2HINTS
-        if (valid) {
-          if (fused)
-            st_hint(out + static_cast<size_t>(f) * fstride, fw, pol_keep);
-          else
-            out[static_cast<size_t>(f) * fstride] = fw;
-        }
-#else
         if (valid) out[static_cast<size_t>(f) * fstride] = fw;
-#endif
       }
 #pragma unroll
       for (int q = 0; q < 6; ++q) P[q] = C[q];
