@@ -449,7 +449,18 @@ def test_cpp_dropin_binary():
     """The C++ drop-in headers (include/tangram/*.hpp) compile against the
     reference's own test expectations and run on the GPU."""
     exe = os.path.join(ROOT, "tests", "cpp", "dropin_test")
-    subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")])
+    subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp"), "dropin_test"])
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "ALL PASS" in out.stdout
+
+
+def test_cpp_pipeline_binary():
+    """The whole path from C++ through the C ABI alone (tests/cpp/
+    pipeline_test.cpp): device frames -> tg_pipeline_run -> descriptors ->
+    tg_batcher_schedule -> event canvases, against the C oracle."""
+    exe = os.path.join(ROOT, "tests", "cpp", "pipeline_test")
+    subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp"), "pipeline_test"])
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "ALL PASS" in out.stdout
