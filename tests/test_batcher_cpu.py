@@ -340,3 +340,40 @@ def test_transmission_known_answers():
                                     sized(2, 150_000, 1_000_000)], 80.0) == \
         [100_000, 200_000, 300_000]
     assert A.transmission_schedule([sized(0, 40_000, 250_000)], 80.0) == [65_000]
+
+
+def test_schedule_descriptors_edge_cases():
+    """tg_batcher_schedule: empty input, cameras without patches, other
+    shards' records (skipped, ids still consumed), out-of-order cameras."""
+    import numpy as np
+
+    from paper_2404_09267_b200 import multicam as MC
+
+    def recs(spec):
+        out = np.zeros(len(spec), MC.DESC_DTYPE)
+        for i, (cam, frame, w) in enumerate(spec):
+            p = out[i]["patch"]
+            p["x"], p["y"], p["w"], p["h"] = 0, 0, w, 100
+            p["generation_time_us"] = frame * 33_333
+            p["slo_us"] = 1_000_000
+            p["deadline_us"] = frame * 33_333 + 1_000_000
+            p["size_bytes"] = w * 150
+            out[i]["patch"] = p
+            out[i]["camera"], out[i]["frame"], out[i]["admitted"] = cam, frame, int(w <= 1024)
+        return out
+
+    def mk():
+        return A.SloScheduler(A.CanvasSpec(1024, 1024), A.LatencyProfile(1024, 1024, SIM_PROFILE), 8)
+
+    n_ev, arr, plan = MC.schedule_descriptors(mk(), recs([]), [0, 1], 4, 80.0)
+    assert n_ev == 0 and len(arr) == 0 and len(plan["patches"]) == 0
+    # camera 1 has no patches; camera 3 belongs to another shard; one oversize patch
+    d = recs([(0, 0, 100), (0, 1, 2000), (1 + 2, 0, 50), (2, 2, 300)])
+    n_ev, arr, plan = MC.schedule_descriptors(mk(), d, [0, 1, 2], 4, 80.0)
+    assert [int(p["patch_id"]) for p in plan["patches"]] == [0, 3]  # ids over all records
+    assert list(plan["src"]) == [0 * 5 + 0 + 1, 2 * 5 + 2 + 1]      # slot * (n + 1) + frame + 1
+    assert n_ev >= 1 and len(arr) == 2
+    with pytest.raises(A.InvalidArgument, match="out of the camera order"):
+        MC.schedule_descriptors(mk(), recs([(2, 0, 100), (0, 0, 100)]), [0, 2], 4, 80.0)
+    with pytest.raises(A.InvalidArgument, match="frame 9 out of range"):
+        MC.schedule_descriptors(mk(), recs([(0, 9, 100)]), [0], 4, 80.0)
