@@ -30,21 +30,21 @@
 // -> packed u32 cell summaries plus an activity bitmask (and the dilated mask
 // on request).
 //
-// Fused launch (launch_mask_fused, the pipeline's mask stage): once a K1
-// CTA's items are streamed, all its warps take K1b tasks from a queue in
-// strip order; a task starts once every K1 item covering its rows has
-// published completion (per-item counters, release/acquire), so the early
-// strips run on CTAs that finish first while others still stream.
-// Cooperative launch guarantees that all CTAs are co-resident, so waiting on
-// other CTAs' items cannot deadlock.  Measured alternatives (300 4K frames,
-// mask stage): 1 / 3 / 5 extra warps running K1b tasks beside the stream
-// 1.29 / 1.31 / 1.46 ms vs 1.27 ms without (TG_K1_DILATE_WARPS) -- the task
-// warps slow the stream more than they hide; L2 evict_first on the frame
-// stream + evict_last on the raw words cut DRAM reads by 0.14 GB but not
-// time (1.28 ms); a sparse raw bitmap (only non-zero words written, plus
-// per-row ballot masks) saved K1 15 us but cost K1b 60 us (the mask loads
-// double its load instructions); consumer warps taking up to 1/2/4/8 ready
-// tasks between their items (never waiting) 1.30/1.33/1.37/1.49 ms.
+// Fused launch (launch_mask_fused, the pipeline's mask stage): ~9 % of the
+// CTAs run only K1b tasks, on SMs of their own, trailing the stream front;
+// the others stream (the same number of items each) and then join them.
+// Tasks come from a queue in strip order; a task starts once every K1 item
+// covering its rows has published completion (per-item counters,
+// release/acquire).  Cooperative launch guarantees that all CTAs are
+// co-resident, so waiting on other CTAs' items cannot deadlock.  Measured
+// alternatives (300 4K frames, mask stage; 1.276 ms with every CTA
+// streaming and K1b as a tail, 1.255 ms as built): 1 / 3 / 5 extra warps per
+// CTA running K1b tasks beside the stream 1.29 / 1.31 / 1.46 ms and consumer
+// warps taking 1/2/4/8 ready tasks between their items 1.30 / 1.33 / 1.37 /
+// 1.49 ms -- K1b on the streaming SMs slows the stream more than it hides;
+// L2 evict_first on the frame stream + evict_last on the raw words cut DRAM
+// reads by 0.14 GB but not time; a sparse raw bitmap (only non-zero words
+// written, plus per-row ballot masks) saved K1 15 us but cost K1b 60 us.
 #include <algorithm>
 #include <cstdlib>
 
@@ -203,6 +203,7 @@ struct MaskArgs {
   int nrb;            // row blocks
   int kf, ntg;        // frames per run, runs
   int total_items;
+  int dctas;          // fused launch: CTAs 0..dctas-1 run only K1b tasks (stream on the rest)
   int nslots;         // ring slots per group
   int slot_bytes;
   uint32_t* raw;      // [F][H][nwords] raw foreground bits
@@ -383,6 +384,13 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
   }
   __syncthreads();
   const int part_bytes = a.part_words * 96;
+  // K1 items go to the streaming CTAs; dedicated K1b CTAs (fused launch)
+  // dilate the strips the stream has finished, on SMs of their own
+  const int scta = static_cast<int>(blockIdx.x) - a.dctas, nscta = static_cast<int>(gridDim.x) - a.dctas;
+  if (scta < 0) {
+    run_dilate_tasks(a, lane);
+    return;
+  }
   const bool fused = a.item_done != nullptr;
 
   if (warp > kK1Groups * kK1Group) {  // K1b task warps (fused launch)
@@ -395,7 +403,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
     const bool mine = g < units;
     uint32_t used = 0, fills = 0;  // per ring slot: filled before; fill-count parity
     int k = 0;                     // ring slot of the next stage
-    for (int item = blockIdx.x; item < a.total_items; item += gridDim.x) {
+    for (int item = scta; item < a.total_items; item += nscta) {
       const ItemK1 it = load_item(a, item);
       const int row = it.y0 + g / a.nparts, part = g % a.nparts;
       const bool live = mine && row < a.H;
@@ -437,7 +445,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
   const bool in_slot = 96 * (col + 1) <= a.slot_bytes;  // lane's bytes inside a slot
   uint32_t fpar = 0;  // bit k: parity of the next full phase of ring slot k
   int k = 0;
-  for (int item = blockIdx.x; g < units && item < a.total_items; item += gridDim.x) {
+  for (int item = scta; g < units && item < a.total_items; item += nscta) {
     const ItemK1 it = load_item(a, item);
     const int row = it.y0 + g / a.nparts, part = g % a.nparts;
     if (row >= a.H) continue;
@@ -578,7 +586,16 @@ cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const*
                       sizeof(uint32_t) * n_frames * a.d.cells_y * a.d.act_words, stream);
   if (e != cudaSuccess) return e;
   // every CTA must be resident: task warps wait on items of other CTAs
-  const int grid = std::min(a.total_items, sms);
+  // Dedicated K1b CTAs: about 9 % of the SMs (the K1b share of the work),
+  // rounded so every streaming CTA gets the same number of items -- the
+  // stream then ends on all SMs at once (4K x 300: 1,620 items on 135 CTAs,
+  // 13 K1b CTAs; mask stage 1.276 -> 1.255 ms, while 14 K1b CTAs leave some
+  // streaming CTAs a 13th item: 1.306 ms).
+  const int reserve = (sms * 9 + 50) / 100;
+  const int per_cta = ceil_div(a.total_items, std::max(1, sms - reserve));
+  const int streaming = ceil_div(a.total_items, per_cta);
+  a.dctas = std::max(0, std::min(sms - 1, env_int("TG_K1_DCTAS", sms - streaming)));
+  const int grid = std::min(a.total_items + a.dctas, sms);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kK1Threads);
