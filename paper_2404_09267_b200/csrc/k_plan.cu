@@ -24,7 +24,10 @@
 
 namespace tg {
 
-constexpr int kPlanThreads = 256;
+#ifndef TG_PLAN_THREADS
+#define TG_PLAN_THREADS 512  // 3 CTAs per SM still fit (300 4K frames: one wave); 256: 0.066 ms, 512: 0.052
+#endif
+constexpr int kPlanThreads = TG_PLAN_THREADS;
 
 // Rank sort of one canvas's jobs by (dx, dy) -- unique, since a canvas's
 // placements and free rects are disjoint -- from tmp into out.  One warp.
