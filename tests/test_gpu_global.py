@@ -1,10 +1,10 @@
-"""Global cross-camera mode on the device: two ranks -- two
-processes on this one GPU, gloo for the host exchange -- each run K1-K4 on
+"""Global cross-camera mode on the device: 2 or 3 ranks --
+processes sharing this one GPU, gloo for the host exchange -- each run K1-K4 on
 their own cameras, all-gather the descriptors, replay ONE batcher over every
 camera and write the canvases of their share of the invoke events, reading
-the other rank's frames through CUDA IPC.
+the other ranks' frames through CUDA IPC.
 
-Checks: both ranks take identical decisions, equal to the reference
+Checks: all ranks take identical decisions, equal to the reference
 simulator (tangram::run) over all cameras on the GPU-extracted RoIs; every
 canvas byte of every event equals a host fill from the frames; the ranks'
 event shares partition the events.
@@ -17,7 +17,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-N_CAMS, N_FRAMES, W, H, BW = 4, 8, 1920, 1080, 40.0
+N_CAMS, N_FRAMES, W, H, BW = 5, 8, 1920, 1080, 40.0
 PROFILE = [(1, 60.0, 3.0), (2, 85.0, 4.0), (4, 135.0, 6.0), (8, 235.0, 10.0)]
 
 
@@ -90,14 +90,15 @@ def _port():
     return port
 
 
-def test_global_cross_camera_mode_two_ranks_one_gpu():
+@pytest.mark.parametrize("world", [2, 3])
+def test_global_cross_camera_mode_ranks_on_one_gpu(world):
     import torch.multiprocessing as mp
 
     from oracle import oracle as O
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted((q.get(timeout=300) for _ in procs), key=lambda r: r[0])
@@ -107,8 +108,9 @@ def test_global_cross_camera_mode_two_ranks_one_gpu():
         assert evs is not None, scenes
         assert counted and not bad, (rank, bad)
         assert n_canv > 0
-    assert res[0][1] == res[1][1], "ranks took different batching decisions"
-    assert res[0][2] == res[1][2]
+    for r in res[1:]:
+        assert r[1] == res[0][1], "ranks took different batching decisions"
+        assert r[2] == res[0][2]
     evs = res[0][1]
     assert sum(r[5] for r in res) == sum(e[2] for e in evs)
     if O.have_ref():
