@@ -241,7 +241,9 @@ int ref_run_tangram(const ref_sim_cfg* c, int n_scenes, const int32_t* frames_pe
     const tangram::RunMetrics m = tangram::run(scenes, cfg, prof, &log);
     if (static_cast<int64_t>(m.patches.size()) > patch_cap) throw std::length_error("patch cap");
     for (std::size_t i = 0; i < m.patches.size(); ++i) {
-      admitted[i] = m.patches[i].admitted ? 1 : 0;
+      // bit 0: admitted (sim.hpp:262); bit 1: infeasible at arrival (:296-300)
+      admitted[i] = static_cast<uint8_t>((m.patches[i].admitted ? 1 : 0) |
+                                         (m.patches[i].infeasible_at_arrival ? 2 : 0));
       arrival_us[i] = m.patches[i].admitted ? m.patches[i].arrival_us : -1;
     }
     *n_patches = static_cast<int32_t>(m.patches.size());

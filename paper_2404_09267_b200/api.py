@@ -674,6 +674,7 @@ class SloScheduler:
         if profile is None:
             raise InvalidArgument("scheduler needs a latency profile")
         self.spec = spec
+        self.profile = profile
         h = C.c_void_p()
         check(N.lib().tg_batcher_create(
             N.tg_canvas_spec(spec.width, spec.height, spec.vram_per_canvas_gb), profile._arr,

@@ -302,7 +302,7 @@ def schedule_descriptors(sched, desc: np.ndarray, cameras, n_frames: int, bandwi
     (sim.hpp:262) sent over the uplinks and replayed through `sched` (an
     api.SloScheduler).  Returns (number of events, arrival times of the
     admitted patches, dict(patches=their renumbered metas, src=their frame
-    table indices))."""
+    table indices, infeasible=infeasible-at-arrival flags, sim.hpp:296-300))."""
     desc = np.ascontiguousarray(desc, DESC_DTYPE)
     cams = np.ascontiguousarray(list(cameras), np.int32)
     n = len(desc)
@@ -315,7 +315,10 @@ def schedule_descriptors(sched, desc: np.ndarray, cameras, n_frames: int, bandwi
                                       int(per_camera_link), patches.ctypes.data, src.ctypes.data,
                                       arrival.ctypes.data, C.byref(n_adm), C.byref(n_ev)))
     k = n_adm.value
-    return n_ev.value, arrival[:k], dict(patches=patches[:k], src=src[:k])
+    # sim.hpp:296-300: a patch whose deadline minus the single-canvas slack
+    # is already behind its arrival (a metrics flag; scheduling is unchanged)
+    infeasible = patches[:k]["deadline_us"] - sched.profile.slack_us(1) < arrival[:k]
+    return n_ev.value, arrival[:k], dict(patches=patches[:k], src=src[:k], infeasible=infeasible)
 
 
 def gather_descriptors(local: np.ndarray, dist, device=None) -> np.ndarray:

@@ -79,7 +79,7 @@ def _worker(rank, world, port, q):
         sched_all = A.SloScheduler(A.CanvasSpec(1024, 1024),
                                    A.LatencyProfile(1024, 1024, PROFILE),
                                    A.max_canvases_per_batch(6.0, 2.0, 1.0))
-        n_all, _, _ = MC.schedule_descriptors(sched_all, glob, range(N_CAMS), N_FRAMES, 40.0)
+        n_all, _, plan_all = MC.schedule_descriptors(sched_all, glob, range(N_CAMS), N_FRAMES, 40.0)
         evs_all = [(e.fire_time_us, e.trigger, e.batch_size, e.estimated_slack_us, e.patch_ids)
                    for e in sched_all._events(n_all)]
         ref = None
@@ -92,6 +92,9 @@ def _worker(rank, world, port, q):
             ref_all = [(e["fire_time_us"], names[e["trigger"]], e["batch_size"],
                         e["estimated_slack_us"], e["patch_ids"]) for e in r["events"]]
             same = same and evs_all == ref_all
+            # infeasible-at-arrival flags of the admitted patches (sim.hpp:296-300)
+            ref_inf = [f for f, a in zip(r["infeasible"], r["admitted"]) if a]
+            same = same and [bool(x) for x in plan_all["infeasible"]] == [bool(x) for x in ref_inf]
         q.put((rank, mine, same, len(glob), evs, ref))
         dist.destroy_process_group()
     except Exception as e:  # surface worker failures in the parent
