@@ -7,9 +7,13 @@ Workload (BASELINE.json configs[1]): per GPU one synthetic 3840x2160 RGB
 camera, 300 frames, moderate RoI density (generate_trace defaults with
 roi_proportion_mean=0.10, roi_max_dim=480, fps=30, seed 1000+camera), 4x4
 zone grid, 1024x1024 canvases.  A step is one pass of the whole path over the
-camera's 300 device-resident frames: K1 mask+cells -> K2-K4 planner -> scan
--> K5 canvas gather (plus, at N>1, the NCCL allgather of patch descriptors).
-Inputs (7.5 GB per GPU) are far larger than L2, so no flush is needed.
+camera's 300 device-resident frames: K1 mask + cells -> K2-K4 planner with the
+frame-order prefix -> K5 canvas gather (three launches).  Per-frame stitching
+has no cross-camera exchange, so at N>1 every rank runs its own camera with
+no collective in the step.  Inputs (7.5 GB per GPU) are far larger than L2,
+so no flush is needed.  --config cfg3|cfg4|cfg5 run the other BASELINE
+configurations (multi-camera SLO batching with the NCCL descriptor
+all-gather at N>1, and the density sweep).
 
 `value` is whole-job device throughput (frames/s, max-over-ranks time),
 `e2e` the same through the public API with pinned host frames copied in and
