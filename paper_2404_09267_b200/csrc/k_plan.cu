@@ -69,11 +69,19 @@ __device__ __forceinline__ uint32_t ld_volatile32(const uint32_t* p) {
   return *reinterpret_cast<const volatile uint32_t*>(p);
 }
 
-// Warp 0 of frame f's CTA: publishes (np, nc), returns the exclusive prefix
-// over frames 0..f-1 and publishes the inclusive one.
+// Warp 0 of frame f's CTA publishes (np, nc) as soon as K4 has them
+// (look_publish), builds its gather jobs, then resolves the exclusive prefix
+// over frames 0..f-1 (look_back) -- the wait for slower predecessors hides
+// behind the job sort.
+__device__ __forceinline__ void look_publish(const PlanArgs& a, int f, uint32_t epoch, uint64_t np,
+                                             uint64_t nc, int lane) {
+  if (lane == 0) st_release64(&a.look[f], look_pack(epoch, f == 0 ? kLookIncl : kLookAgg, np, nc));
+}
+
+// after look_publish: sums the predecessors back to the nearest inclusive
+// prefix and publishes this frame's
 __device__ void look_back(const PlanArgs& a, int f, uint32_t epoch, uint64_t np, uint64_t nc,
                           uint64_t* ex_p, uint64_t* ex_c, int lane) {
-  if (lane == 0) st_release64(&a.look[f], look_pack(epoch, f == 0 ? kLookIncl : kLookAgg, np, nc));
   uint64_t sp = 0, sc = 0;
   for (int j = f - 1; j >= 0; j -= 32) {
     const int idx = j - lane;
@@ -226,27 +234,12 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     a.n_canvases[f] = nc < 0 ? 0 : nc;
   }
   const int ncv = nc < 0 ? 0 : nc;
-  uint64_t ex_p, ex_c;
-  look_back(a, f, s_epoch, static_cast<uint64_t>(np), static_cast<uint64_t>(ncv), &ex_p, &ex_c,
-            lane);
-  const uint64_t id0 = s_first + ex_p;
-  const long long cb = static_cast<long long>(ex_c);
-  for (int j = lane; j < np; j += 32) a.patches[static_cast<size_t>(f) * nz + j].patch_id = id0 + j;
-  if (lane == 0) {
-    a.canvas_base[f] = cb;
-    if (f == a.n_frames - 1) plan_totals(a, s_first, ex_p + np, cb + ncv);
-  }
+  look_publish(a, f, s_epoch, static_cast<uint64_t>(np), static_cast<uint64_t>(ncv), lane);
+  // Gather jobs (frame-local): placements and free rects grouped by canvas,
+  // sorted by x; lane c keeps canvases c and c + 32's (first job, count)
+  // for their ranges (a frame has at most zones <= 64 canvases).
+  uint32_t my_rng[2] = {0u, 0u};  // first job | count << 16
   if (ncv > 0) {
-    tg_placement* fpl = a.placements + static_cast<size_t>(f) * nz;
-    for (int k = lane; k < na; k += 32) {
-      tg_placement p;
-      p.patch_id = id0 + static_cast<uint64_t>(adm_idx[k]);
-      p.canvas_index = souts[k].canvas;
-      p.position = tg_rect{souts[k].x, souts[k].y, adm_w[k], adm_h[k]};
-      p.reserved = 0;
-      fpl[k] = p;
-    }
-    // Gather jobs: placements and free rects grouped by canvas, sorted by x.
     Job* fj = a.jobs + static_cast<size_t>(f) * a.job_cap;
     uint32_t* fcj = a.canvas_jobs + static_cast<size_t>(f) * nz;
     const int nitems = na + nfree;
@@ -277,13 +270,37 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
       __syncwarp();
       sort_jobs_by_x(sjobs, cnt, fj + pos, lane);
       __syncwarp();
-      if (lane == 0) {
-        fcj[c] = static_cast<uint32_t>(pos) | static_cast<uint32_t>(cnt) << 16;
-        if (cb + c < a.max_canvases)
-          a.ranges[cb + c] = make_uint2(static_cast<uint32_t>(f) * a.job_cap + pos, cnt);
-      }
+      if (lane == 0) fcj[c] = static_cast<uint32_t>(pos) | static_cast<uint32_t>(cnt) << 16;
+      if (lane == (c & 31)) my_rng[c >> 5] = static_cast<uint32_t>(pos) | static_cast<uint32_t>(cnt) << 16;
       pos += cnt;
     }
+  }
+  // frame-order prefix: global patch ids, canvas numbering
+  uint64_t ex_p, ex_c;
+  look_back(a, f, s_epoch, static_cast<uint64_t>(np), static_cast<uint64_t>(ncv), &ex_p, &ex_c,
+            lane);
+  const uint64_t id0 = s_first + ex_p;
+  const long long cb = static_cast<long long>(ex_c);
+  for (int j = lane; j < np; j += 32) a.patches[static_cast<size_t>(f) * nz + j].patch_id = id0 + j;
+  if (lane == 0) {
+    a.canvas_base[f] = cb;
+    if (f == a.n_frames - 1) plan_totals(a, s_first, ex_p + np, cb + ncv);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = lane + 32 * h;
+    if (c < ncv && cb + c < a.max_canvases)
+      a.ranges[cb + c] = make_uint2(static_cast<uint32_t>(f) * a.job_cap + (my_rng[h] & 0xffffu),
+                                    my_rng[h] >> 16);
+  }
+  tg_placement* fpl = a.placements + static_cast<size_t>(f) * nz;
+  for (int k = lane; k < na; k += 32) {
+    tg_placement p;
+    p.patch_id = id0 + static_cast<uint64_t>(adm_idx[k]);
+    p.canvas_index = souts[k].canvas;
+    p.position = tg_rect{souts[k].x, souts[k].y, adm_w[k], adm_h[k]};
+    p.reserved = 0;
+    fpl[k] = p;
   }
   if (lane == 0) {  // the last CTA out resets the ticket and moves the epoch on
     __threadfence();
