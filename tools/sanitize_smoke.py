@@ -1,0 +1,32 @@
+"""Small end-to-end runs for compute-sanitizer (memcheck / racecheck /
+synccheck): the per-frame pipeline (fused and staged mask paths), the
+batcher gather, and the drop-in stitch.  Tuning / verification aid."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+from paper_2404_09267_b200 import _native as N  # noqa: E402
+from paper_2404_09267_b200 import api as A  # noqa: E402
+from paper_2404_09267_b200 import multicam as MC  # noqa: E402
+from tests._helpers import GpuRun  # noqa: E402
+
+ctx = A.Context(0)
+run = GpuRun(ctx, 640, 368, 4, seed=1000, trace_kw=dict(roi_max_dim=200), keep_mask=False)
+gpu = run.run()
+A.check(N.lib().tg_pipeline_stage_mask_fg(run.pipe.handle, run.n, run.d_cur, run.d_prev, None))
+A.check(N.lib().tg_pipeline_stage_mask_cells(run.pipe.handle, run.n, None))
+ctx.synchronize()
+print("pipeline", gpu["total_canvases"], "canvases")
+run.close()
+path = MC.MultiCameraPath(ctx, [0, 1], 640, 368, 4, [(1, 60.0, 3.0), (2, 85.0, 4.0)],
+                          bandwidth_mbps=40.0, trace_kw=dict(roi_max_dim=200))
+_, n_ev, n_canv = path.step()
+ctx.synchronize()
+print("batcher", n_ev, "events", n_canv, "canvases")
+path.close()
+q = [A.PatchMeta(i, 0, A.Rect(0, 0, 30 + 7 * i, 20 + 5 * i), 0, 1, 1, 1) for i in range(12)]
+res = A.stitch_all(q, A.CanvasSpec(128, 128), ctx=ctx)
+print("stitch", res.canvas_count(), "canvases")
+ctx.close()
