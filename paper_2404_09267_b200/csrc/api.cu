@@ -668,7 +668,7 @@ tg_status tg_pipeline_params_default(int32_t width, int32_t height, tg_pipeline_
 void tg_pipeline_destroy(tg_pipeline* p) {
   if (!p) return;
   cudaSetDevice(p->ctx->device);
-  void* bufs[] = {p->raw, p->mask_sync, p->cells, p->active, p->mask, p->n_rois, p->n_patches, p->n_placements,
+  void* bufs[] = {p->raw, p->mask_sync, p->cells, p->mask, p->n_rois, p->n_patches, p->n_placements,
                   p->n_canvases, p->rois, p->patches, p->admitted, p->placements,
                   p->canvas_base, p->jobs, p->canvas_jobs, p->ranges, p->gather_units,
                   p->id_state, p->look, p->psync};
@@ -722,9 +722,11 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
   };
   cudaError_t e = cudaSuccess;
   if (!e) e = alloc(&p->raw, F * q.height * p->mask_words);
-  if (!e) e = alloc(&p->mask_sync, mask_sync_words(q.height, q.max_frames));
+  // K1 counters followed by the activity bits (p->active): one memset per launch
+  const size_t sync_words = mask_sync_words(q.height, ctx->sms);
+  if (!e) e = alloc(&p->mask_sync, sync_words + F * cy * p->act_words);
+  if (!e) p->active = p->mask_sync + sync_words;
   if (!e) e = alloc(&p->cells, F * cx * cy);
-  if (!e) e = alloc(&p->active, F * cy * p->act_words);
   if (!e && q.keep_mask) e = alloc(&p->mask, F * q.height * p->mask_words);
   if (!e) e = alloc(&p->n_rois, F);
   if (!e) e = alloc(&p->rois, F * q.max_rois_per_frame);

@@ -557,8 +557,9 @@ cudaError_t launch_mask_fg(const uint8_t* const* d_cur, const uint8_t* const* d_
   return cudaGetLastError();
 }
 
-// item counters (<= frames x row blocks) + the task queue head
-size_t mask_sync_words(int H, int max_frames) { return static_cast<size_t>(max_frames) * H + 2; }
+// The task queue head + item counters: total_items = runs x row blocks <=
+// (8 sms / row blocks + 1) x row blocks <= 8 sms + H (plan_k1).
+size_t mask_sync_words(int H, int sms) { return static_cast<size_t>(8) * sms + H + 2; }
 
 cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                               int n_frames, int W, int H, int pitch, int threshold, int radius,
@@ -572,18 +573,21 @@ cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const*
   if (e != cudaSuccess) return e;
   a.d = dilate_args(d_raw, W, H, d_cells, d_active, d_mask);
   if (a.d.act_words > kK1MaxActWords) return cudaErrorInvalidConfiguration;
-  if (static_cast<size_t>(a.total_items) + 1 > mask_sync_words(H, n_frames))
-    return cudaErrorInvalidConfiguration;
+  const size_t sync_words = mask_sync_words(H, sms);
+  if (static_cast<size_t>(a.total_items) + 1 > sync_words) return cudaErrorInvalidConfiguration;
   a.radius = radius;
   a.dgroups = ceil_div(a.nwords, kK1GroupWords);
   a.strips = ceil_div(a.d.cells_y, kK1bBands);
   a.n_tasks = a.strips * n_frames * a.dgroups;
   a.task_next = d_sync;
   a.item_done = d_sync + 1;
-  e = cudaMemsetAsync(d_sync, 0, sizeof(uint32_t) * (a.total_items + 1), stream);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(d_active, 0,
-                      sizeof(uint32_t) * n_frames * a.d.cells_y * a.d.act_words, stream);
+  const size_t act_words = static_cast<size_t>(n_frames) * a.d.cells_y * a.d.act_words;
+  if (d_active == d_sync + sync_words) {  // one allocation: one memset clears both
+    e = cudaMemsetAsync(d_sync, 0, sizeof(uint32_t) * (sync_words + act_words), stream);
+  } else {
+    e = cudaMemsetAsync(d_sync, 0, sizeof(uint32_t) * (a.total_items + 1), stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_active, 0, sizeof(uint32_t) * act_words, stream);
+  }
   if (e != cudaSuccess) return e;
   // every CTA must be resident: task warps wait on items of other CTAs
   // Dedicated K1b CTAs: about 9 % of the SMs (the K1b share of the work),

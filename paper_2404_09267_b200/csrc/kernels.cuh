@@ -13,8 +13,9 @@ cudaError_t launch_dilate_cells(const uint32_t* d_raw, int n_frames, int W, int 
                                 uint32_t* d_cells, uint32_t* d_active, uint32_t* d_mask,
                                 cudaStream_t stream);
 // K1 + K1b in one cooperative launch (K1b tasks run beside the stream);
-// d_sync: mask_sync_words(H, max_frames) u32 of scratch.
-size_t mask_sync_words(int H, int max_frames);
+// d_sync: mask_sync_words(H, sms) u32 of scratch; when d_active follows it
+// directly (one allocation) a single memset clears both.
+size_t mask_sync_words(int H, int sms);
 cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                               int n_frames, int W, int H, int pitch, int threshold, int radius,
                               uint32_t* d_raw, uint32_t* d_cells, uint32_t* d_active,
