@@ -502,3 +502,31 @@ def test_c07_granularity_on_device_partition(ctx):
         return float(sum(p.size_bytes for p in got))
 
     check_c07(*c07_means(pb))
+
+
+def test_chunked_runs_continue_patch_ids_on_device(ctx):
+    """The e2e path's chunked streaming: runs over consecutive chunks with
+    first_patch_id = TG_CONTINUE_PATCH_IDS number patches exactly as one run
+    over all frames (sim.hpp:249-251), with no host round trip, and every
+    chunk's canvases equal the single run's."""
+    n, chunk = 20, 7
+    run = GpuRun(ctx, 1280, 720, n, seed=1010, trace_kw=dict(roi_proportion_mean=0.2),
+                 keep_mask=False)
+    whole = run.run()
+    want_canv = run.canvases()
+    got_patches, got_pl, got_canv = [], [], []
+    for c0 in range(0, n, chunk):
+        m = min(chunk, n - c0)
+        first = 0 if c0 == 0 else 0xFFFFFFFFFFFFFFFF  # TG_CONTINUE_PATCH_IDS
+        run.pipe.run(m, run.d_cur + 8 * c0, run.d_prev + 8 * c0, run.d_ids + 8 * c0,
+                     run.d_gen + 8 * c0, first, run.d_canvases)
+        res = run.pipe.results(m)
+        got_patches += patch_tuples(res["patch_list"])
+        got_pl += res["placement_list"]
+        got_canv.append(run.ctx.download(run.d_canvases, (res["total_canvases"], 1024, 1024 * 3),
+                                         np.uint8))
+    assert got_patches == patch_tuples(whole["patch_list"])
+    # placements: same patch ids and positions; canvas indices are per frame
+    assert got_pl == whole["placement_list"]
+    assert np.array_equal(np.concatenate(got_canv), want_canv)
+    run.close()
