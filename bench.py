@@ -68,6 +68,19 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def bind_to_gpu_numa(local: int) -> None:
+    """Pins this rank's host threads to the CPUs nearest its GPU (NVML), so the
+    pinned frame buffers of the e2e leg sit on the GPU's NUMA node.  Best
+    effort: no NVML, no change."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        pynvml.nvmlDeviceSetCpuAffinity(pynvml.nvmlDeviceGetHandleByIndex(local))
+        pynvml.nvmlShutdown()
+    except Exception:
+        pass
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -127,6 +140,8 @@ class Clocks:
 # ================================================================== ours
 def run_ours(args):
     rank, world, local = dist_env()
+    if world > 1:
+        bind_to_gpu_numa(local)
     dist = None
     if world > 1:
         import torch
