@@ -68,6 +68,34 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def gpu_of(local: int) -> int:
+    """This rank's device.  TG_BENCH_SHARE_GPU=1 (validation only: every rank
+    on the visible GPUs round-robin, gloo for the host exchange) lets the
+    multi-rank control flow run on a one-GPU box; timings are then not a
+    scaling measurement."""
+    if os.environ.get("TG_BENCH_SHARE_GPU") == "1":
+        import torch
+        return local % max(1, torch.cuda.device_count())
+    return local
+
+
+def init_dist(local: int):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(gpu_of(local))
+    dist.init_process_group("gloo" if os.environ.get("TG_BENCH_SHARE_GPU") == "1" else "nccl")
+    return dist
+
+
+def reduce_max(dist, value: float, local: int) -> float:
+    """Max over ranks (device tensor on NCCL, host tensor on gloo)."""
+    import torch
+    dev = "cpu" if dist.get_backend() == "gloo" else f"cuda:{gpu_of(local)}"
+    t = torch.tensor([value], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def bind_to_gpu_numa(local: int) -> None:
     """Pins this rank's host threads to the CPUs nearest its GPU (NVML), so the
     pinned frame buffers of the e2e leg sit on the GPU's NUMA node.  Best
@@ -141,18 +169,16 @@ class Clocks:
 def run_ours(args):
     rank, world, local = dist_env()
     if world > 1:
-        bind_to_gpu_numa(local)
+        bind_to_gpu_numa(gpu_of(local))
     dist = None
     if world > 1:
         import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist = init_dist(local)
     from paper_2404_09267_b200 import api as A
     from paper_2404_09267_b200 import _native as N
 
     n = args.frames
-    ctx = A.Context(local)
+    ctx = A.Context(gpu_of(local))
     camera = rank
     seed = 1000 + camera
     t_us, rects = A.generate_trace(n_frames=n, fps=30.0, frame_width=W, frame_height=H,
@@ -191,7 +217,7 @@ def run_ours(args):
     K = args.steps
     evs = [[ctx.event() for _ in range(4)] for _ in range(K)]
     e0, e1 = ctx.event(), ctx.event()
-    clocks = Clocks(local)
+    clocks = Clocks(gpu_of(local))
     if dist is not None:
         torch.cuda.synchronize()
         dist.barrier()
@@ -210,9 +236,7 @@ def run_ours(args):
     plan = [ctx.elapsed_ms(e[1], e[2]) for e in evs]
     gat = [ctx.elapsed_ms(e[2], e[3]) for e in evs]
     if dist is not None:
-        t = torch.tensor([total_ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = reduce_max(dist, total_ms, local)
         dist.barrier()
     ms_step = total_ms / K
     frames_total = n * K * world
@@ -356,9 +380,7 @@ def e2e(ctx, pipe, ring, n, d_ids, d_gen, d_canv, stream, args, world, dist):
     ms = ctx.elapsed_ms(e0, e1)
     if dist is not None:
         import torch
-        t = torch.tensor([ms], device=f"cuda:{ctx.device}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = reduce_max(dist, ms, ctx.device)
     ctx.free_host(host)
     ctx.free_host(hdesc)
     return {"value": round(n * args.steps * world / (ms / 1e3), 1), "unit": "frames/s",
@@ -473,21 +495,19 @@ def run_multicam(args):
     dist = None
     if world > 1:
         import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist = init_dist(local)
     from paper_2404_09267_b200 import api as A
     from paper_2404_09267_b200 import multicam as MC
     n_cams_total = 5 if args.config == "cfg3" else 64
     frames = min(args.frames, 300 if args.config == "cfg3" else 30)
     cams = MC.shard_cameras(n_cams_total, world, rank)
-    ctx = A.Context(local)
+    ctx = A.Context(gpu_of(local))
     kw = dict(bandwidth_mbps=SIM_BANDWIDTH_MBPS, gpu_memory_gb=SIM_GPU_MEMORY_GB, model_size_gb=4.0,
               trace_kw=dict(roi_proportion_mean=0.10, roi_max_dim=480))
     glob = args.global_batching and dist is not None
     if glob:
         path = MC.GlobalCameraPath(ctx, n_cams_total, rank, world, dist, W, H, frames, SIM_PROFILE,
-                                   device=f"cuda:{local}", **kw)
+                                   device=f"cuda:{gpu_of(local)}" if dist.get_backend() == "nccl" else None, **kw)
     else:
         path = MC.MultiCameraPath(ctx, cams, W, H, frames, SIM_PROFILE, **kw)
     e0, e1 = ctx.event(), ctx.event()
@@ -495,13 +515,14 @@ def run_multicam(args):
     if dist is not None and not glob:
         # every rank schedules its shard from the all-gathered list (global ids)
         def exchange(desc):
-            return MC.gather_descriptors(desc, dist, device=f"cuda:{local}")
+            return MC.gather_descriptors(
+                desc, dist, device=f"cuda:{gpu_of(local)}" if dist.get_backend() == "nccl" else None)
 
     # K steps = K passes over the shard's frames; the host batcher of pass i
     # overlaps the device planes of pass i+1 (MultiCameraPath.run_pipelined)
     n_canv = path.run_pipelined(args.warmup, exchange)
     ctx.stream_sync(path.stream)
-    clocks = Clocks(local)
+    clocks = Clocks(gpu_of(local))
     if dist is not None:
         dist.barrier()
     ctx.synchronize()
@@ -514,9 +535,7 @@ def run_multicam(args):
     ms = ctx.elapsed_ms(e0, e1)
     if dist is not None:
         import torch
-        t = torch.tensor([ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = reduce_max(dist, ms, local)
     n_events = path._nev
     out = {
         "metric": METRIC, "value": round(len(cams) * frames * args.steps * world / (ms / 1e3), 1),
