@@ -144,6 +144,7 @@ tg_status tg_event_destroy(tg_ctx* ctx, void* event);
 tg_status tg_event_record(tg_ctx* ctx, void* event, void* stream);
 tg_status tg_event_elapsed_ms(tg_ctx* ctx, void* start, void* stop, float* ms);
 tg_status tg_stream_wait_event(tg_ctx* ctx, void* stream, void* event);
+tg_status tg_event_synchronize(tg_ctx* ctx, void* event);  /* host waits for the event */
 
 /* ---- drop-in rect-level API (host in, host out, blocking) ----------------
  * Replaces, call for call:

@@ -134,6 +134,7 @@ SIGNATURES = {
     "tg_event_record": (st, [vp, vp, vp]),
     "tg_event_elapsed_ms": (st, [vp, vp, vp, P(C.c_float)]),
     "tg_stream_wait_event": (st, [vp, vp, vp]),
+    "tg_event_synchronize": (st, [vp, vp]),
     "tg_make_zones": (st, [P(tg_frame_spec), tg_partition_config, P(tg_rect), i32]),
     "tg_assign_rois": (st, [vp, P(tg_rect), i32, P(tg_rect), i32, P(i32)]),
     "tg_partition": (st, [vp, P(tg_frame_spec), tg_partition_config, P(tg_rect), i32, C.c_double,

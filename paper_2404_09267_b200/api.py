@@ -285,6 +285,9 @@ class Context:
     def record(self, ev: int, stream=None) -> None:
         check(self._lib.tg_event_record(self.handle, ev, stream))
 
+    def event_sync(self, ev: int) -> None:
+        check(self._lib.tg_event_synchronize(self.handle, ev))
+
     def elapsed_ms(self, start: int, stop: int) -> float:
         ms = C.c_float()
         check(self._lib.tg_event_elapsed_ms(self.handle, start, stop, C.byref(ms)))

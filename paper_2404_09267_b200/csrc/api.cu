@@ -420,6 +420,13 @@ tg_status tg_event_elapsed_ms(tg_ctx* ctx, void* start, void* stop, float* ms) {
   return TG_OK;
 }
 
+tg_status tg_event_synchronize(tg_ctx* ctx, void* event) {
+  tg_status s = use_device(ctx);
+  if (s) return s;
+  TG_CUDA(cudaEventSynchronize(static_cast<cudaEvent_t>(event)));
+  return TG_OK;
+}
+
 tg_status tg_stream_wait_event(tg_ctx* ctx, void* stream, void* event) {
   tg_status s = use_device(ctx);
   if (s) return s;

@@ -97,9 +97,11 @@ class MultiCameraPath:
         self.gstream = ctx.new_stream()  # K5 (event canvases)
         self._gdone = ctx.event()
         # pinned landing zone of the descriptor read-back: patches, admission, counts
+        # (two of them: pass i+1's read-back lands while pass i's is compacted)
         nslot = len(self.cameras) * n_frames * self.zones
-        self._hbytes = nslot * 64 + nslot + 4 * len(self.cameras) * n_frames
-        self._h = ctx.malloc_host(max(1, self._hbytes))
+        self._hbytes = (nslot * 64 + nslot + 4 * len(self.cameras) * n_frames + 255) & ~255
+        self._h = ctx.malloc_host(max(1, 2 * self._hbytes))
+        self._fetched = [ctx.event(), ctx.event()]
         self._cams = np.array(self.cameras, np.int32)
         self._desc = np.zeros(max(1, nslot), DESC_DTYPE)
 
@@ -124,23 +126,38 @@ class MultiCameraPath:
                                          self.stream))
 
     # ---- 2. descriptors to the host ----------------------------------------
-    def descriptors(self) -> np.ndarray:
-        """DESC_DTYPE records of every patch of the shard, camera-major,
-        frame order, zone order (ids numbered over the shard; `schedule`
-        renumbers them over the whole camera set).  Waits for the planes."""
+    def fetch_descriptors(self, slot: int = 0):
+        """Enqueues the read-back of the planes' patch slots into pinned
+        buffer `slot` on `stream` (after the planes, before anything later)."""
         Z, F = self.zones, len(self.cameras) * self.n
         if not F:
-            return self._desc[:0]
-        v, h = self.pipe.views, self._h
+            return
+        v, h = self.pipe.views, self._h + slot * self._hbytes
         self.ctx.memcpy(h, v.patches, F * Z * 64, 1, self.stream)
         self.ctx.memcpy(h + F * Z * 64, v.admitted, F * Z, 1, self.stream)
         self.ctx.memcpy(h + F * Z * 65, v.n_patches, F * 4, 1, self.stream)
-        self.ctx.stream_sync(self.stream)
+        self.ctx.record(self._fetched[slot], self.stream)
+
+    def compact_descriptors(self, slot: int = 0) -> np.ndarray:
+        """Waits for read-back `slot` and compacts it (tg_descriptors_compact)
+        into DESC_DTYPE records; the view is valid until the next call."""
+        Z, F = self.zones, len(self.cameras) * self.n
+        if not F:
+            return self._desc[:0]
+        self.ctx.event_sync(self._fetched[slot])
+        h = self._h + slot * self._hbytes
         n = C.c_int64()
         check(N.lib().tg_descriptors_compact(h, h + F * Z * 65, h + F * Z * 64, Z,
                                              self._cams.ctypes.data, len(self.cameras), self.n,
                                              self._desc.ctypes.data, len(self._desc), C.byref(n)))
         return self._desc[:n.value]
+
+    def descriptors(self) -> np.ndarray:
+        """DESC_DTYPE records of every patch of the shard, camera-major,
+        frame order, zone order (ids numbered over the shard; `schedule`
+        renumbers them over the whole camera set).  Waits for the planes."""
+        self.fetch_descriptors(0)
+        return self.compact_descriptors(0)
 
     # ---- 3. host: ids, admission, links, batcher ----------------------------
     def schedule(self, desc: np.ndarray):
@@ -173,22 +190,24 @@ class MultiCameraPath:
 
     def run_pipelined(self, steps: int, exchange=None) -> int:
         """`steps` passes over the shard's frames with the host batcher of
-        pass i overlapping the device planes (K1-K4) of pass i+1; K5 of pass
-        i runs on `gstream`.  `exchange(desc) -> desc` (e.g. the NCCL
+        pass i overlapping the device planes (K1-K4) of pass i+1, which are
+        queued behind pass i's descriptor read-back (double-buffered pinned
+        memory), so the device never waits for the host; K5 of pass i runs
+        on `gstream`.  `exchange(desc) -> desc` (e.g. the NCCL
         descriptor all-gather) runs before each schedule.  Returns the last
         pass's canvas count; `stream` is joined with every gather."""
         n_canv = 0
         self.run_planes()
-        desc = self.descriptors()
+        self.fetch_descriptors(0)
         for i in range(steps):
-            if i + 1 < steps:
+            if i + 1 < steps:  # queued behind pass i's read-back: no host wait in between
                 self.run_planes()
+                self.fetch_descriptors((i + 1) % 2)
+            desc = self.compact_descriptors(i % 2)
             if exchange is not None:
                 desc = exchange(desc)
             self.schedule(desc)
             n_canv = self.gather(join=False)
-            if i + 1 < steps:
-                desc = self.descriptors()
         self.join()
         return n_canv
 
