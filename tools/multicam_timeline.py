@@ -18,7 +18,7 @@ path = MC.MultiCameraPath(ctx, list(range(ncam)), W, H, frames, bench.SIM_PROFIL
                           trace_kw=dict(roi_proportion_mean=0.10, roi_max_dim=480))
 path.run_pipelined(3)
 ctx.synchronize()
-steps = 6
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 6
 ev = {k: [ctx.event() for _ in range(steps + 1)] for k in ("p0", "p1", "g0", "g1")}
 host = []
 t_start = time.perf_counter()
@@ -33,18 +33,18 @@ def planes(i):
 origin = ctx.event()
 ctx.record(origin, path.stream)
 planes(0)
-desc = path.descriptors()
-for i in range(steps):
+path.fetch_descriptors(0)
+for i in range(steps):  # MultiCameraPath.run_pipelined, with events
     h0 = time.perf_counter()
     if i + 1 < steps:
         planes(i + 1)
+        path.fetch_descriptors((i + 1) % 2)
+    desc = path.compact_descriptors(i % 2)
     path.schedule(desc)
     h1 = time.perf_counter()
     ctx.record(ev["g0"][i], path.gstream)
     path.gather(join=False)
     ctx.record(ev["g1"][i], path.gstream)
-    if i + 1 < steps:
-        desc = path.descriptors()
     host.append((1e3 * (h0 - t_start), 1e3 * (h1 - h0)))
 path.join()
 ctx.synchronize()
