@@ -20,6 +20,20 @@ A.check(N.lib().tg_pipeline_stage_mask_cells(run.pipe.handle, run.n, None))
 ctx.synchronize()
 print("pipeline", gpu["total_canvases"], "canvases")
 run.close()
+# edge geometries: partial words / cell rows, uneven K1 parts, radius 0 / 8,
+# odd canvases, fine zone grids, padded pitch, masks kept
+for W, H, n, kw in [(208, 100, 3, dict(radius=2)), (2080, 70, 3, {}), (8192, 48, 2, {}),
+                    (640, 360, 3, dict(radius=8, keep_mask=True)), (640, 360, 3, dict(radius=0)),
+                    (1280, 720, 2, dict(zones=(8, 8))),
+                    (1280, 720, 2, dict(zones=(3, 5), canvas=(300, 200))),
+                    (640, 352, 2, dict(pitch=640 * 3 + 64))]:
+    kw = dict(kw)
+    kw.setdefault("keep_mask", False)
+    r = GpuRun(ctx, W, H, n, seed=7, trace_kw=dict(roi_max_dim=min(480, W, H)), **kw)
+    g = r.run()
+    ctx.synchronize()
+    print("edge", W, H, g["total_canvases"], "canvases")
+    r.close()
 path = MC.MultiCameraPath(ctx, [0, 1], 640, 368, 4, [(1, 60.0, 3.0), (2, 85.0, 4.0)],
                           bandwidth_mbps=40.0, trace_kw=dict(roi_max_dim=200))
 _, n_ev, n_canv = path.step()
