@@ -315,6 +315,13 @@ tg_status tg_transmission_schedule(const tg_patch_meta* patches, int32_t n, doub
 tg_status tg_batcher_create(tg_canvas_spec spec, const tg_profile_entry* entries, int32_t n_entries,
                             int32_t max_canvases, tg_batcher** out);
 void tg_batcher_destroy(tg_batcher* b);
+/* Event log (scheduler.hpp:93-188 through event_log.hpp): with a policy
+ * name set, every arrival / repack / invoke / timer_set record the
+ * reference SloScheduler writes is appended as its JSON line, byte for byte
+ * (NULL turns logging off).  take_log copies the accumulated lines and
+ * clears them; out == NULL only reports *len. */
+tg_status tg_batcher_set_log(tg_batcher* b, const char* policy);
+tg_status tg_batcher_take_log(tg_batcher* b, char* out, int64_t cap, int64_t* len);
 /* on_patch_arrival (scheduler.hpp:90-126).  src_frame tags the patch's pixels
  * for tg_batcher_gather.  *n_events (0..2) events become readable through
  * tg_batcher_event(b, 0..n-1) until the next call. */

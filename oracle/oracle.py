@@ -361,8 +361,8 @@ def run_tangram(scenes, width, height, profile, zones=(4, 4), canvas=(1024, 1024
                 per_scene_link=True, bytes_per_pixel=1.5, slo_us=1_000_000):
     """The reference's tangram::run() (sim.hpp:206-552, tangram policy) on
     scenes = [(t_us list, per-frame rect lists)].  Returns per-patch
-    (admitted, infeasible-at-arrival, arrival_us) and the scheduler's invoke
-    events from its log."""
+    (admitted, infeasible-at-arrival, arrival_us), the scheduler's invoke
+    events and its raw event log (JSON lines)."""
     dll = load("ref")
     dll.ref_run_tangram.restype = C.c_int
     cfg = SimCfg(width, height, zones[0], zones[1], canvas[0], canvas[1], int(per_scene_link),
@@ -401,7 +401,12 @@ def run_tangram(scenes, width, height, profile, zones=(4, 4), canvas=(1024, 1024
         k += ev_np[i]
         events.append(dict(fire_time_us=ev_fire[i], trigger=ev_trig[i], batch_size=ev_k[i],
                            estimated_slack_us=ev_slack[i], patch_ids=ids))
-    return dict(admitted=[adm[i] & 1 for i in range(npatch.value)],
+    dll.ref_last_log.restype = C.c_int64
+    nlog = dll.ref_last_log(None, C.c_int64(0))
+    logbuf = C.create_string_buffer(max(1, nlog))
+    dll.ref_last_log(logbuf, C.c_int64(nlog))
+    return dict(log=logbuf.raw[:nlog].decode(),
+                admitted=[adm[i] & 1 for i in range(npatch.value)],
                 infeasible=[adm[i] >> 1 & 1 for i in range(npatch.value)],
                 arrival_us=[arrival[i] for i in range(npatch.value)], events=events,
                 mean_canvas_efficiency=eff_mean.value, median_canvas_efficiency=eff_median.value)

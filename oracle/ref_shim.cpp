@@ -195,6 +195,15 @@ typedef struct {
   int64_t slo_us;
 } ref_sim_cfg;
 
+// the event log of the last ref_run_tangram (EventLog JSON lines)
+static std::string g_last_log;
+
+int64_t ref_last_log(char* out, int64_t cap) {
+  const int64_t n = static_cast<int64_t>(g_last_log.size());
+  if (out != nullptr && cap >= n) std::copy(g_last_log.begin(), g_last_log.end(), out);
+  return n;
+}
+
 int ref_run_tangram(const ref_sim_cfg* c, int n_scenes, const int32_t* frames_per_scene,
                     const int64_t* t_us, const int32_t* roi_counts, const orc_rect* rois,
                     const double* profile, int n_profile, int64_t* arrival_us, uint8_t* admitted,
@@ -249,6 +258,7 @@ int ref_run_tangram(const ref_sim_cfg* c, int n_scenes, const int32_t* frames_pe
     *n_patches = static_cast<int32_t>(m.patches.size());
     *eff_mean = m.summary.mean_canvas_efficiency;
     *eff_median = m.summary.median_canvas_efficiency;
+    g_last_log = log_text.str();
     std::istringstream in(log_text.str());
     std::string line;
     int64_t ne = 0, nid = 0;

@@ -164,6 +164,8 @@ SIGNATURES = {
     "tg_transmission_schedule": (st, [P(tg_patch_meta), i32, C.c_double, P(i64)]),
     "tg_batcher_create": (st, [tg_canvas_spec, P(tg_profile_entry), i32, i32, P(vp)]),
     "tg_batcher_destroy": (None, [vp]),
+    "tg_batcher_set_log": (st, [vp, C.c_char_p]),
+    "tg_batcher_take_log": (st, [vp, vp, i64, P(i64)]),
     "tg_batcher_on_patch_arrival": (st, [vp, P(tg_patch_meta), i32, i64, P(i32)]),
     "tg_batcher_on_timer": (st, [vp, i64, u64, P(i32)]),
     "tg_batcher_pending_timer": (st, [vp, P(i32), P(i64), P(u64)]),

@@ -684,6 +684,19 @@ class SloScheduler:
             len(profile.entries), max_canvases, C.byref(h)))
         self.handle = h
 
+    def enable_log(self, policy: str = "tangram") -> None:
+        """Record the reference scheduler's event-log lines (scheduler.hpp:
+        93-188) from now on."""
+        check(N.lib().tg_batcher_set_log(self.handle, policy.encode()))
+
+    def take_log(self) -> str:
+        """The JSON lines recorded since the last call."""
+        n = C.c_int64()
+        check(N.lib().tg_batcher_take_log(self.handle, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(max(1, n.value))
+        check(N.lib().tg_batcher_take_log(self.handle, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value].decode()
+
     def close(self):
         if self.handle:
             N.lib().tg_batcher_destroy(self.handle)

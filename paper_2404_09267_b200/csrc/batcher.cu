@@ -223,6 +223,57 @@ struct tg_batcher {
   int64_t timer_at = 0;
   uint64_t timer_epoch = 0, next_epoch = 1;
   std::vector<Event> events;
+  // Optional event log: the records the reference SloScheduler writes
+  // (scheduler.hpp:93-99 arrival, 153-159 repack, 173-178 invoke, 186-188
+  // timer_set) through EventLog::record (event_log.hpp: nlohmann dump(),
+  // keys sorted, plus "policy"), one JSON line each, byte for byte.
+  bool log_on = false;
+  std::string policy, log;
+
+  static const char* trigger_name(tg_trigger t) {
+    return t == TG_TRIGGER_DEADLINE_TIMER ? "deadline_timer"
+           : t == TG_TRIGGER_INFEASIBLE_ARRIVAL ? "infeasible_arrival"
+                                                : "memory_cap";
+  }
+  void logf(const char* fmt, ...) {
+    char buf[256];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    log += buf;
+  }
+  void log_arrival(const tg_patch_meta& p, int64_t now) {
+    if (!log_on) return;
+    logf("{\"deadline_us\":%lld,\"event\":\"arrival\",\"h\":%d,\"patch\":%llu,\"policy\":\"%s\","
+         "\"t_us\":%lld,\"w\":%d}\n",
+         static_cast<long long>(p.deadline_us), p.rect.h,
+         static_cast<unsigned long long>(p.patch_id), policy.c_str(), static_cast<long long>(now),
+         p.rect.w);
+  }
+  void log_repack(int64_t now, size_t n, int k, int64_t slack, int64_t remain) {
+    if (!log_on) return;
+    logf("{\"canvases\":%d,\"event\":\"repack\",\"patches\":%zu,\"policy\":\"%s\",\"slack_us\":%lld,"
+         "\"t_remain_us\":%lld,\"t_us\":%lld}\n",
+         k, n, policy.c_str(), static_cast<long long>(slack), static_cast<long long>(remain),
+         static_cast<long long>(now));
+  }
+  void log_timer() {
+    if (!log_on) return;
+    logf("{\"epoch\":%llu,\"event\":\"timer_set\",\"fire_at_us\":%lld,\"policy\":\"%s\"}\n",
+         static_cast<unsigned long long>(timer_epoch), static_cast<long long>(timer_at),
+         policy.c_str());
+  }
+  void log_invoke(const Event& ev) {
+    if (!log_on) return;
+    logf("{\"event\":\"invoke\",\"k\":%d,\"patches\":[", ev.info.batch_size);
+    for (size_t i = 0; i < ev.patches.size(); ++i)
+      logf(i ? ",%llu" : "%llu", static_cast<unsigned long long>(ev.patches[i].meta.patch_id));
+    logf("],\"policy\":\"%s\",\"slack_us\":%lld,\"t_us\":%lld,\"trigger\":\"%s\"}\n",
+         policy.c_str(), static_cast<long long>(ev.info.estimated_slack_us),
+         static_cast<long long>(ev.info.fire_time_us),
+         trigger_name(static_cast<tg_trigger>(ev.info.trigger)));
+  }
 
   void reset() {
     queue.clear();
@@ -247,11 +298,13 @@ struct tg_batcher {
         ev.free.push_back(tg_free_rect{c.free[k], ci, k});
     }
     ev.info.n_free = static_cast<int32_t>(ev.free.size());
+    log_invoke(ev);
     events.push_back(std::move(ev));
   }
 
   tg_status arrival(const tg_patch_meta& p, int32_t src, int64_t now) {
     const int M = spec.width, N = spec.height;
+    log_arrival(p, now);
     if (p.rect.w > M || p.rect.h > N)  // stitch.hpp:114-118 (raised inside repack)
       return bfail(TG_ERR_INVALID_ARGUMENT, "patch exceeds canvas (patch %llu, %dx%d)",
                    static_cast<unsigned long long>(p.patch_id), p.rect.w, p.rect.h);
@@ -260,6 +313,7 @@ struct tg_batcher {
     const int k = static_cast<int>(st.canvases.size()) + (ch.fi < 0 ? 1 : 0);
     const int64_t ddl = queue.empty() ? p.deadline_us : std::min(t_ddl, p.deadline_us);
     const int64_t remain = ddl - prof.slack_us(k);
+    log_repack(now, queue.size() + 1, k, prof.slack_us(k), remain);
     const bool over_cap = k > max_canvases;
     if (over_cap || remain < now) {                      // :106-123
       const tg_trigger trig = over_cap ? TG_TRIGGER_MEMORY_CAP : TG_TRIGGER_INFEASIBLE_ARRIVAL;
@@ -269,6 +323,7 @@ struct tg_batcher {
       commit(st, choose(st, p.rect.w, p.rect.h, M, N), p, 0, M, N);
       t_ddl = p.deadline_us;
       t_remain = t_ddl - prof.slack_us(1);
+      log_repack(now, 1, 1, prof.slack_us(1), t_remain);
       if (t_remain < now) {                              // infeasible even alone
         make_event(now, TG_TRIGGER_INFEASIBLE_ARRIVAL);
         reset();
@@ -283,6 +338,7 @@ struct tg_batcher {
     has_timer = true;                                    // arm_timer :124
     timer_at = t_remain;
     timer_epoch = next_epoch++;
+    log_timer();
     return TG_OK;
   }
 
@@ -391,6 +447,23 @@ tg_status tg_batcher_create(tg_canvas_spec spec, const tg_profile_entry* entries
 }
 
 void tg_batcher_destroy(tg_batcher* b) { delete b; }
+
+tg_status tg_batcher_set_log(tg_batcher* b, const char* policy) {
+  b->log_on = policy != nullptr;
+  b->policy = policy ? policy : "";
+  b->log.clear();
+  return TG_OK;
+}
+
+tg_status tg_batcher_take_log(tg_batcher* b, char* out, int64_t cap, int64_t* len) {
+  *len = static_cast<int64_t>(b->log.size());
+  if (out == nullptr) return TG_OK;  // size query
+  if (cap < *len) return bfail(TG_ERR_CAPACITY, "log buffer too small (%lld < %lld)",
+                               static_cast<long long>(cap), static_cast<long long>(*len));
+  std::copy(b->log.begin(), b->log.end(), out);
+  b->log.clear();
+  return TG_OK;
+}
 
 tg_status tg_batcher_on_patch_arrival(tg_batcher* b, const tg_patch_meta* patch, int32_t src_frame,
                                       int64_t now_us, int32_t* n_events) {

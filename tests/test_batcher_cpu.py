@@ -207,7 +207,9 @@ def our_run(scenes, W, H, profile, bandwidth, zones=(4, 4), canvas=(1024, 1024),
         order_arrivals += arr
     s = A.SloScheduler(A.CanvasSpec(*canvas), A.LatencyProfile(*canvas, profile),
                        A.max_canvases_per_batch(gpu_mem, model, 1.0))
+    s.enable_log("tangram")
     events = s.replay(order_patches, order_arrivals)
+    our_run.log = s.take_log()
     return admitted_all, arrival_of, events
 
 
@@ -234,6 +236,9 @@ def test_multi_camera_stream_matches_reference_simulator(n_cams, W, H, bw, kw):
                e["patch_ids"]) for e in ref["events"]]
     assert ours == theirs
     assert len(ours) > 0
+    # the whole event log (arrival / repack / invoke / timer_set lines),
+    # byte for byte (scheduler_test.cpp:302-320 replays it the same way)
+    assert our_run.log == ref["log"]
 
 
 def test_descriptor_compaction_layout():
