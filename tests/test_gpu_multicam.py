@@ -27,7 +27,9 @@ PROFILE = [(1, 60.0, 3.0), (2, 85.0, 4.0), (4, 135.0, 6.0), (8, 235.0, 10.0)]
 def test_multicam_events_and_canvases_match_reference(ctx, cams, W, H, n, bw, link):
     path = MC.MultiCameraPath(ctx, cams, W, H, n, PROFILE, bandwidth_mbps=bw, per_camera_link=link,
                               trace_kw=dict(roi_proportion_mean=0.15))
+    path.sched.enable_log("tangram")
     desc, n_events, n_canvases = path.step()
+    log = path.sched.take_log()
     ctx.stream_sync(path.stream)
     assert n_events > 0 and n_canvases > 0
     events = path.events()
@@ -47,6 +49,7 @@ def test_multicam_events_and_canvases_match_reference(ctx, cams, W, H, n, bw, li
               e["patch_ids"]) for e in ref["events"]]
         adm_ids = [i for i, a in enumerate(ref["admitted"]) if a]
         assert list(path.arrival) == [ref["arrival_us"][i] for i in adm_ids]
+        assert log == ref["log"]  # the whole scheduler event log, byte for byte
     # canvas bytes: host fill of every event canvas from the same frames
     plan = path._last
     by_id = {int(p["patch_id"]): (int(s), p) for p, s in zip(plan["patches"], plan["src"])}
