@@ -1,5 +1,5 @@
 // k_plan.cu -- per-frame planner (K2 RoI boxes + K3 partition + K4 stitch
-// plan), the frame-order scan, and the drop-in rect-level kernels.
+// plan) with the frame-order prefix, and the drop-in rect-level kernels.
 //
 // One CTA per frame:
 //   K2 (absent from the reference): ccl.cuh -- 8-connected

@@ -21,7 +21,7 @@ cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const*
                               uint32_t* d_raw, uint32_t* d_cells, uint32_t* d_active,
                               uint32_t* d_mask, uint32_t* d_sync, int sms, cudaStream_t stream);
 
-// ---- K2-K4 per-frame planner + scan (k_plan.cu) ----------------------------
+// ---- K2-K4 per-frame planner + frame-order prefix (k_plan.cu) --------------
 struct PlanArgs {
   int n_frames, W, H, X, Y, M, N;
   int cells_x, cells_y, act_words, max_rois, job_cap;
