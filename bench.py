@@ -403,7 +403,11 @@ def cpu_baseline(ring, t_us, n, sample=None):
     threads = os.cpu_count() or 1
     sample = sample or min(n, max(8, min(48, 2 * threads)))
     frames = [ring.download_frame(i) for i in range(sample + 1)]
-    return cpu_measure(frames, t_us[:sample], threads)
+    out = cpu_measure(frames, t_us[:sample], threads)
+    # also one core (a few frames, a few passes)
+    one = cpu_measure(frames[:5], t_us[:4], 1, passes=3)
+    out["single_core_value"] = one["value"]
+    return out
 
 
 def cpu_measure(frames, t_us, threads, passes=None):
