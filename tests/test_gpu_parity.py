@@ -351,6 +351,9 @@ def test_round_trip_fixture(ctx):
     dict(W=640, H=352, n=3, pitch=640 * 3 + 64),       # padded rows
     dict(W=8192, H=48, n=3),                           # 4 K1 parts per row, 2 rows per item
     dict(W=2080, H=70, n=5),                           # 65 words: two uneven K1 parts
+    dict(W=5008, H=40, n=3),                           # 5 K1 parts: 3 of 8 groups idle
+    dict(W=16, H=8, n=4),                              # half a word, one partial cell row
+    dict(W=32, H=3000, n=2),                           # tall: 750 row blocks, 47 K1b strips
     dict(W=1920, H=1080, n=6, trace_kw=dict(roi_proportion_mean=0.59, roi_max_dim=1080,
                                             roi_count_max=30)),  # dense, oversize patches
 ])
