@@ -1,6 +1,7 @@
 """Times the mask stage of the cfg2 workload three ways on one GPU: the
 fused launch (K1 + K1b tasks, tg_pipeline_stage_mask), K1 alone
-(tg_pipeline_stage_mask_fg) and K1b alone (tg_pipeline_stage_mask_cells).
+(tg_pipeline_stage_mask_fg), K1b alone (tg_pipeline_stage_mask_cells) and
+the two back to back ("split").
 Tuning aid; CUDA events on the launching stream, mean of N launches."""
 import sys
 
@@ -24,7 +25,8 @@ calls = {
     "k1": lambda: A.check(lib.tg_pipeline_stage_mask_fg(pipe.handle, n, d_cur, d_prev, st)),
     "k1b": lambda: A.check(lib.tg_pipeline_stage_mask_cells(pipe.handle, n, st)),
 }
-which = sys.argv[2].split(",") if len(sys.argv) > 2 else list(calls)
+calls["split"] = lambda: (calls["k1"](), calls["k1b"]())
+which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["fused", "k1", "k1b"]
 for name, fn in [(k, calls[k]) for k in which] * 2:
     for _ in range(3):
         fn()
