@@ -490,6 +490,29 @@ def test_gather_repeats_and_rewrites_every_byte(ctx):
     run.close()
 
 
+@pytest.mark.parametrize("keep", [True, False])
+def test_two_launch_mask_path_stage_by_stage(ctx, keep):
+    """The mask stage as two launches (K1 tg_pipeline_stage_mask_fg, then
+    K1b tg_pipeline_stage_mask_cells: the fallback tg_pipeline_stage_mask
+    takes when the cooperative launch cannot be co-scheduled), followed by
+    the plan and gather stages called one by one: bit-exact like the fused
+    tg_pipeline_run."""
+    from paper_2404_09267_b200 import _native as N
+    lib = N.lib()
+    run = GpuRun(ctx, 1920, 1080, 9, seed=1006, keep_mask=keep,
+                 trace_kw=dict(roi_proportion_mean=0.2))
+    ctx.memset(run.d_canvases, 0x5A, run.canvas_bytes * run.max_canvases)
+    A.check(lib.tg_pipeline_stage_mask_fg(run.pipe.handle, run.n, run.d_cur, run.d_prev, None))
+    A.check(lib.tg_pipeline_stage_mask_cells(run.pipe.handle, run.n, None))
+    A.check(lib.tg_pipeline_stage_plan(run.pipe.handle, run.n, run.d_ids, run.d_gen,
+                                       run.first_patch_id, None))
+    A.check(lib.tg_pipeline_stage_gather(run.pipe.handle, run.n, run.d_cur, run.d_canvases, None))
+    run.ctx.stream_sync()
+    run.res = run.pipe.results(run.n)
+    _compare_full(run, run.res, run.oracle())
+    run.close()
+
+
 def test_c07_granularity_on_device_partition(ctx):
     """acceptance_test.cpp:310-347 with the device partition (drop-in
     tg_partition): finer zone grids transmit no more bytes; and every frame's
