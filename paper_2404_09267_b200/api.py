@@ -779,6 +779,27 @@ class SloScheduler:
         check(N.lib().tg_batcher_replay(self.handle, arr, src, arv, n, C.byref(cnt)))
         return self._events(cnt.value)
 
+    def replay_links(self, camera_patches: Sequence[Sequence[PatchMeta]], bandwidth_mbps: float,
+                     per_camera_link: bool = True) -> tuple[list[InvokeEvent], list[int]]:
+        """Multi-camera front end (sim.hpp:274-290) + the event loop: each
+        camera's admitted patches, in generation order, delivered over one
+        FIFO uplink per camera (or one shared link).  Returns the events and
+        each patch's arrival time (camera-major order)."""
+        flat = [p for cam in camera_patches for p in cam]
+        n = len(flat)
+        offs = [0]
+        for cam in camera_patches:
+            offs.append(offs[-1] + len(cam))
+        c_offs = (C.c_int32 * len(offs))(*offs)
+        arr = (N.tg_patch_meta * max(1, n))(*[_c_patch(p) for p in flat])
+        src = (C.c_int32 * max(1, n))(*([-1] * n))
+        arv = (C.c_int64 * max(1, n))()
+        cnt = C.c_int32()
+        check(N.lib().tg_batcher_replay_links(self.handle, len(camera_patches), c_offs, arr, src,
+                                              float(bandwidth_mbps), int(bool(per_camera_link)),
+                                              arv, C.byref(cnt)))
+        return self._events(cnt.value), list(arv[:n])
+
     def gather(self, ctx: Context, event_index: int, d_frames: int, pitch: int, d_canvases: int,
                stream=None) -> None:
         """Writes event `event_index` (of the last call) into d_canvases."""

@@ -241,6 +241,41 @@ def test_multi_camera_stream_matches_reference_simulator(n_cams, W, H, bw, kw):
     assert our_run.log == ref["log"]
 
 
+@need_ref
+@pytest.mark.parametrize("per_camera_link", [True, False])
+def test_replay_links_matches_reference_simulator(per_camera_link):
+    """tg_batcher_replay_links (the link model of sim.hpp:274-290 + the event
+    loop in one call): per-camera FIFO uplinks and the single shared link
+    sorted by (generation time, patch id), against tangram::run."""
+    W, H, bw = 1920, 1080, 30.0
+    scenes = scenes_for(4, 20, W, H, roi_proportion_mean=0.2)
+    ref = O.run_tangram(scenes, W, H, SIM_PROFILE, bandwidth_mbps=bw,
+                        per_scene_link=per_camera_link)
+    first, cams = 0, []
+    for t_us, frames in scenes:
+        adm = []
+        for i, rois in enumerate(frames):
+            patches = O.partition(i, W, H, t_us[i], 1_000_000, 4, 4, rois, 1.5, first)
+            first += len(patches)
+            adm += [A.PatchMeta(p["patch_id"], p["source_frame_id"], A.Rect(*p["rect"]),
+                                p["generation_time_us"], p["slo_us"], p["deadline_us"], p["size_bytes"])
+                    for p in patches if p["rect"][2] <= 1024 and p["rect"][3] <= 1024]
+        cams.append(adm)
+    s = A.SloScheduler(A.CanvasSpec(1024, 1024), A.LatencyProfile(1024, 1024, SIM_PROFILE),
+                       A.max_canvases_per_batch(6.0, 2.0, 1.0))
+    s.enable_log("tangram")
+    events, arrivals = s.replay_links(cams, bw, per_camera_link)
+    flat = [p for cam in cams for p in cam]
+    for p, a in zip(flat, arrivals):
+        assert ref["arrival_us"][p.patch_id] == a
+    ours = [(e.fire_time_us, {"deadline_timer": 0, "infeasible_arrival": 1, "memory_cap": 2}[e.trigger],
+             e.batch_size, e.estimated_slack_us, e.patch_ids) for e in events]
+    theirs = [(e["fire_time_us"], e["trigger"], e["batch_size"], e["estimated_slack_us"],
+               e["patch_ids"]) for e in ref["events"]]
+    assert ours == theirs and len(ours) > 0
+    assert s.take_log() == ref["log"]
+
+
 def test_descriptor_compaction_layout():
     """tg_descriptors_compact: pipeline slots [F][Z] -> camera-major records."""
     import ctypes as C

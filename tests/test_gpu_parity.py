@@ -513,6 +513,65 @@ def test_two_launch_mask_path_stage_by_stage(ctx, keep):
     run.close()
 
 
+def test_stitch_gather_explicit_plan(ctx):
+    """tg_stitch_gather (A13 on a caller-built plan): the oracle's stitch of
+    patches cut from several frames -> placement jobs + zero jobs for the
+    final free rects; every canvas byte equals the SURVEY A13 fill
+    canvas[py+v][(px+u)*3+c] = frame[ry+v][(rx+u)*3+c], uncovered = 0,
+    over canvases pre-filled with garbage.  Malformed plans fail loudly."""
+    import ctypes as C
+
+    from paper_2404_09267_b200 import _native as N
+    W, H, n, M, Nh = 640, 360, 4, 300, 200
+    run = GpuRun(ctx, W, H, n, seed=1007, trace_kw=dict(roi_max_dim=200))
+    frames = run.host_frames()
+    rng = O.Rng(O.derive_seed(1007, "stitch-gather"))
+    src = {}
+    queue = []
+    for pid in range(40):
+        w, h = rng.uniform_int(1, M), rng.uniform_int(1, Nh)
+        f = rng.uniform_int(0, n - 1)
+        src[pid] = (f, rng.uniform_int(0, W - w), rng.uniform_int(0, H - h))
+        queue.append((pid, w, h))
+    pl, nc, free = O.stitch_all(queue, M, Nh)
+    jobs, offs = [], [0]
+    for c in range(nc):
+        for pid, ci, x, y, w, h in pl:
+            if ci == c:
+                f, rx, ry = src[pid]
+                jobs.append(N.tg_gather_job(N.tg_rect(x, y, w, h), f, rx, ry))
+        for ci, x, y, w, h in free:
+            if ci == c:
+                jobs.append(N.tg_gather_job(N.tg_rect(x, y, w, h), -1, 0, 0))
+        offs.append(len(jobs))
+    want = np.zeros((nc, Nh, M * 3), np.uint8)
+    for pid, ci, x, y, w, h in pl:
+        f, rx, ry = src[pid]
+        want[ci, y:y + h, 3 * x:3 * (x + w)] = frames[f + 1][ry:ry + h, 3 * rx:3 * (rx + w)]
+    cbytes = M * Nh * 3
+    d_canv = ctx.malloc(cbytes * nc)
+    ctx.memset(d_canv, 0xC3, cbytes * nc)
+    c_jobs = (N.tg_gather_job * len(jobs))(*jobs)
+    c_offs = (C.c_int32 * len(offs))(*offs)
+    spec = N.tg_canvas_spec(M, Nh, 1.0)
+    A.check(N.lib().tg_stitch_gather(ctx.handle, c_jobs, len(jobs), c_offs, nc, spec, run.d_cur,
+                                     run.ring.pitch, d_canv, None))
+    ctx.stream_sync()
+    got = ctx.download(d_canv, (nc, Nh, M * 3), np.uint8)
+    assert nc >= 2
+    for k in range(nc):
+        assert np.array_equal(got[k], want[k]), f"canvas {k}"
+    bad = (C.c_int32 * 2)(0, len(jobs) + 1)
+    with pytest.raises(A.InvalidArgument, match="bad job offsets"):
+        A.check(N.lib().tg_stitch_gather(ctx.handle, c_jobs, len(jobs), bad, 1, spec, run.d_cur,
+                                         run.ring.pitch, d_canv, None))
+    with pytest.raises(A.InvalidArgument, match="pitch must be a multiple of 16"):
+        A.check(N.lib().tg_stitch_gather(ctx.handle, c_jobs, len(jobs), c_offs, nc, spec, run.d_cur,
+                                         run.ring.pitch + 8, d_canv, None))
+    ctx.free(d_canv)
+    run.close()
+
+
 def test_c07_granularity_on_device_partition(ctx):
     """acceptance_test.cpp:310-347 with the device partition (drop-in
     tg_partition): finer zone grids transmit no more bytes; and every frame's
