@@ -134,6 +134,12 @@ __device__ int block_exclusive_scan(int* v, int n, int* warp_tmp) {
   return carry;
 }
 
+#ifdef TG_PLAN_PHASES  // diagnostics build: per-phase clock64 marks of thread 0
+#define TG_PH(i) do { if (threadIdx.x == 0) tg_ph_mark[i] = clock64(); } while (0)
+#else
+#define TG_PH(i) do { } while (0)
+#endif
+
 constexpr int kHeadsPerWord = 16;  // run heads in a 32-cell activity word
 
 struct CclSmem {
@@ -154,11 +160,16 @@ __device__ __forceinline__ int head_slot(const uint32_t* row, int wi, int word, 
 // pixel bounds), ranked by root cell.  Latches kErrRoiCapacity and clamps.
 __device__ int ccl_frame(const uint32_t* gact, const uint32_t* gcells, int cx_n, int cy_n,
                          int max_rois, const CclSmem& s, int* warp_tmp, int* s_n, DevError* err,
-                         int frame) {
+                         int frame
+#ifdef TG_PLAN_PHASES
+                         , long long* tg_ph_mark
+#endif
+                         ) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int aw = ceil_div(cx_n, 32), ncw = cy_n * aw;
   for (int i = tid; i < ncw; i += nt) s.act[i] = gact[i];
   __syncthreads();
+  TG_PH(1);
   // labels of run heads
   for (int i = tid; i < ncw; i += nt) {
     const int cy = i / aw, wi = i - cy * aw;
@@ -166,6 +177,7 @@ __device__ int ccl_frame(const uint32_t* gact, const uint32_t* gcells, int cx_n,
     for (int k = 0; k < nh; ++k) s.L[i * kHeadsPerWord + k] = static_cast<uint16_t>(i * kHeadsPerWord + k);
   }
   __syncthreads();
+  TG_PH(2);
   // unions between each run and the runs it touches in the row above
   for (int i = tid; i < ncw; i += nt) {
     const int cy = i / aw, wi = i - cy * aw;
@@ -195,6 +207,7 @@ __device__ int ccl_frame(const uint32_t* gact, const uint32_t* gcells, int cx_n,
     }
   }
   __syncthreads();
+  TG_PH(3);
   // roots, and every head's label compressed to its root in the same pass:
   // the unions are over, so a stored root is final and concurrent finds
   // through this slot just arrive sooner
@@ -212,6 +225,7 @@ __device__ int ccl_frame(const uint32_t* gact, const uint32_t* gcells, int cx_n,
     s.wpre[i] = __popc(roots);
   }
   __syncthreads();
+  TG_PH(4);
   const int ncomp = block_exclusive_scan(s.wpre, ncw, warp_tmp);
   if (tid == 0) {
     s.wpre[ncw] = ncomp;
@@ -231,6 +245,7 @@ __device__ int ccl_frame(const uint32_t* gact, const uint32_t* gcells, int cx_n,
     s.by1[r] = INT_MIN;
   }
   __syncthreads();
+  TG_PH(5);
   // Boxes.  x: every run's end cells.  y: only the component's top cell row
   // (its root's row) can hold the box's top pixel and only its bottom row the
   // bottom one, so just those runs scan their cells' y extents.  Pass 1 also
@@ -283,6 +298,7 @@ __device__ int ccl_frame(const uint32_t* gact, const uint32_t* gcells, int cx_n,
       }
     }
     __syncthreads();
+    TG_PH(6 + pass);
   }
   __syncthreads();
   return nr;

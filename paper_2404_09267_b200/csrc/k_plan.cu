@@ -139,6 +139,10 @@ struct PlanTail {
   Job sjobs[3 * kMaxZones];
 };
 
+#ifdef TG_PLAN_PHASES
+__device__ unsigned long long g_plan_phase[16];
+#endif
+
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ ZoneAcc zacc;
@@ -169,6 +173,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     return;
   }
   const int f = s_f;
+#ifdef TG_PLAN_PHASES
+  __shared__ long long tg_ph_mark[16];
+  TG_PH(0);
+#endif
   const int cx_n = a.cells_x, cy_n = a.cells_y, aw = a.act_words, ncw = cy_n * aw;
   CclSmem cs;
   cs.act = reinterpret_cast<uint32_t*>(dsm);
@@ -183,7 +191,11 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   // ---- K2: RoI boxes ---------------------------------------------------------
   const int nr = ccl_frame(a.active + static_cast<size_t>(f) * ncw,
                            a.cells + static_cast<size_t>(f) * cy_n * cx_n, cx_n, cy_n, a.max_rois,
-                           cs, warp_tmp, &s_nrois, a.err, f);
+                           cs, warp_tmp, &s_nrois, a.err, f
+#ifdef TG_PLAN_PHASES
+                           , tg_ph_mark
+#endif
+                           );
   tg_rect* frois = a.rois + static_cast<size_t>(f) * a.max_rois;
   for (int r = tid; r < nr; r += nt)
     frois[r] = tg_rect{cs.bx0[r], cs.by0[r], cs.bx1[r] - cs.bx0[r] + 1, cs.by1[r] - cs.by0[r] + 1};
@@ -195,6 +207,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   // ---- K3: partition (Alg. 1) --------------------------------------------
   partition_accumulate(frois, nr, a.W, a.H, a.X, a.Y, zacc, a.err, f, nullptr, tid, nt);
   __syncthreads();
+  TG_PH(8);
   if (tid >= 32) return;
   const int lane = tid;
   const int np = partition_emit(zacc, nz, a.frame_ids[f], a.gen_us[f], a.slo_us, a.bpp, 0, spatch,
@@ -221,6 +234,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   }
   for (int j = np + lane; j < nz; j += 32) a.admitted[static_cast<size_t>(f) * nz + j] = 0;
   __syncwarp();
+  TG_PH(9);
 
   // ---- K4: stitch plan (Alg. 2 solver) -------------------------------------
   int nfree = 0;
@@ -233,6 +247,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     a.n_placements[f] = na;
     a.n_canvases[f] = nc < 0 ? 0 : nc;
   }
+  TG_PH(10);
   const int ncv = nc < 0 ? 0 : nc;
   look_publish(a, f, s_epoch, static_cast<uint64_t>(np), static_cast<uint64_t>(ncv), lane);
   // Gather jobs (frame-local): placements and free rects grouped by canvas,
@@ -275,10 +290,12 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
       pos += cnt;
     }
   }
+  TG_PH(11);
   // frame-order prefix: global patch ids, canvas numbering
   uint64_t ex_p, ex_c;
   look_back(a, f, s_epoch, static_cast<uint64_t>(np), static_cast<uint64_t>(ncv), &ex_p, &ex_c,
             lane);
+  TG_PH(12);
   const uint64_t id0 = s_first + ex_p;
   const long long cb = static_cast<long long>(ex_c);
   for (int j = lane; j < np; j += 32) a.patches[static_cast<size_t>(f) * nz + j].patch_id = id0 + j;
@@ -302,6 +319,14 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     p.reserved = 0;
     fpl[k] = p;
   }
+#ifdef TG_PLAN_PHASES
+  TG_PH(13);
+  if (lane == 0) {
+    for (int i = 1; i < 14; ++i)
+      atomicAdd(&g_plan_phase[i], static_cast<unsigned long long>(tg_ph_mark[i] - tg_ph_mark[i - 1]));
+    atomicAdd(&g_plan_phase[0], 1ull);
+  }
+#endif
   if (lane == 0) {  // the last CTA out resets the ticket and moves the epoch on
     __threadfence();
     if (atomicAdd(&a.psync[1], 1u) == static_cast<uint32_t>(a.n_frames) - 1) {
@@ -404,3 +429,13 @@ cudaError_t launch_stitch_batch(const StitchBatchArgs& a, cudaStream_t stream) {
 }
 
 }  // namespace tg
+
+#ifdef TG_PLAN_PHASES
+// Diagnostics build only: phase cycle sums of thread 0 over all frame CTAs
+// since the last call (out[0] = CTA count); resets them.
+extern "C" int tg_debug_plan_phases(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, tg::g_plan_phase, sizeof(unsigned long long) * 16);
+  unsigned long long z[16] = {};
+  return static_cast<int>(cudaMemcpyToSymbol(tg::g_plan_phase, z, sizeof(z)));
+}
+#endif
