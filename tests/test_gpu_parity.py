@@ -432,6 +432,45 @@ def test_pipeline_capacity_errors(ctx):
     run.close()
 
 
+def test_pipeline_argument_validation(ctx):
+    """tg_pipeline_create and the stages reject bad geometry / capacities
+    with tg_last_error messages (no device work is launched), and the
+    context stays usable."""
+    from paper_2404_09267_b200 import _native as N
+    bad = [
+        (dict(W=100, H=64), "multiple of 16"),
+        (dict(W=8208, H=64), "multiple of 16"),
+        (dict(W=640, H=0), "multiple of 16"),
+        (dict(W=640, H=70000), "height must be <= 65535"),
+        (dict(W=640, H=64, pitch=640 * 3 - 16), "pitch"),
+        (dict(W=640, H=64, pitch=640 * 3 + 8), "pitch"),
+        (dict(W=640, H=64, threshold=256), "threshold"),
+        (dict(W=640, H=64, dilate_radius=9), "dilate radius"),
+        (dict(W=640, H=32, zones=(1, 40)), "zone grid finer than frame"),
+        (dict(W=640, H=64, zones=(13, 5)), "device limit"),
+        (dict(W=640, H=64, canvas=(0, 1024)), "canvas dimensions"),
+        (dict(W=640, H=64, max_frames=0), "capacities"),
+        (dict(W=8192, H=2064), "more than 65535"),
+        (dict(W=640, H=64, max_rois_per_frame=100000), "max_rois_per_frame too large"),
+        (dict(W=640, H=64, max_frames=600000), "below 2\\^23"),
+    ]
+    for kw, msg in bad:
+        kw = dict(kw)
+        W, H = kw.pop("W"), kw.pop("H")
+        kw.setdefault("max_frames", 2)
+        with pytest.raises(A.InvalidArgument, match=msg):
+            A.Pipeline(ctx, W, H, **kw)
+    run = GpuRun(ctx, 640, 64, 2, seed=5, trace_kw=dict(roi_max_dim=60))
+    lib = N.lib()
+    with pytest.raises(A.InvalidArgument, match="n_frames must be in"):
+        A.check(lib.tg_pipeline_stage_mask(run.pipe.handle, 3, run.d_cur, run.d_prev, None))
+    with pytest.raises(A.InvalidArgument, match="null frame pointer table"):
+        A.check(lib.tg_pipeline_stage_mask(run.pipe.handle, 2, None, None, None))
+    gpu = run.run()  # still fine afterwards
+    _compare_full(run, gpu, run.oracle())
+    run.close()
+
+
 def test_pipeline_graph_replay_and_patch_id_base(ctx):
     run = GpuRun(ctx, 1920, 1080, 8, seed=3, first_patch_id=1000)
     gpu = run.run()
