@@ -101,37 +101,41 @@ __device__ __forceinline__ uint32_t run_heads(const uint32_t* row, int wi) {
   return w & ~((w << 1) | carry);
 }
 
-// Block-wide exclusive scan of n ints in place; returns the total.
+// Block-wide exclusive scan of n ints in place; returns the total.  One
+// pass: thread t owns the contiguous chunk [t*k, t*k + k), k = ceil(n / nt),
+// so the block needs two barriers however large n is (ncw = 1,080 words at
+// 4K: 3 per thread).
 __device__ int block_exclusive_scan(int* v, int n, int* warp_tmp) {
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
-  int carry = 0;
-  for (int base = 0; base < n; base += nt) {
-    const int i = base + tid;
-    const int x = i < n ? v[i] : 0;
-    int s = x;
+  const int k = (n + nt - 1) / nt;
+  const int i0 = min(n, tid * k), i1 = min(n, i0 + k);
+  int own = 0;
+  for (int i = i0; i < i1; ++i) own += v[i];
+  int s = own;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, s, o);
+    if (lane >= o) s += y;
+  }
+  if (lane == 31) warp_tmp[wid] = s;
+  __syncthreads();
+  if (wid == 0) {
+    int t = lane < nt / 32 ? warp_tmp[lane] : 0;
     for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += y;
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
     }
-    if (lane == 31) warp_tmp[wid] = s;
-    __syncthreads();
-    if (wid == 0) {
-      int t = lane < nt / 32 ? warp_tmp[lane] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, t, o);
-        if (lane >= o) t += y;
-      }
-      warp_tmp[lane] = t;
-    }
-    __syncthreads();
-    const int before = (wid ? warp_tmp[wid - 1] : 0) + s - x;
-    const int total = warp_tmp[nt / 32 - 1];
-    __syncthreads();
-    if (i < n) v[i] = carry + before;
-    carry += total;
+    warp_tmp[lane] = t;
   }
   __syncthreads();
-  return carry;
+  int run = (wid ? warp_tmp[wid - 1] : 0) + s - own;
+  const int total = warp_tmp[nt / 32 - 1];
+  for (int i = i0; i < i1; ++i) {
+    const int x = v[i];
+    v[i] = run;
+    run += x;
+  }
+  __syncthreads();
+  return total;
 }
 
 #ifdef TG_PLAN_PHASES  // diagnostics build: per-phase clock64 marks of thread 0
