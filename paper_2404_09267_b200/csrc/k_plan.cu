@@ -188,6 +188,9 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   cs.by1 = cs.bx1 + a.max_rois;
   cs.L = reinterpret_cast<uint16_t*>(cs.by1 + a.max_rois);
 
+  const int nz = a.X * a.Y;
+  zone_acc_init(zacc, nz, tid, nt);  // ordered before K3 by the CCL's barriers
+
   // ---- K2: RoI boxes ---------------------------------------------------------
   const int nr = ccl_frame(a.active + static_cast<size_t>(f) * ncw,
                            a.cells + static_cast<size_t>(f) * cy_n * cx_n, cx_n, cy_n, a.max_rois,
@@ -197,15 +200,15 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
 #endif
                            );
   tg_rect* frois = a.rois + static_cast<size_t>(f) * a.max_rois;
-  for (int r = tid; r < nr; r += nt)
-    frois[r] = tg_rect{cs.bx0[r], cs.by0[r], cs.bx1[r] - cs.bx0[r] + 1, cs.by1[r] - cs.by0[r] + 1};
-  const int nz = a.X * a.Y;
-  zone_acc_init(zacc, nz, tid, nt);
+  auto box = [&cs](int r) {
+    return tg_rect{cs.bx0[r], cs.by0[r], cs.bx1[r] - cs.bx0[r] + 1, cs.by1[r] - cs.by0[r] + 1};
+  };
+  for (int r = tid; r < nr; r += nt) frois[r] = box(r);
   if (tid == 0) a.n_rois[f] = nr;
-  __syncthreads();
 
   // ---- K3: partition (Alg. 1) --------------------------------------------
-  partition_accumulate(frois, nr, a.W, a.H, a.X, a.Y, zacc, a.err, f, nullptr, tid, nt);
+  // straight from the CCL's shared-memory boxes (final after its last barrier)
+  partition_accumulate_at(box, nr, a.W, a.H, a.X, a.Y, zacc, a.err, f, nullptr, tid, nt);
   __syncthreads();
   TG_PH(8);
   if (tid >= 32) return;

@@ -33,15 +33,24 @@ __device__ __forceinline__ long long overlap_area(const tg_rect& a, const tg_rec
 
 // assign_rois (partition.hpp:93-112): zone of maximum overlap, strict '>'
 // so ties keep the lowest zone index; -1 if the RoI misses the frame.
+// Only the zones in the RoI's column and row span can overlap it (zone c
+// covers [c*zw, (c+1)*zw), the last one up to W), and visiting them in
+// row-major order keeps the reference's tie rule.
 __device__ __forceinline__ int best_zone(const tg_rect& r, int W, int H, int X, int Y) {
+  const int zw = W / X, zh = H / Y;  // >= 1: finer grids are rejected up front
+  const int xe = r.x + r.w - 1, ye = r.y + r.h - 1;
+  const int c0 = r.x <= 0 ? 0 : min(r.x / zw, X - 1), c1 = xe <= 0 ? 0 : min(xe / zw, X - 1);
+  const int r0 = r.y <= 0 ? 0 : min(r.y / zh, Y - 1), r1 = ye <= 0 ? 0 : min(ye / zh, Y - 1);
   long long best = 0;
   int bz = -1;
-  const int nz = X * Y;
-  for (int z = 0; z < nz; ++z) {
-    const long long s = overlap_area(r, zone_rect(z, W, H, X, Y));
-    if (s > best) {
-      best = s;
-      bz = z;
+  for (int row = r0; row <= r1; ++row) {
+    for (int col = c0; col <= c1; ++col) {
+      const int z = row * X + col;
+      const long long s = overlap_area(r, zone_rect(z, W, H, X, Y));
+      if (s > best) {
+        best = s;
+        bz = z;
+      }
     }
   }
   return bz;
@@ -64,12 +73,13 @@ __device__ __forceinline__ void zone_acc_init(ZoneAcc& z, int nz, int tid, int n
 
 // Block-cooperative assignment of n RoIs into the zone accumulators.
 // Returns nothing; an RoI outside the frame latches kErrRoiOutside.
-__device__ __forceinline__ void partition_accumulate(const tg_rect* rois, int n, int W, int H,
-                                                     int X, int Y, ZoneAcc& z, DevError* err,
-                                                     int frame, int* zone_of, int tid,
-                                                     int nthreads) {
+template <class RectAt>
+__device__ __forceinline__ void partition_accumulate_at(RectAt rect_at, int n, int W, int H,
+                                                        int X, int Y, ZoneAcc& z, DevError* err,
+                                                        int frame, int* zone_of, int tid,
+                                                        int nthreads) {
   for (int i = tid; i < n; i += nthreads) {
-    const tg_rect r = rois[i];
+    const tg_rect r = rect_at(i);
     const int bz = best_zone(r, W, H, X, Y);
     if (zone_of) zone_of[i] = bz;
     if (bz < 0) {
@@ -84,6 +94,14 @@ __device__ __forceinline__ void partition_accumulate(const tg_rect* rois, int n,
     atomicMax(&z.y1[bz], r.y + r.h);
     atomicAdd(&z.cnt[bz], 1);
   }
+}
+
+__device__ __forceinline__ void partition_accumulate(const tg_rect* rois, int n, int W, int H,
+                                                     int X, int Y, ZoneAcc& z, DevError* err,
+                                                     int frame, int* zone_of, int tid,
+                                                     int nthreads) {
+  partition_accumulate_at([rois](int i) { return rois[i]; }, n, W, H, X, Y, z, err, frame, zone_of,
+                          tid, nthreads);
 }
 
 // One warp: one patch per non-empty zone in zone order (partition.hpp:
