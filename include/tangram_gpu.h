@@ -255,6 +255,16 @@ typedef struct {
 } tg_pipeline_views;
 tg_status tg_pipeline_device_views(tg_pipeline* p, tg_pipeline_views* out);
 
+/* Which mask-stage path ran (host-side launch counts since creation): the
+ * fused cooperative K1 + K1b launch, or its two-launch fallback when the
+ * device cannot co-schedule one K1 CTA per SM (e.g. a shared GPU).  Graph
+ * replays are not counted (the capture is). */
+typedef struct {
+  int64_t mask_fused_launches;
+  int64_t mask_split_launches;
+} tg_pipeline_stats;
+tg_status tg_pipeline_get_stats(tg_pipeline* p, tg_pipeline_stats* out);
+
 /* Blocking copies of the last run's results to host (waits on `stream`,
  * then reports latched device errors). */
 tg_status tg_pipeline_download(tg_pipeline* p, int32_t n_frames, void* stream,

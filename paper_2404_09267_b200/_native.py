@@ -70,6 +70,10 @@ class tg_pipeline_views(C.Structure):
                 ("mask_words", C.c_int32)]
 
 
+class tg_pipeline_stats(C.Structure):
+    _fields_ = [("mask_fused_launches", C.c_int64), ("mask_split_launches", C.c_int64)]
+
+
 class tg_workload_config(C.Structure):
     _fields_ = [("n_frames", C.c_int32), ("fps", C.c_double), ("frame_width", C.c_int32),
                 ("frame_height", C.c_int32), ("roi_proportion_mean", C.c_double),
@@ -155,6 +159,7 @@ SIGNATURES = {
     "tg_graph_launch": (st, [vp, vp]),
     "tg_graph_destroy": (None, [vp]),
     "tg_pipeline_device_views": (st, [vp, P(tg_pipeline_views)]),
+    "tg_pipeline_get_stats": (st, [vp, P(tg_pipeline_stats)]),
     "tg_pipeline_download": (st, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, P(i64)]),
     "tg_pipeline_free_rects": (st, [vp, i32, P(tg_free_rect), i32, P(i32)]),
     "tg_stitch_gather": (st, [vp, P(tg_gather_job), i32, P(i32), i32, tg_canvas_spec, vp, i32, vp,

@@ -85,6 +85,7 @@ struct tg_pipeline {
   uint64_t* look = nullptr;   // [F] plan look-back words
   uint32_t* psync = nullptr;  // [3] plan frame ticket, finished CTAs, epoch
   int last_frames = 0;
+  tg_pipeline_stats stats{};
 };
 
 struct tg_graph {
@@ -568,12 +569,6 @@ tg_status tg_stitch_batch(tg_ctx* ctx, int32_t n_queues, int32_t total_patches,
   if (spec.width < 1 || spec.height < 1 || spec.width > 65535 || spec.height > 65535)
     return fail(TG_ERR_INVALID_ARGUMENT, "canvas dimensions must be in [1, 65535]");
   if (n_queues <= 0) return TG_OK;
-  Carver cv;
-  const size_t o_d = cv.take<int32_t>(5 * static_cast<size_t>(std::max(1, total_patches))),
-               o_i = cv.take<uint64_t>(std::max(1, total_patches));
-  void* base;
-  if ((s = scratch(ctx, cv.off, &base))) return s;
-  char* b = static_cast<char*>(base);
   StitchBatchArgs a;
   a.n_queues = n_queues;
   a.M = spec.width;
@@ -584,8 +579,6 @@ tg_status tg_stitch_batch(tg_ctx* ctx, int32_t n_queues, int32_t total_patches,
   a.n_canvases = d_n_canvases;
   a.free_ws = reinterpret_cast<FreeRect*>(d_free_ws);
   a.n_free = d_n_free;
-  a.dims_ws = reinterpret_cast<int32_t*>(b + o_d);
-  a.ids_ws = reinterpret_cast<uint64_t*>(b + o_i);
   a.err = ctx->d_err;
   TG_CUDA(launch_stitch_batch(a, pick(ctx, stream)));
   return TG_OK;
@@ -603,13 +596,11 @@ tg_status tg_stitch_all(tg_ctx* ctx, const tg_patch_meta* queue, int32_t n, tg_c
     if (n_free) *n_free = 0;
     return TG_OK;
   }
-  // Scratch for the stitch itself lives after our own arrays, so carve ours
-  // from a second region: queue, offsets, placements, counts, free list.
+  // Staging for the blocking call: queue, offsets, placements, counts, free list.
   Carver cv;
   const size_t o_q = cv.take<tg_patch_meta>(n), o_off = cv.take<int32_t>(2),
                o_pl = cv.take<tg_placement>(n), o_nc = cv.take<int32_t>(1),
-               o_nf = cv.take<int32_t>(1), o_fr = cv.take<tg_free_rect>(2 * static_cast<size_t>(n) + 1),
-               o_d = cv.take<int32_t>(5 * static_cast<size_t>(n)), o_i = cv.take<uint64_t>(n);
+               o_nf = cv.take<int32_t>(1), o_fr = cv.take<tg_free_rect>(2 * static_cast<size_t>(n) + 1);
   void* base;
   if ((s = scratch(ctx, cv.off, &base))) return s;
   char* b = static_cast<char*>(base);
@@ -627,8 +618,6 @@ tg_status tg_stitch_all(tg_ctx* ctx, const tg_patch_meta* queue, int32_t n, tg_c
   a.n_canvases = reinterpret_cast<int32_t*>(b + o_nc);
   a.free_ws = reinterpret_cast<FreeRect*>(b + o_fr);
   a.n_free = reinterpret_cast<int32_t*>(b + o_nf);
-  a.dims_ws = reinterpret_cast<int32_t*>(b + o_d);
-  a.ids_ws = reinterpret_cast<uint64_t*>(b + o_i);
   a.err = ctx->d_err;
   TG_CUDA(launch_stitch_batch(a, st));
   int32_t nc = 0, nf = 0;
@@ -804,6 +793,7 @@ tg_status tg_pipeline_stage_mask(tg_pipeline* p, int32_t n_frames, const uint8_t
       p->mask_sync, p->ctx->sms, pick(p->ctx, stream));
   if (e == cudaSuccess) {
     p->last_frames = n_frames;
+    if (n_frames > 0) ++p->stats.mask_fused_launches;
     return TG_OK;
   }
   if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported)
@@ -811,6 +801,7 @@ tg_status tg_pipeline_stage_mask(tg_pipeline* p, int32_t n_frames, const uint8_t
   cudaGetLastError();
   s = tg_pipeline_stage_mask_fg(p, n_frames, d_cur, d_prev, stream);
   if (!s) s = tg_pipeline_stage_mask_cells(p, n_frames, stream);
+  if (!s && n_frames > 0) ++p->stats.mask_split_launches;
   return s;
 }
 
@@ -859,6 +850,7 @@ tg_status tg_pipeline_stage_plan(tg_pipeline* p, int32_t n_frames, const uint64_
   a.gather_units = p->gather_units;
   a.id_state = p->id_state;
   a.look = p->look;
+  a.look_cap = p->p.max_frames;
   a.psync = p->psync;
   TG_CUDA(launch_plan(a, st));
   p->last_frames = n_frames;
@@ -963,6 +955,12 @@ tg_status tg_pipeline_device_views(tg_pipeline* p, tg_pipeline_views* v) {
   v->cells_x = p->cells_x;
   v->cells_y = p->cells_y;
   v->mask_words = p->mask_words;
+  return TG_OK;
+}
+
+tg_status tg_pipeline_get_stats(tg_pipeline* p, tg_pipeline_stats* out) {
+  if (!p || !out) return fail(TG_ERR_INVALID_ARGUMENT, "null pipeline or output");
+  *out = p->stats;
   return TG_OK;
 }
 

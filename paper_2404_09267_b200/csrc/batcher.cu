@@ -135,32 +135,35 @@ struct Choice {
 // BSSF over every free rect of every open canvas; ties by canvas, y, x
 // (candidate_better, stitch.hpp:72-81).
 Choice choose(const Packing& st, int w, int h, int M, int N) {
-  // One 64-bit key per candidate, (score, canvas, y, x) from the top 16 bits
-  // down (all < 2^16), so the minimum key is the candidate_better winner;
-  // infeasible rects get ~0.  The scan is a branch-free min; free rects of a
-  // canvas are disjoint, so (canvas, y, x) names the winner, found again in
-  // its canvas's list afterwards.
-  uint64_t best = ~0ull;
+  // One 128-bit key per candidate, (score, canvas, y, x) from the top 32
+  // bits down, so the minimum key is the candidate_better winner for any
+  // canvas count; infeasible rects get all ones.  The scan is a branch-free
+  // min; free rects of a canvas are disjoint, so (canvas, y, x) names the
+  // winner, found again in its canvas's list afterwards.
+  using u128 = unsigned __int128;
+  const u128 none = ~static_cast<u128>(0);
+  u128 best = none;
   for (int ci = 0; ci < static_cast<int>(st.canvases.size()); ++ci) {
     const uint32_t bd = st.bound[ci];
     if (static_cast<int>(bd >> 16) < w || static_cast<int>(bd & 0xffff) < h) continue;
     const tg_rect* fr = st.canvases[ci].free.data();
     const int nf = static_cast<int>(st.canvases[ci].free.size());
-    const uint64_t cbits = static_cast<uint64_t>(ci) << 32;
+    const u128 cbits = static_cast<u128>(static_cast<uint32_t>(ci)) << 64;
     for (int fi = 0; fi < nf; ++fi) {
       const tg_rect c = fr[fi];
       const int dw = c.w - w, dh = c.h - h;
       // all ones when the patch does not fit (dw or dh negative): no branch
-      const uint64_t bad = static_cast<uint64_t>(static_cast<int64_t>(dw | dh) >> 63);
-      const uint64_t s = static_cast<uint64_t>(static_cast<uint32_t>(dw < dh ? dw : dh));
-      const uint64_t key = (s << 48 | cbits | static_cast<uint64_t>(c.y) << 16 |
-                            static_cast<uint64_t>(c.x)) | bad;
+      const u128 bad = static_cast<u128>(static_cast<__int128>(static_cast<int64_t>(dw | dh) >> 63));
+      const u128 s = static_cast<u128>(static_cast<uint32_t>(dw < dh ? dw : dh));
+      const u128 key = (s << 96 | cbits | static_cast<u128>(static_cast<uint32_t>(c.y)) << 32 |
+                        static_cast<u128>(static_cast<uint32_t>(c.x))) | bad;
       best = key < best ? key : best;
     }
   }
-  if (best == ~0ull) return Choice{static_cast<int>(st.canvases.size()), -1, tg_rect{0, 0, M, N}};
-  const int ci = static_cast<int>(best >> 32 & 0xffff);
-  const int by = static_cast<int>(best >> 16 & 0xffff), bx = static_cast<int>(best & 0xffff);
+  if (best == none) return Choice{static_cast<int>(st.canvases.size()), -1, tg_rect{0, 0, M, N}};
+  const int ci = static_cast<int>(static_cast<uint32_t>(best >> 64));
+  const int by = static_cast<int>(static_cast<uint32_t>(best >> 32));
+  const int bx = static_cast<int>(static_cast<uint32_t>(best));
   const auto& fr = st.canvases[ci].free;
   int fi = 0;
   while (fr[fi].x != bx || fr[fi].y != by) ++fi;

@@ -1,7 +1,9 @@
 // common.cuh -- shared device helpers for the sm_100a Tangram kernels.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "tangram_gpu.h"
@@ -136,5 +138,46 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long k)
 }
 
 __host__ __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// ---- once-only launch setup (host) -------------------------------------------
+// Launchers run every step, so the runtime calls that only configure a kernel
+// (dynamic smem opt-in, occupancy) are made once per device and kernel, and
+// tuning overrides are read from the environment once per process.
+constexpr int kMaxDevices = 64;
+
+// Unset (or unparsable): -1.  Read once; later calls return the cached value.
+struct EnvInt {
+  const char* name;
+  std::atomic<int> state{0};  // 0 unread, 1 read
+  int value = -1;
+  int get() {
+    if (state.load(std::memory_order_acquire) == 0) {
+      const char* e = std::getenv(name);
+      value = e ? std::atoi(e) : -1;
+      state.store(1, std::memory_order_release);
+    }
+    return value;
+  }
+};
+
+// Per-device high-water mark of the dynamic smem a kernel was opted into.
+struct SmemOptIn {
+  std::atomic<int> bytes[kMaxDevices] = {};
+  template <class K>
+  cudaError_t ensure(K* kernel, int smem) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < kMaxDevices && bytes[dev].load(std::memory_order_relaxed) >= smem)
+      return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess && dev >= 0 && dev < kMaxDevices) {
+      int cur = bytes[dev].load(std::memory_order_relaxed);
+      while (cur < smem && !bytes[dev].compare_exchange_weak(cur, smem)) {
+      }
+    }
+    return e;
+  }
+};
 
 }  // namespace tg

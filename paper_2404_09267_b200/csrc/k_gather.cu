@@ -464,18 +464,23 @@ __global__ void __launch_bounds__(kGatherThreads, TG_GATHER_MIN_BLOCKS) gather_k
 }
 
 cudaError_t launch_gather(const GatherArgs& a, int sms, cudaStream_t stream) {
-  static int blocks_per_sm = 0;
-  if (blocks_per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kGatherSmem));
+  // resident CTAs per SM, per device (0 = not yet queried)
+  static std::atomic<int> blocks_per_sm[kMaxDevices] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  int nb = (dev >= 0 && dev < kMaxDevices) ? blocks_per_sm[dev].load(std::memory_order_relaxed) : 0;
+  if (nb == 0) {
+    e = cudaFuncSetAttribute(gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kGatherSmem));
     if (e != cudaSuccess) return e;
-    int nb = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gather_kernel, kGatherThreads,
                                                       kGatherSmem);
     if (e != cudaSuccess) return e;
-    blocks_per_sm = nb > 0 ? nb : 1;
+    nb = nb > 0 ? nb : 1;
+    if (dev >= 0 && dev < kMaxDevices) blocks_per_sm[dev].store(nb, std::memory_order_relaxed);
   }
-  gather_kernel<<<sms * blocks_per_sm, kGatherThreads, kGatherSmem, stream>>>(a);
+  gather_kernel<<<sms * nb, kGatherThreads, kGatherSmem, stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -483,9 +483,14 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
 }
 
 // ---- host launcher ---------------------------------------------------------
-static int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::atoi(e) : dflt;
+// Tuning overrides (probes only), read once per process.
+static EnvInt g_env_slots{"TG_K1_SLOTS"}, g_env_runs{"TG_K1_RUNS"}, g_env_grid{"TG_K1_GRID"},
+    g_env_dctas{"TG_K1_DCTAS"};
+static SmemOptIn g_k1_smem[2];
+
+static int env_or(EnvInt& e, int dflt) {
+  const int v = e.get();
+  return v >= 0 ? v : dflt;
 }
 
 static DilateArgs dilate_args(const uint32_t* d_raw, int W, int H, uint32_t* d_cells,
@@ -525,10 +530,10 @@ static cudaError_t plan_k1(MaskArgs& a, const uint8_t* const* d_cur, const uint8
   a.nrb = ceil_div(H, a.rows_per_item);
   a.slot_bytes = (a.part_words * 96 + 127) & ~127;
   a.nslots = std::min(kK1MaxSlots, (kK1SmemBudget - 1024) / (kK1Groups * (a.slot_bytes + 16)));
-  a.nslots = std::max(2, std::min(a.nslots, env_int("TG_K1_SLOTS", a.nslots)));
+  a.nslots = std::max(2, std::min(a.nslots, env_or(g_env_slots, a.nslots)));
   // frame runs: enough items to balance the SMs
   int ntg = std::max(1, std::min(n_frames, ceil_div(8 * sms, a.nrb)));
-  ntg = std::max(1, std::min(n_frames, env_int("TG_K1_RUNS", ntg)));
+  ntg = std::max(1, std::min(n_frames, env_or(g_env_runs, ntg)));
   a.kf = ceil_div(n_frames, ntg);
   a.ntg = ceil_div(n_frames, a.kf);
   a.total_items = a.ntg * a.nrb;
@@ -536,8 +541,8 @@ static cudaError_t plan_k1(MaskArgs& a, const uint8_t* const* d_cur, const uint8
   *smem = static_cast<size_t>(kK1Groups) * a.nslots * (a.slot_bytes + 16);
   if (*smem > static_cast<size_t>(kK1SmemBudget)) return cudaErrorInvalidConfiguration;
   const bool low = threshold <= 127;
-  return cudaFuncSetAttribute(low ? mask_fg_kernel<true> : mask_fg_kernel<false>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(*smem));
+  return low ? g_k1_smem[1].ensure(mask_fg_kernel<true>, static_cast<int>(*smem))
+             : g_k1_smem[0].ensure(mask_fg_kernel<false>, static_cast<int>(*smem));
 }
 
 cudaError_t launch_mask_fg(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
@@ -549,7 +554,7 @@ cudaError_t launch_mask_fg(const uint8_t* const* d_cur, const uint8_t* const* d_
   cudaError_t e = plan_k1(a, d_cur, d_prev, n_frames, W, H, pitch, threshold, d_raw, sms, &smem);
   if (e != cudaSuccess) return e;
   int grid = std::min(a.total_items, sms);
-  grid = std::max(1, std::min(a.total_items, env_int("TG_K1_GRID", grid)));
+  grid = std::max(1, std::min(a.total_items, env_or(g_env_grid, grid)));
   if (threshold <= 127)
     mask_fg_kernel<true><<<grid, kK1Threads, smem, stream>>>(a);
   else
@@ -598,7 +603,7 @@ cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const*
   const int reserve = (sms * 9 + 50) / 100;
   const int per_cta = ceil_div(a.total_items, std::max(1, sms - reserve));
   const int streaming = ceil_div(a.total_items, per_cta);
-  a.dctas = std::max(0, std::min(sms - 1, env_int("TG_K1_DCTAS", sms - streaming)));
+  a.dctas = std::max(0, std::min(sms - 1, env_or(g_env_dctas, sms - streaming)));
   const int grid = std::min(a.total_items + a.dctas, sms);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);

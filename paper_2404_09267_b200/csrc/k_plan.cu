@@ -330,12 +330,26 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     atomicAdd(&g_plan_phase[0], 1ull);
   }
 #endif
-  if (lane == 0) {  // the last CTA out resets the ticket and moves the epoch on
+  // The last CTA out resets the ticket and moves the epoch on.  Look-back
+  // words carry a 16-bit epoch and are never cleared per launch, so every
+  // 32768 launches the whole array is zeroed: a surviving word is then less
+  // than 32768 launches old and cannot alias the current epoch.
+  unsigned last = 0;
+  if (lane == 0) {
     __threadfence();
-    if (atomicAdd(&a.psync[1], 1u) == static_cast<uint32_t>(a.n_frames) - 1) {
+    last = atomicAdd(&a.psync[1], 1u) == static_cast<uint32_t>(a.n_frames) - 1;
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (last) {
+    const uint32_t next = s_epoch + 1;
+    if ((next & 0x7fffu) == 0)
+      for (int i = lane; i < a.look_cap; i += 32) a.look[i] = 0;
+    __syncwarp();
+    if (lane == 0) {
       a.psync[0] = 0;
       a.psync[1] = 0;
-      a.psync[2] = s_epoch + 1;
+      __threadfence();
+      a.psync[2] = next;
       __threadfence();
     }
   }
@@ -362,36 +376,30 @@ __global__ void __launch_bounds__(256) partition_batch_kernel(const PartitionBat
   if (tid == 0) a.n_patches[f] = np;
 }
 
-// One warp per queue; the free set lives in global workspace.
+// One warp per queue; the free set lives in the caller's workspace, the
+// queue is read and the placements written in place (no context scratch, so
+// stream-ordered batches never share buffers with other calls).
 __global__ void __launch_bounds__(128) stitch_batch_kernel(const StitchBatchArgs a) {
   const int q = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (q >= a.n_queues) return;
   const int o0 = a.offsets[q], n = a.offsets[q + 1] - o0;
-  int* pw = a.dims_ws + 5 * o0;
-  int* ph = pw + n;
-  StitchOut* so = reinterpret_cast<StitchOut*>(ph + n);
-  uint64_t* ids = a.ids_ws + o0;
-  for (int i = lane; i < n; i += 32) {
-    pw[i] = a.queue[o0 + i].rect.w;
-    ph[i] = a.queue[o0 + i].rect.h;
-    ids[i] = a.queue[o0 + i].patch_id;
-  }
-  __syncwarp();
-  FreeRect* fl = a.free_ws + 2 * o0 + q;
+  const tg_patch_meta* qu = a.queue + o0;
+  tg_placement* pl = a.placements + o0;
+  FreeRect* fl = a.free_ws + 2 * static_cast<size_t>(o0) + q;
   int nfree = 0;
-  const int nc = bssf_stitch(pw, ph, ids, n, a.M, a.N, fl, 2 * n + 1, so, &nfree, a.err, q, lane);
-  __syncwarp();
-  if (nc >= 0) {
-    for (int i = lane; i < n; i += 32) {
-      tg_placement p;
-      p.patch_id = ids[i];
-      p.canvas_index = so[i].canvas;
-      p.position = tg_rect{so[i].x, so[i].y, pw[i], ph[i]};
-      p.reserved = 0;
-      a.placements[o0 + i] = p;
-    }
-  }
+  const int nc = bssf_stitch_q(
+      [qu](int i) { return make_int2(qu[i].rect.w, qu[i].rect.h); },
+      [qu](int i) { return qu[i].patch_id; },
+      [qu, pl](int i, int c, int x, int y) {
+        tg_placement p;
+        p.patch_id = qu[i].patch_id;
+        p.canvas_index = c;
+        p.position = tg_rect{x, y, qu[i].rect.w, qu[i].rect.h};
+        p.reserved = 0;
+        pl[i] = p;
+      },
+      n, a.M, a.N, fl, 2 * n + 1, &nfree, a.err, q, lane);
   if (lane == 0) {
     a.n_canvases[q] = nc;
     if (a.n_free) a.n_free[q] = nfree;
@@ -409,9 +417,9 @@ size_t plan_smem_bytes(int cells_x, int cells_y, int max_rois) {
 
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
   if (a.n_frames < 0) return cudaErrorInvalidValue;
+  static SmemOptIn opt_in;
   const size_t smem = plan_smem_bytes(a.cells_x, a.cells_y, a.max_rois);
-  cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = opt_in.ensure(plan_kernel, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   plan_kernel<<<a.n_frames > 0 ? a.n_frames : 1, kPlanThreads, smem, stream>>>(a);
   return cudaGetLastError();

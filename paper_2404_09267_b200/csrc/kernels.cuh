@@ -50,7 +50,8 @@ struct PlanArgs {
   uint2* ranges;          // [max_canvases] (first job, job count) in the flat job array
   int32_t* gather_units;  // out: [0] min(total, cap) * nbands; [1], [2] K5 counters := 0
   uint64_t* id_state;     // next patch id after this run
-  uint64_t* look;         // [F] look-back words: epoch | flag | patches | canvases
+  uint64_t* look;         // [look_cap] look-back words: epoch | flag | patches | canvases
+  int look_cap;           // max_frames
   uint32_t* psync;        // [3] frame ticket, finished CTAs, epoch
   DevError* err;
 };
@@ -76,8 +77,6 @@ struct StitchBatchArgs {
   int32_t* n_canvases;
   FreeRect* free_ws;   // [2*total + n_queues]
   int32_t* n_free;     // optional [n_queues]
-  int32_t* dims_ws;    // [5*total] scratch: w, h, StitchOut{canvas, x, y}
-  uint64_t* ids_ws;    // [total] scratch patch ids
   DevError* err;
 };
 

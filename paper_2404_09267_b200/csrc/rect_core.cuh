@@ -139,51 +139,58 @@ __device__ __forceinline__ int partition_emit(const ZoneAcc& z, int nz, uint64_t
 // Best-short-side fit over every live free rect of every open canvas;
 // ties by lower canvas, then lower y, then lower x (candidate_better,
 // stitch.hpp:72-81) -- a total order because a canvas's free rects are
-// disjoint, so one 64-bit key min finds the reference's choice.  The free
-// set is kept unordered (swap-remove); each rect carries its insertion seq
-// so the reference's list order can be rebuilt.  Guillotine split per
-// stitch.hpp:86-99.  Returns the canvas count, or -1 after latching an
-// error (oversize patch / free capacity).
+// disjoint, so a lexicographic min over two 64-bit keys, (score, canvas) then
+// (y, x), finds the reference's choice for any canvas count (scores,
+// coordinates < 2^16: canvas sides are bounded by 65535 at the ABI).  The
+// free set is kept unordered (swap-remove); each rect carries its insertion
+// seq so the reference's list order can be rebuilt.  Guillotine split per
+// stitch.hpp:86-99.  dims(i) -> int2 (w, h) and id(i) read the queue;
+// emit(i, canvas, x, y) receives each placement (lane 0).  Returns the canvas
+// count, or -1 after latching an error (oversize patch / free capacity).
 struct StitchOut {
   int canvas;
   int x, y;
 };
 
-__device__ __forceinline__ int bssf_stitch(const int* pw, const int* ph, const uint64_t* pid,
-                                           int n, int M, int N, FreeRect* fl, int cap,
-                                           StitchOut* out, int* n_free_out, DevError* err,
-                                           int queue, int lane) {
+template <class Dims, class Id, class Emit>
+__device__ __forceinline__ int bssf_stitch_q(Dims dims, Id id, Emit emit, int n, int M, int N,
+                                             FreeRect* fl, int cap, int* n_free_out, DevError* err,
+                                             int queue, int lane) {
   int nfree = 0, nc = 0, seq = 0;
   for (int i = 0; i < n; ++i) {
-    const int w = pw[i], h = ph[i];
+    const int2 d = dims(i);
+    const int w = d.x, h = d.y;
     if (w > M || h > N) {
       if (lane == 0)
         raise_error(err, TG_ERR_INVALID_ARGUMENT, kErrPatchOversize,
-                    static_cast<long long>(pid ? pid[i] : static_cast<uint64_t>(i)), w, h, queue);
+                    static_cast<long long>(id(i)), w, h, queue);
       return -1;
     }
-    unsigned long long best = ~0ull;
+    unsigned long long b1 = ~0ull, b2 = ~0ull;
     int bi = -1;
     for (int k = lane; k < nfree; k += 32) {
       const FreeRect c = fl[k];
       if (c.w < w || c.h < h) continue;
       const unsigned s = static_cast<unsigned>(min(c.w - w, c.h - h));
-      const unsigned long long key = (static_cast<unsigned long long>(s) << 48) |
-                                     (static_cast<unsigned long long>(c.canvas) << 32) |
-                                     (static_cast<unsigned long long>(c.y) << 16) |
-                                     static_cast<unsigned long long>(c.x);
-      if (key < best) {
-        best = key;
+      const unsigned long long k1 = (static_cast<unsigned long long>(s) << 32) |
+                                    static_cast<unsigned long long>(static_cast<unsigned>(c.canvas));
+      const unsigned long long k2 = (static_cast<unsigned long long>(c.y) << 32) |
+                                    static_cast<unsigned long long>(static_cast<unsigned>(c.x));
+      if (k1 < b1 || (k1 == b1 && k2 < b2)) {
+        b1 = k1;
+        b2 = k2;
         bi = k;
       }
     }
-    const unsigned long long gmin = warp_min_u64(best);
+    const unsigned long long g1 = warp_min_u64(b1);
+    const unsigned long long g2 = warp_min_u64(b1 == g1 ? b2 : ~0ull);
     FreeRect chosen;
-    if (gmin == ~0ull) {  // nothing fits: open a blank canvas (stitch.hpp:129-135)
+    const bool fits = g1 != ~0ull;
+    if (!fits) {  // nothing fits: open a blank canvas (stitch.hpp:129-135)
       chosen = FreeRect{0, 0, M, N, nc, -1};
       ++nc;
     } else {
-      const unsigned owner = __ballot_sync(0xffffffffu, best == gmin && bi >= 0);
+      const unsigned owner = __ballot_sync(0xffffffffu, b1 == g1 && b2 == g2 && bi >= 0);
       const int src = __ffs(owner) - 1;
       bi = __shfl_sync(0xffffffffu, bi, src);
       chosen = fl[bi];
@@ -200,14 +207,14 @@ __device__ __forceinline__ int bssf_stitch(const int* pw, const int* ph, const u
     }
     const bool keep_a = a.w > 0 && a.h > 0, keep_b = b.w > 0 && b.h > 0;
     int nf = nfree;
-    if (gmin != ~0ull) --nf;  // swap-remove the chosen rect
+    if (fits) --nf;  // swap-remove the chosen rect
     const int need = nf + (keep_a ? 1 : 0) + (keep_b ? 1 : 0);
     if (need > cap) {
       if (lane == 0) raise_error(err, TG_ERR_CAPACITY, kErrFreeCapacity, queue, cap);
       return -1;
     }
     if (lane == 0) {
-      if (gmin != ~0ull) fl[bi] = fl[nfree - 1];
+      if (fits) fl[bi] = fl[nfree - 1];
       if (keep_a) {
         a.seq = seq++;
         fl[nf++] = a;
@@ -216,7 +223,7 @@ __device__ __forceinline__ int bssf_stitch(const int* pw, const int* ph, const u
         b.seq = seq++;
         fl[nf++] = b;
       }
-      out[i] = StitchOut{chosen.canvas, chosen.x, chosen.y};
+      emit(i, chosen.canvas, chosen.x, chosen.y);
     } else {
       seq += (keep_a ? 1 : 0) + (keep_b ? 1 : 0);
       nf += (keep_a ? 1 : 0) + (keep_b ? 1 : 0);
@@ -226,6 +233,17 @@ __device__ __forceinline__ int bssf_stitch(const int* pw, const int* ph, const u
   }
   if (n_free_out) *n_free_out = nfree;
   return nc;
+}
+
+// Queue in shared arrays (the per-frame planner).
+__device__ __forceinline__ int bssf_stitch(const int* pw, const int* ph, const uint64_t* pid,
+                                           int n, int M, int N, FreeRect* fl, int cap,
+                                           StitchOut* out, int* n_free_out, DevError* err,
+                                           int queue, int lane) {
+  return bssf_stitch_q([pw, ph](int i) { return make_int2(pw[i], ph[i]); },
+                       [pid](int i) { return pid ? pid[i] : static_cast<uint64_t>(i); },
+                       [out](int i, int c, int x, int y) { out[i] = StitchOut{c, x, y}; }, n, M, N,
+                       fl, cap, n_free_out, err, queue, lane);
 }
 
 }  // namespace tg

@@ -417,3 +417,16 @@ def test_schedule_descriptors_edge_cases():
         MC.schedule_descriptors(mk(), recs([(2, 0, 100), (0, 0, 100)]), [0, 2], 4, 80.0)
     with pytest.raises(A.InvalidArgument, match="frame 9 out of range"):
         MC.schedule_descriptors(mk(), recs([(0, 9, 100)]), [0], 4, 80.0)
+
+
+def test_batcher_beyond_65535_canvases():
+    """The host best-fit key covers any canvas count: the winner sits on
+    canvas 65540 (see tests/test_gpu_parity.py::wide_key_queue)."""
+    dims = [(60, 60)] + [(100, 100)] * 65539 + [(61, 61), (39, 39)]
+    patches = [A.PatchMeta(i, i, A.Rect(0, 0, w, h), 0, 10**12, 10**12, w * h)
+               for i, (w, h) in enumerate(dims)]
+    s = sched(max_canvases=70000, profile=[(1, 1.0, 0.0), (2, 1.0, 0.0)])
+    evs = s.replay(patches, [0] * len(patches))
+    assert len(evs) == 1 and evs[0].batch_size == 65541
+    last = evs[0].stitch.placement_index[len(dims) - 1]
+    assert (last.canvas_index, last.position) == (65540, A.Rect(61, 0, 39, 39))

@@ -113,6 +113,27 @@ def test_stitch_dropin_kat_values(ctx):
     assert A.canvas_efficiency(r) == [0.36, 0.25]
 
 
+def wide_key_queue():
+    """A queue whose best-fit winner sits on canvas 65540: canvas 0 offers a
+    score-1 fit, canvases 1..65539 are full, canvas 65540 an exact (score 0)
+    fit.  A (score, canvas, y, x) key with 16 canvas bits lets canvas 65540's
+    high bit spill into the score and picks canvas 0 instead."""
+    dims = [(60, 60)] + [(100, 100)] * 65539 + [(61, 61), (39, 39)]
+    return [A.PatchMeta(i, 0, A.Rect(0, 0, w, h)) for i, (w, h) in enumerate(dims)]
+
+
+def test_stitch_dropin_beyond_65535_canvases(ctx):
+    q = wide_key_queue()
+    r = A.stitch_all(q, A.CanvasSpec(100, 100), ctx=ctx)
+    assert r.canvas_count() == 65541
+    last = r.placement_index[len(q) - 1]
+    assert (last.canvas_index, last.position) == (65540, A.Rect(61, 0, 39, 39))
+    if O.have_ref():
+        pl, nc, _ = O.stitch_all([(p.patch_id, p.rect.w, p.rect.h) for p in q[-3:]], 100, 100,
+                                 lib="ref")
+        assert nc == 2 and pl[-1][1:] == (1, 61, 0, 39, 39)  # same choice on a 2-canvas queue
+
+
 def test_stitch_batch_c01_acceptance(ctx):
     """Acceptance C01 (acceptance_test.cpp:48-101): all 10,000 seeded sets,
     stitched in one batched launch (one warp per queue), every placement and
