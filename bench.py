@@ -87,6 +87,26 @@ def init_dist(local: int):
     return dist
 
 
+def make_comm(A, ctx, dist, rank: int, world: int):
+    """The descriptor all-gather's communicator (tg_comm): NCCL between the
+    ranks' GPUs (the id travels over torch.distributed, the bench's
+    rendezvous), or a host transport over gloo when ranks share a GPU."""
+    if dist is None:
+        return None
+    if dist.get_backend() == "nccl":
+        obj = [A.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return A.Comm.nccl(ctx, obj[0], rank, world)
+    import torch
+
+    def allgather(data: bytes):
+        t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        return [p.numpy().tobytes() for p in parts]
+    return A.Comm.host(rank, world, allgather)
+
+
 def reduce_max(dist, value: float, local: int) -> float:
     """Max over ranks (device tensor on NCCL, host tensor on gloo)."""
     import torch
@@ -514,22 +534,17 @@ def run_multicam(args):
     kw = dict(bandwidth_mbps=SIM_BANDWIDTH_MBPS, gpu_memory_gb=SIM_GPU_MEMORY_GB, model_size_gb=4.0,
               trace_kw=dict(roi_proportion_mean=0.10, roi_max_dim=480))
     glob = args.global_batching and dist is not None
+    comm = make_comm(A, ctx, dist, rank, world)
+    per_rank = max(len(MC.shard_cameras(n_cams_total, world, r)) for r in range(world))
     if glob:
-        path = MC.GlobalCameraPath(ctx, n_cams_total, rank, world, dist, W, H, frames, SIM_PROFILE,
-                                   device=f"cuda:{gpu_of(local)}" if dist.get_backend() == "nccl" else None, **kw)
+        path = MC.GlobalCameraPath(ctx, n_cams_total, comm, W, H, frames, SIM_PROFILE, **kw)
     else:
-        path = MC.MultiCameraPath(ctx, cams, W, H, frames, SIM_PROFILE, **kw)
+        path = MC.MultiCameraPath(ctx, cams, W, H, frames, SIM_PROFILE, comm=comm,
+                                  cameras_per_rank=per_rank, **kw)
     e0, e1 = ctx.event(), ctx.event()
-    exchange = None
-    if dist is not None and not glob:
-        # every rank schedules its shard from the all-gathered list (global ids)
-        def exchange(desc):
-            return MC.gather_descriptors(
-                desc, dist, device=f"cuda:{gpu_of(local)}" if dist.get_backend() == "nccl" else None)
-
     # K steps = K passes over the shard's frames; the host batcher of pass i
     # overlaps the device planes of pass i+1 (MultiCameraPath.run_pipelined)
-    n_canv = path.run_pipelined(args.warmup, exchange)
+    n_canv = path.run_pipelined(args.warmup)
     ctx.stream_sync(path.stream)
     clocks = Clocks(gpu_of(local))
     if dist is not None:
@@ -537,7 +552,7 @@ def run_multicam(args):
     ctx.synchronize()
     clocks.start()
     ctx.record(e0, path.stream)
-    n_canv = path.run_pipelined(args.steps, exchange)
+    n_canv = path.run_pipelined(args.steps)
     ctx.record(e1, path.stream)
     ctx.stream_sync(path.stream)
     clk = clocks.stop()

@@ -47,7 +47,8 @@ typedef enum {
   TG_ERR_OUT_OF_RANGE = 2,     /* reference: std::out_of_range    */
   TG_ERR_CAPACITY = 3,         /* a fixed device capacity was exceeded */
   TG_ERR_CUDA = 4,             /* CUDA runtime failure */
-  TG_ERR_NO_DEVICE = 5         /* no usable CUDA device: no fallback exists */
+  TG_ERR_NO_DEVICE = 5,        /* no usable CUDA device: no fallback exists */
+  TG_ERR_COMM = 6              /* collective (NCCL / host transport) failure */
 } tg_status;
 
 /* ---- POD mirrors of the reference value types --------------------------- */
@@ -348,6 +349,12 @@ tg_status tg_batcher_status(tg_batcher* b, int32_t* queue_len, int32_t* canvases
  * may be NULL. */
 tg_status tg_batcher_event(tg_batcher* b, int32_t i, tg_invoke_info* info, uint64_t* patch_ids,
                            tg_placement* placements, tg_free_rect* free_rects);
+/* The live batch (SloScheduler::queue() / current_stitch(), scheduler.hpp:
+ * 137-141): info->n_patches queued patches in queue order, their packing
+ * (placements canvas-major, free rects canvas-major in list order);
+ * info->batch_size = open canvases; arrays may be NULL (sizes first). */
+tg_status tg_batcher_current(tg_batcher* b, tg_invoke_info* info, tg_patch_meta* queue,
+                             tg_placement* placements, tg_free_rect* free_rects);
 /* Writes event i's canvases: d_frames[src_frame] holds each patch's frame. */
 tg_status tg_batcher_gather(tg_ctx* ctx, tg_batcher* b, int32_t i, const uint8_t* const* d_frames,
                             int32_t pitch, uint8_t* d_canvases, void* stream);
@@ -388,9 +395,65 @@ typedef struct {
   int32_t admitted;  /* w <= M && h <= N (sim.hpp:262) */
   int32_t pad;
 } tg_descriptor;     /* 80 B */
-/* Compacts a pipeline's per-frame patch slots (patches[F][zones],
- * n_patches[F], admitted[F][zones], as tg_pipeline_views lays them out) into
- * descriptors, frame order then zone order.  Pipeline frame f is frame
+
+/* A descriptor block -- what one rank contributes to the all-gather: this
+ * header, then `cap` records.  `count` records are valid. */
+typedef struct {
+  int64_t count;
+  int64_t cap;
+  int64_t reserved[8];
+} tg_descriptor_header; /* 80 B, one record's size */
+size_t tg_descriptor_block_bytes(int64_t cap);
+
+/* Device-side descriptor list.  With an output block attached (device
+ * memory of tg_descriptor_block_bytes(cap)), every plan stage of the
+ * pipeline writes its run's patches there as dense records: record i is the
+ * run's i-th patch in frame, zone order (the reference's scene/frame-ordered
+ * patch list, sim.hpp:241-262), patch_id run-local from 0.  The planner's
+ * frame-order prefix (decoupled look-back over the frames' patch counts) is
+ * the compaction scan, so this costs no extra launch.  Pipeline frame f is
+ * frame f % frames_per_camera of camera d_cameras[f / frames_per_camera]
+ * (d_cameras: device int32 array; NULL: camera 0, frame f).  A run with
+ * more than cap patches latches TG_ERR_CAPACITY.  d_block == NULL detaches. */
+tg_status tg_pipeline_set_descriptor_output(tg_pipeline* p, void* d_block, int64_t cap,
+                                            const int32_t* d_cameras, int32_t frames_per_camera);
+/* Host: concatenates the valid records of n_blocks blocks (each
+ * tg_descriptor_block_bytes(cap) bytes, e.g. the all-gathered blocks read
+ * back) -- rank-major, which is camera-major under contiguous sharding. */
+tg_status tg_descriptor_blocks_flatten(const void* blocks, int32_t n_blocks, int64_t cap,
+                                       tg_descriptor* out, int64_t out_cap, int64_t* n_out);
+
+/* ---- the collective: descriptor all-gather --------
+ * Replaces the reference's single-process scene loop (sim.hpp:241-272) when
+ * cameras are sharded over GPUs.  A device communicator runs NCCL on device
+ * buffers (stream-ordered); a host communicator moves host buffers through
+ * a caller-supplied all-gather (tests, or any out-of-band transport). */
+typedef struct tg_comm tg_comm;
+typedef struct { uint8_t bytes[128]; } tg_comm_id; /* ncclUniqueId */
+/* Rank 0 creates the id and sends it to every rank out of band. */
+tg_status tg_comm_get_unique_id(tg_comm_id* out);
+tg_status tg_comm_create(tg_ctx* ctx, const tg_comm_id* id, int32_t rank, int32_t world,
+                         tg_comm** out);
+/* fn gathers `bytes` from every rank into recv (rank-major); returns 0 on
+ * success. */
+typedef int32_t (*tg_host_allgather_fn)(const void* send, size_t bytes, void* recv, void* user);
+tg_status tg_comm_create_host(int32_t rank, int32_t world, tg_host_allgather_fn fn, void* user,
+                              tg_comm** out);
+void tg_comm_destroy(tg_comm* comm);
+tg_status tg_comm_info(tg_comm* comm, int32_t* rank, int32_t* world, int32_t* on_device);
+/* recv (world * bytes) receives every rank's send buffer, rank-major.
+ * Device communicator: device buffers, async on `stream`; host
+ * communicator: host buffers, blocking. */
+tg_status tg_comm_allgather(tg_comm* comm, const void* send, size_t bytes, void* recv,
+                            void* stream);
+/* Every rank's descriptor block (cap records each) into blocks_out, rank-major. */
+tg_status tg_descriptors_allgather(tg_comm* comm, const void* block, int64_t cap,
+                                   void* blocks_out, void* stream);
+
+/* Host compaction of per-frame patch slots (patches[F][zones], n_patches[F],
+ * admitted[F][zones], as tg_pipeline_views lays them out) into descriptors,
+ * frame order then zone order -- the host restatement of the device list
+ * above (for callers holding slots on the host).  Pipeline frame f is frame
  * f % frames_per_camera of camera cameras[f / frames_per_camera]
  * (F = n_cams * frames_per_camera).  TG_ERR_CAPACITY if cap is too small. */
 tg_status tg_descriptors_compact(const tg_patch_meta* patches, const int32_t* n_patches,

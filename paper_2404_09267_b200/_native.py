@@ -18,6 +18,7 @@ TG_ERR_OUT_OF_RANGE = 2
 TG_ERR_CAPACITY = 3
 TG_ERR_CUDA = 4
 TG_ERR_NO_DEVICE = 5
+TG_ERR_COMM = 6
 
 
 class tg_rect(C.Structure):
@@ -90,6 +91,14 @@ class tg_gather_job(C.Structure):
 
 class tg_ipc_handle(C.Structure):
     _fields_ = [("bytes", C.c_uint8 * 64)]
+
+
+class tg_comm_id(C.Structure):
+    _fields_ = [("bytes", C.c_uint8 * 128)]
+
+
+# tg_host_allgather_fn: (send, bytes, recv, user) -> 0 on success
+HOST_ALLGATHER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 
 
 class tg_profile_entry(C.Structure):
@@ -177,11 +186,23 @@ SIGNATURES = {
     "tg_batcher_status": (st, [vp, P(i32), P(i32), P(i64), P(i64)]),
     "tg_batcher_event": (st, [vp, i32, P(tg_invoke_info), P(u64), P(tg_placement),
                               P(tg_free_rect)]),
+    "tg_batcher_current": (st, [vp, P(tg_invoke_info), P(tg_patch_meta), P(tg_placement),
+                                P(tg_free_rect)]),
     "tg_batcher_gather": (st, [vp, vp, i32, vp, i32, vp, vp]),
     "tg_batcher_gather_all": (st, [vp, vp, vp, i32, vp, i64, P(i64), vp]),
     "tg_batcher_gather_events": (st, [vp, vp, i32, i32, vp, i32, vp, i64, P(i64), vp]),
     "tg_batcher_replay": (st, [vp, P(tg_patch_meta), P(i32), P(i64), i32, P(i32)]),
     "tg_batcher_replay_links": (st, [vp, i32, vp, vp, vp, C.c_double, i32, vp, P(i32)]),
+    "tg_descriptor_block_bytes": (sz, [i64]),
+    "tg_pipeline_set_descriptor_output": (st, [vp, vp, i64, vp, i32]),
+    "tg_descriptor_blocks_flatten": (st, [vp, i32, i64, vp, i64, P(i64)]),
+    "tg_comm_get_unique_id": (st, [P(tg_comm_id)]),
+    "tg_comm_create": (st, [vp, P(tg_comm_id), i32, i32, P(vp)]),
+    "tg_comm_create_host": (st, [i32, i32, HOST_ALLGATHER_FN, vp, P(vp)]),
+    "tg_comm_destroy": (None, [vp]),
+    "tg_comm_info": (st, [vp, P(i32), P(i32), P(i32)]),
+    "tg_comm_allgather": (st, [vp, vp, sz, vp, vp]),
+    "tg_descriptors_allgather": (st, [vp, vp, i64, vp, vp]),
     "tg_descriptors_compact": (st, [vp, vp, vp, i32, vp, i32, i32, vp, i64, P(i64)]),
     "tg_batcher_schedule": (st, [vp, vp, i64, vp, i32, i32, C.c_double, i32, vp, vp, vp, P(i64),
                                  P(i32)]),

@@ -52,8 +52,13 @@ class NoDevice(TangramError):
     pass
 
 
+class CommError(TangramError):
+    pass
+
+
 _ERRS = {N.TG_ERR_INVALID_ARGUMENT: InvalidArgument, N.TG_ERR_OUT_OF_RANGE: OutOfRange,
-         N.TG_ERR_CAPACITY: CapacityError, N.TG_ERR_CUDA: CudaError, N.TG_ERR_NO_DEVICE: NoDevice}
+         N.TG_ERR_CAPACITY: CapacityError, N.TG_ERR_CUDA: CudaError, N.TG_ERR_NO_DEVICE: NoDevice,
+         N.TG_ERR_COMM: CommError}
 
 
 def check(status: int) -> None:
@@ -292,6 +297,78 @@ class Context:
         ms = C.c_float()
         check(self._lib.tg_event_elapsed_ms(self.handle, start, stop, C.byref(ms)))
         return ms.value
+
+
+class Comm:
+    """The descriptor all-gather's communicator (tg_comm): NCCL over device
+    buffers (stream-ordered), or a host transport -- any callable
+    ``allgather(data: bytes) -> list[bytes]`` (rank-major) -- over host
+    buffers.  Ranks of a device communicator meet through a 128-byte id that
+    rank 0 creates (:meth:`unique_id`) and sends out of band."""
+
+    def __init__(self, handle, ctx: Context | None, rank: int, world: int, on_device: bool,
+                 keep=None):
+        self.handle, self.ctx, self.rank, self.world = handle, ctx, rank, world
+        self.on_device, self._keep = on_device, keep
+
+    @staticmethod
+    def unique_id() -> bytes:
+        uid = N.tg_comm_id()
+        check(N.lib().tg_comm_get_unique_id(C.byref(uid)))
+        return bytes(uid.bytes)
+
+    @classmethod
+    def nccl(cls, ctx: Context, uid: bytes, rank: int, world: int) -> "Comm":
+        u = N.tg_comm_id()
+        C.memmove(u.bytes, uid, 128)
+        h = C.c_void_p()
+        check(N.lib().tg_comm_create(ctx.handle, C.byref(u), rank, world, C.byref(h)))
+        return cls(h, ctx, rank, world, True)
+
+    @classmethod
+    def host(cls, rank: int, world: int, allgather) -> "Comm":
+        def fn(send, nbytes, recv, _user):
+            try:
+                parts = allgather(C.string_at(send, nbytes) if nbytes else b"")
+                if len(parts) != world or any(len(x) != nbytes for x in parts):
+                    return 1
+                if nbytes:
+                    C.memmove(recv, b"".join(parts), nbytes * world)
+                return 0
+            except Exception:
+                return 1
+        cb = N.HOST_ALLGATHER_FN(fn)
+        h = C.c_void_p()
+        check(N.lib().tg_comm_create_host(rank, world, cb, None, C.byref(h)))
+        return cls(h, None, rank, world, False, keep=cb)
+
+    def allgather(self, send: int, nbytes: int, recv: int, stream=None) -> None:
+        """Raw all-gather (device pointers for NCCL, host pointers otherwise)."""
+        check(N.lib().tg_comm_allgather(self.handle, send, nbytes, recv, stream))
+
+    def allgather_bytes(self, data: bytes) -> list[bytes]:
+        """Blocking all-gather of equal-sized host byte strings (e.g. IPC
+        handles), staged through device memory on an NCCL communicator."""
+        n = len(data)
+        out = C.create_string_buffer(max(1, n * self.world))
+        src = C.create_string_buffer(data, max(1, n))
+        if self.on_device:
+            d_send, d_recv = self.ctx.malloc(n), self.ctx.malloc(n * self.world)
+            self.ctx.memcpy(d_send, C.addressof(src), n, 0)
+            self.allgather(d_send, n, d_recv, self.ctx.stream)
+            self.ctx.memcpy(C.addressof(out), d_recv, n * self.world, 1)
+            self.ctx.stream_sync()
+            self.ctx.free(d_send)
+            self.ctx.free(d_recv)
+        else:
+            self.allgather(C.addressof(src), n, C.addressof(out))
+        raw = out.raw
+        return [raw[r * n:(r + 1) * n] for r in range(self.world)]
+
+    def close(self):
+        if self.handle:
+            N.lib().tg_comm_destroy(self.handle)
+            self.handle = None
 
 
 _DEFAULT: Context | None = None
@@ -577,6 +654,19 @@ class Pipeline:
                                         for k in range(out["n_placements"][f]))]
             for f in range(F)]
         return out
+
+    def set_descriptor_output(self, d_block: int | None, cap: int = 0, d_cameras: int | None = None,
+                              frames_per_camera: int = 1) -> None:
+        """Plan stages write the run's patches as dense device descriptors
+        (tg_pipeline_set_descriptor_output); None detaches."""
+        check(N.lib().tg_pipeline_set_descriptor_output(self.handle, d_block, cap, d_cameras,
+                                                        frames_per_camera))
+
+    def stats(self) -> dict:
+        s = N.tg_pipeline_stats()
+        check(N.lib().tg_pipeline_get_stats(self.handle, C.byref(s)))
+        return {"mask_fused_launches": s.mask_fused_launches,
+                "mask_split_launches": s.mask_split_launches}
 
     def free_rects(self, frame: int):
         cap = 3 * self.zones + 4

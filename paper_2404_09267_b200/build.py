@@ -1,6 +1,6 @@
 """Builds the in-tree CUDA library ``lib/libtangram_gpu.so`` for sm_100a.
 
-Plain nvcc, no torch extension machinery: the library exports the C ABI in
+Plain nvcc, no Python extension machinery: the library exports the C ABI in
 include/tangram_gpu.h and is loaded with ctypes (Python) or linked directly
 (C++ drop-in, tests/cpp).  Run ``python -m paper_2404_09267_b200.build``.
 """
@@ -70,7 +70,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     if failed:
         raise RuntimeError("nvcc failed for: " + ", ".join(failed))
     tmp = target + ".tmp"
-    subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", tmp, *objs])
+    # NCCL (the descriptor all-gather, csrc/comm.cu): the system library
+    subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lnccl"])
     os.replace(tmp, target)
     return target
 

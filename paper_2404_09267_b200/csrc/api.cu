@@ -86,6 +86,11 @@ struct tg_pipeline {
   uint32_t* psync = nullptr;  // [3] plan frame ticket, finished CTAs, epoch
   int last_frames = 0;
   tg_pipeline_stats stats{};
+  // optional dense descriptor output (tg_pipeline_set_descriptor_output)
+  tg_descriptor_header* desc_head = nullptr;
+  int64_t desc_cap = 0;
+  const int32_t* desc_cameras = nullptr;
+  int32_t desc_fpc = 1;
 };
 
 struct tg_graph {
@@ -125,6 +130,9 @@ tg_status check_device_error(tg_ctx* ctx) {
                   e.a, e.b);
     case kErrFreeCapacity:
       return fail(static_cast<tg_status>(e.code), "free rect capacity exceeded (queue %lld)", e.a);
+    case kErrDescCapacity:
+      return fail(static_cast<tg_status>(e.code),
+                  "descriptor capacity exceeded (%lld patches > %lld records)", e.a, e.b);
     default:
       return fail(static_cast<tg_status>(e.code), "device error kind %d", e.kind);
   }
@@ -173,8 +181,9 @@ extern "C" {
 
 int tg_abi_version(void) { return TG_ABI_VERSION; }
 
-// ---- internal hooks for batcher.cu (not part of the public header) ---------
+// ---- internal hooks for batcher.cu / comm.cu (not part of the public header) --
 void tg_internal_set_error(const char* msg) { g_err = msg; }
+int tg_internal_ctx_device(tg_ctx* ctx) { return ctx ? ctx->device : -1; }
 
 // Uploads an explicit gather plan (host Job[] + per-canvas ranges) on the
 // stream and launches K5 over it.  Pageable host sources: cudaMemcpyAsync
@@ -852,6 +861,11 @@ tg_status tg_pipeline_stage_plan(tg_pipeline* p, int32_t n_frames, const uint64_
   a.look = p->look;
   a.look_cap = p->p.max_frames;
   a.psync = p->psync;
+  a.desc_head = p->desc_head;
+  a.desc = p->desc_head ? reinterpret_cast<tg_descriptor*>(p->desc_head + 1) : nullptr;
+  a.desc_cap = p->desc_cap;
+  a.desc_cameras = p->desc_cameras;
+  a.desc_fpc = p->desc_fpc;
   TG_CUDA(launch_plan(a, st));
   p->last_frames = n_frames;
   return TG_OK;
@@ -955,6 +969,26 @@ tg_status tg_pipeline_device_views(tg_pipeline* p, tg_pipeline_views* v) {
   v->cells_x = p->cells_x;
   v->cells_y = p->cells_y;
   v->mask_words = p->mask_words;
+  return TG_OK;
+}
+
+size_t tg_descriptor_block_bytes(int64_t cap) {
+  static_assert(sizeof(tg_descriptor) == 80 && sizeof(tg_descriptor_header) == 80,
+                "descriptor records and headers are 80 bytes");
+  return sizeof(tg_descriptor_header) + static_cast<size_t>(cap < 0 ? 0 : cap) * sizeof(tg_descriptor);
+}
+
+tg_status tg_pipeline_set_descriptor_output(tg_pipeline* p, void* d_block, int64_t cap,
+                                            const int32_t* d_cameras, int32_t frames_per_camera) {
+  if (!p) return fail(TG_ERR_INVALID_ARGUMENT, "null pipeline");
+  if (d_block && (cap < 0 || (d_cameras && frames_per_camera < 1)))
+    return fail(TG_ERR_INVALID_ARGUMENT, "descriptor output needs cap >= 0 and frames_per_camera >= 1");
+  if (reinterpret_cast<uintptr_t>(d_block) % 16)
+    return fail(TG_ERR_INVALID_ARGUMENT, "descriptor block must be 16-byte aligned");
+  p->desc_head = static_cast<tg_descriptor_header*>(d_block);
+  p->desc_cap = d_block ? cap : 0;
+  p->desc_cameras = d_block ? d_cameras : nullptr;
+  p->desc_fpc = d_block && d_cameras ? frames_per_camera : 1;
   return TG_OK;
 }
 

@@ -500,6 +500,31 @@ tg_status tg_batcher_status(tg_batcher* b, int32_t* queue_len, int32_t* canvases
   return TG_OK;
 }
 
+tg_status tg_batcher_current(tg_batcher* b, tg_invoke_info* info, tg_patch_meta* queue,
+                             tg_placement* placements, tg_free_rect* free_rects) {
+  tg_invoke_info in{};
+  in.batch_size = static_cast<int32_t>(b->st.canvases.size());
+  in.n_patches = static_cast<int32_t>(b->queue.size());
+  in.estimated_slack_us = in.batch_size > 0 ? b->prof.slack_us(in.batch_size) : 0;
+  int32_t nf = 0, np = 0;
+  for (int ci = 0; ci < in.batch_size; ++ci) {
+    const CanvasSt& c = b->st.canvases[ci];
+    for (const Placed& p : c.placed) {
+      if (placements) placements[np] = p.pl;
+      ++np;
+    }
+    for (int k = 0; k < static_cast<int>(c.free.size()); ++k) {
+      if (free_rects) free_rects[nf] = tg_free_rect{c.free[k], ci, k};
+      ++nf;
+    }
+  }
+  in.n_free = nf;
+  if (queue)
+    for (size_t k = 0; k < b->queue.size(); ++k) queue[k] = b->queue[k].meta;
+  if (info) *info = in;
+  return TG_OK;
+}
+
 tg_status tg_batcher_event(tg_batcher* b, int32_t i, tg_invoke_info* info, uint64_t* patch_ids,
                            tg_placement* placements, tg_free_rect* free_rects) {
   if (i < 0 || i >= static_cast<int32_t>(b->events.size()))

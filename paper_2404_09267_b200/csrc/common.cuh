@@ -28,6 +28,7 @@ enum ErrKind : int {
   kErrRoiCapacity = 3,     // a = frame, b = rois found, c = cap
   kErrCanvasCapacity = 4,  // a = total canvases, b = cap
   kErrFreeCapacity = 5,    // a = queue
+  kErrDescCapacity = 6,    // a = patches, b = cap
 };
 
 __device__ __forceinline__ void raise_error(DevError* e, int code, int kind, long long a,

@@ -128,6 +128,12 @@ __device__ void plan_totals(const PlanArgs& a, uint64_t first_id, uint64_t total
   a.gather_units[0] = static_cast<int32_t>(total * a.nbands);
   a.gather_units[1] = 0;  // K5's claim counters
   a.gather_units[2] = 0;
+  if (a.desc_head) {
+    const long long np = static_cast<long long>(total_p);
+    if (np > a.desc_cap) raise_error(a.err, TG_ERR_CAPACITY, kErrDescCapacity, np, a.desc_cap);
+    a.desc_head->count = np < a.desc_cap ? np : a.desc_cap;
+    a.desc_head->cap = a.desc_cap;
+  }
 }
 
 // K3/K4 working set; aliases the K2 (CCL) region of dynamic smem once the
@@ -302,6 +308,22 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   const uint64_t id0 = s_first + ex_p;
   const long long cb = static_cast<long long>(ex_c);
   for (int j = lane; j < np; j += 32) a.patches[static_cast<size_t>(f) * nz + j].patch_id = id0 + j;
+  if (a.desc_head) {  // dense descriptor list: the look-back prefix is the compaction scan
+    const int cam = a.desc_cameras ? a.desc_cameras[f / a.desc_fpc] : 0;
+    const int fr = a.desc_cameras ? f % a.desc_fpc : f;
+    for (int j = lane; j < np; j += 32) {
+      const long long k = static_cast<long long>(ex_p) + j;
+      if (k >= a.desc_cap) continue;
+      tg_descriptor d;
+      d.patch = spatch[j];
+      d.patch.patch_id = ex_p + j;
+      d.camera = cam;
+      d.frame = fr;
+      d.admitted = (d.patch.rect.w <= a.M && d.patch.rect.h <= a.N) ? 1 : 0;
+      d.pad = 0;
+      a.desc[k] = d;
+    }
+  }
   if (lane == 0) {
     a.canvas_base[f] = cb;
     if (f == a.n_frames - 1) plan_totals(a, s_first, ex_p + np, cb + ncv);

@@ -53,6 +53,12 @@ struct PlanArgs {
   uint64_t* look;         // [look_cap] look-back words: epoch | flag | patches | canvases
   int look_cap;           // max_frames
   uint32_t* psync;        // [3] frame ticket, finished CTAs, epoch
+  // optional dense descriptor list: record i = the run's i-th patch
+  tg_descriptor_header* desc_head;  // NULL: no descriptor output
+  tg_descriptor* desc;              // desc_head + 1
+  int64_t desc_cap;
+  const int32_t* desc_cameras;      // camera of frame f: [f / desc_fpc] (NULL: 0)
+  int desc_fpc;
   DevError* err;
 };
 

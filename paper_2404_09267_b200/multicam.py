@@ -5,8 +5,10 @@ One GPU holds a shard of cameras.  Per step:
 1. every camera's frames run through K1 (mask/cells) and K2-K4 (RoIs,
    partition, per-frame plan) on the device -- the per-frame canvases are not
    materialized, the batcher decides canvases across cameras;
-2. the patch descriptors (64 B each) come back to the host -- a few hundred
-   KB, never pixels;
+2. the planner writes every patch as a dense 80-byte descriptor on the
+   device (its frame-order look-back prefix is the compaction scan); the
+   descriptor block comes back to the host -- a few hundred KB, never
+   pixels;
 3. patch ids are renumbered camera-major (sim.hpp:249-251), admission applied
    (sim.hpp:262), per-camera uplink arrivals computed (trace.hpp:255-267) and
    the SLO batcher replays the reference event loop (sim.hpp:334-458);
@@ -14,9 +16,10 @@ One GPU holds a shard of cameras.  Per step:
    the device-resident frames of all cameras.
 
 Across GPUs (config 4) cameras are sharded in contiguous blocks (camera c on
-rank floor(c*G/n)); canvases are shard-local, and the descriptors are
-all-gathered (NCCL through torch.distributed) so every rank holds the global
-patch list in reference order (`gather_descriptors`).
+rank floor(c*G/n)); canvases are shard-local, and the device descriptor
+blocks are all-gathered by the C ABI's communicator (api.Comm: NCCL on the
+device blocks, or a host transport) so every rank holds the global patch
+list in reference order.
 """
 from __future__ import annotations
 
@@ -44,14 +47,65 @@ def shard_cameras(n_cams: int, world: int, rank: int) -> list[int]:
     return [c for c in range(n_cams) if (c * world) // n_cams == rank]
 
 
+def block_bytes(cap: int) -> int:
+    """Bytes of one descriptor block (tg_descriptor_header + cap records)."""
+    return int(N.lib().tg_descriptor_block_bytes(cap))
+
+
+def descriptor_block(records: np.ndarray, cap: int) -> np.ndarray:
+    """Host descriptor block (header + cap records) holding `records`."""
+    records = np.ascontiguousarray(records, DESC_DTYPE)
+    if len(records) > cap:
+        raise ValueError(f"{len(records)} records exceed the block capacity {cap}")
+    blk = np.zeros(block_bytes(cap), np.uint8)
+    blk[:16].view(np.int64)[:] = (len(records), cap)
+    blk[DESC_DTYPE.itemsize:DESC_DTYPE.itemsize * (1 + len(records))] = records.view(np.uint8)
+    return blk
+
+
+def flatten_blocks(ptr: int, n_blocks: int, cap: int, out: np.ndarray | None = None) -> np.ndarray:
+    """Valid records of n_blocks consecutive blocks at host address `ptr`,
+    rank-major (tg_descriptor_blocks_flatten)."""
+    if out is None:
+        out = np.zeros(max(1, n_blocks * cap), DESC_DTYPE)
+    n = C.c_int64()
+    check(N.lib().tg_descriptor_blocks_flatten(ptr, n_blocks, cap, out.ctypes.data, len(out),
+                                               C.byref(n)))
+    return out[:n.value]
+
+
+def allgather_descriptors(comm, records: np.ndarray, cap: int) -> np.ndarray:
+    """All-gathers every rank's host descriptor records through `comm`
+    (api.Comm) as blocks of `cap` records (equal on every rank) and returns
+    them rank-major -- camera-major under contiguous sharding."""
+    blk = descriptor_block(records, cap)
+    world = comm.world
+    if comm.on_device:
+        ctx, nb = comm.ctx, blk.nbytes
+        d_send, d_recv = ctx.malloc(nb), ctx.malloc(nb * world)
+        ctx.upload(d_send, blk)
+        comm.allgather(d_send, nb, d_recv, ctx.stream)
+        got = ctx.download(d_recv, (world * nb,), np.uint8)
+        ctx.free(d_send)
+        ctx.free(d_recv)
+    else:
+        got = np.zeros(blk.nbytes * world, np.uint8)
+        comm.allgather(blk.ctypes.data, blk.nbytes, got.ctypes.data)
+    return flatten_blocks(got.ctypes.data, world, cap).copy()
+
+
 class MultiCameraPath:
     def __init__(self, ctx: Context, cameras, width, height, n_frames, profile, bandwidth_mbps=80.0,
                  gpu_memory_gb=6.0, model_size_gb=2.0, canvas=(1024, 1024), zones=(4, 4),
                  slo_us=1_000_000, fps=30.0, per_camera_link=True, trace_kw=None,
-                 canvas_capacity=None):
+                 canvas_capacity=None, comm=None, cameras_per_rank=None):
+        """`comm` (api.Comm, optional): every pass all-gathers the ranks'
+        descriptor blocks through it; blocks hold `cameras_per_rank` (the
+        largest shard; equal on every rank) x n_frames x zones records."""
         self.ctx, self.cameras, self.W, self.H, self.n = ctx, list(cameras), width, height, n_frames
         self.canvas = canvas
         self.bandwidth, self.per_camera_link = bandwidth_mbps, per_camera_link
+        self.comm = comm
         trace_kw = dict(trace_kw or {})
         self.rings, self.t_us, self.rects = [], [], []
         for c in self.cameras:
@@ -90,79 +144,90 @@ class MultiCameraPath:
         self.canvas_bytes = canvas[0] * canvas[1] * 3
         self.canvas_cap = canvas_capacity
         self.d_canvases = None
+        # the planner's dense descriptor block (device), gathered per pass
+        self.world = comm.world if comm is not None else 1
+        self.cap = max(1, (cameras_per_rank or len(self.cameras))) * n_frames * self.zones
+        self.bb = block_bytes(self.cap)
+        self.d_block = ctx.malloc(self.bb)
+        self.d_cams = ctx.malloc(4 * max(1, len(self.cameras)))
+        if self.cameras:
+            ctx.upload(self.d_cams, np.array(self.cameras, np.int32))
+        self.pipe.set_descriptor_output(self.d_block, self.cap, self.d_cams, n_frames)
+        self.d_blocks = ctx.malloc(self.world * self.bb) if comm is not None and comm.on_device \
+            else None
         # K1-K4 and the descriptor read-back; high priority, so pass i+1's
         # planner CTAs run ahead of pass i's pending K5 CTAs and the host gets
         # the descriptors without waiting for the gather
         self.stream = ctx.new_stream(high_priority=True)
         self.gstream = ctx.new_stream()  # K5 (event canvases)
         self._gdone = ctx.event()
-        # pinned landing zone of the descriptor read-back: patches, admission, counts
-        # (two of them: pass i+1's read-back lands while pass i's is compacted)
-        nslot = len(self.cameras) * n_frames * self.zones
-        self._hbytes = (nslot * 64 + nslot + 4 * len(self.cameras) * n_frames + 255) & ~255
-        self._h = ctx.malloc_host(max(1, 2 * self._hbytes))
+        # pinned landing zone of the read-back, two of them: pass i+1's
+        # read-back lands while pass i's is scheduled
+        self._hslot = self.world * self.bb
+        self._h = ctx.malloc_host(2 * self._hslot)
         self._fetched = [ctx.event(), ctx.event()]
-        self._cams = np.array(self.cameras, np.int32)
-        self._desc = np.zeros(max(1, nslot), DESC_DTYPE)
+        self._desc = np.zeros(self.world * self.cap, DESC_DTYPE)
+        self._nev, self._last = 0, {"patches": np.zeros(0, PATCH_DTYPE)}
 
     def close(self):
         self.pipe.close()
         for r in self.rings:
             r.close()
-        for p in (self.d_cur, self.d_prev, self.d_ids, self.d_gen, self.d_frames):
+        for p in (self.d_cur, self.d_prev, self.d_ids, self.d_gen, self.d_frames, self.d_block,
+                  self.d_cams):
             self.ctx.free(p)
+        if self.d_blocks:
+            self.ctx.free(self.d_blocks)
         if self.d_canvases:
             self.ctx.free(self.d_canvases)
         self.ctx.free_host(self._h)
         self.sched.close()
 
-    # ---- 1. device: K1-K4 for every camera --------------------------------
+    # ---- 1. device: K1-K4 for every camera, descriptors on the device -------
     def run_planes(self):
-        if not self.cameras:
-            return
         lib, F = N.lib(), len(self.cameras) * self.n
         check(lib.tg_pipeline_stage_mask(self.pipe.handle, F, self.d_cur, self.d_prev, self.stream))
         check(lib.tg_pipeline_stage_plan(self.pipe.handle, F, self.d_ids, self.d_gen, 0,
                                          self.stream))
 
-    # ---- 2. descriptors to the host ----------------------------------------
+    # ---- 2. descriptor blocks: all-gather (NCCL) and read-back ---------------
     def fetch_descriptors(self, slot: int = 0):
-        """Enqueues the read-back of the planes' patch slots into pinned
-        buffer `slot` on `stream` (after the planes, before anything later)."""
-        Z, F = self.zones, len(self.cameras) * self.n
-        if not F:
-            return
-        v, h = self.pipe.views, self._h + slot * self._hbytes
-        self.ctx.memcpy(h, v.patches, F * Z * 64, 1, self.stream)
-        self.ctx.memcpy(h + F * Z * 64, v.admitted, F * Z, 1, self.stream)
-        self.ctx.memcpy(h + F * Z * 65, v.n_patches, F * 4, 1, self.stream)
+        """Enqueues, on `stream` after the planes: the NCCL all-gather of the
+        ranks' device blocks (device communicator) and the read-back of the
+        gathered blocks -- or of this rank's block -- into pinned slot `slot`."""
+        h = self._h + slot * self._hslot
+        if self.d_blocks is not None:
+            check(N.lib().tg_descriptors_allgather(self.comm.handle, self.d_block, self.cap,
+                                                   self.d_blocks, self.stream))
+            self.ctx.memcpy(h, self.d_blocks, self.world * self.bb, 1, self.stream)
+        else:
+            self.ctx.memcpy(h, self.d_block, self.bb, 1, self.stream)
         self.ctx.record(self._fetched[slot], self.stream)
 
     def compact_descriptors(self, slot: int = 0) -> np.ndarray:
-        """Waits for read-back `slot` and compacts it (tg_descriptors_compact)
-        into DESC_DTYPE records; the view is valid until the next call."""
-        Z, F = self.zones, len(self.cameras) * self.n
-        if not F:
-            return self._desc[:0]
+        """Waits for read-back `slot` and returns the gathered records
+        (DESC_DTYPE, rank-major = camera-major); with a host communicator the
+        ranks' blocks are exchanged here.  The view is valid until the next
+        call."""
         self.ctx.event_sync(self._fetched[slot])
-        h = self._h + slot * self._hbytes
-        n = C.c_int64()
-        check(N.lib().tg_descriptors_compact(h, h + F * Z * 65, h + F * Z * 64, Z,
-                                             self._cams.ctypes.data, len(self.cameras), self.n,
-                                             self._desc.ctypes.data, len(self._desc), C.byref(n)))
-        return self._desc[:n.value]
+        h = self._h + slot * self._hslot
+        if self.comm is not None and self.d_blocks is None:  # host transport
+            mine = C.string_at(h, self.bb)
+            C.memmove(h, b"".join(self.comm.allgather_bytes(mine)), self._hslot)
+        return flatten_blocks(h, self.world, self.cap, self._desc)
 
     def descriptors(self) -> np.ndarray:
-        """DESC_DTYPE records of every patch of the shard, camera-major,
-        frame order, zone order (ids numbered over the shard; `schedule`
-        renumbers them over the whole camera set).  Waits for the planes."""
+        """DESC_DTYPE records of every patch of every rank's shard (this
+        shard's alone without a communicator), camera-major, frame order,
+        zone order (ids numbered per shard; `schedule` renumbers them over
+        the whole camera set).  Waits for the planes."""
         self.fetch_descriptors(0)
         return self.compact_descriptors(0)
 
     # ---- 3. host: ids, admission, links, batcher ----------------------------
     def schedule(self, desc: np.ndarray):
-        """Renumbers patch ids camera-major, keeps admitted patches and
-        replays the batcher; returns the number of invoke events."""
+        """Renumbers patch ids camera-major, keeps this shard's admitted
+        patches and replays the batcher; returns the number of invoke events."""
         self._nev, self.arrival, self._last = schedule_descriptors(
             self.sched, desc, self.cameras, self.n, self.bandwidth, self.per_camera_link)
         return self._nev
@@ -188,14 +253,13 @@ class MultiCameraPath:
         self.ctx.record(self._gdone, self.gstream)
         check(N.lib().tg_stream_wait_event(self.ctx.handle, self.stream, self._gdone))
 
-    def run_pipelined(self, steps: int, exchange=None) -> int:
+    def run_pipelined(self, steps: int) -> int:
         """`steps` passes over the shard's frames with the host batcher of
         pass i overlapping the device planes (K1-K4) of pass i+1, which are
-        queued behind pass i's descriptor read-back (double-buffered pinned
-        memory), so the device never waits for the host; K5 of pass i runs
-        on `gstream`.  `exchange(desc) -> desc` (e.g. the NCCL
-        descriptor all-gather) runs before each schedule.  Returns the last
-        pass's canvas count; `stream` is joined with every gather."""
+        queued behind pass i's descriptor all-gather and read-back
+        (double-buffered pinned memory), so the device never waits for the
+        host; K5 of pass i runs on `gstream`.  Returns the last pass's canvas
+        count; `stream` is joined with every gather."""
         n_canv = 0
         self.run_planes()
         self.fetch_descriptors(0)
@@ -204,8 +268,6 @@ class MultiCameraPath:
                 self.run_planes()
                 self.fetch_descriptors((i + 1) % 2)
             desc = self.compact_descriptors(i % 2)
-            if exchange is not None:
-                desc = exchange(desc)
             self.schedule(desc)
             n_canv = self.gather(join=False)
         self.join()
@@ -245,25 +307,32 @@ class GlobalCameraPath(MultiCameraPath):
     CUDA IPC (peer reads over NVLink; on one GPU, the same memory).  Each
     rank still runs K1-K4 only on its own cameras.
 
-    `dist` is torch.distributed (gloo or NCCL): it exchanges the rings' IPC
-    handles once, here, and the descriptors every pass (`exchange`)."""
+    `comm` (api.Comm) exchanges the rings' IPC handles once, here, and the
+    descriptor blocks every pass."""
 
-    def __init__(self, ctx: Context, n_cameras: int, rank: int, world: int, dist, width, height,
-                 n_frames, profile, device=None, **kw):
+    def __init__(self, ctx: Context, n_cameras: int, comm, width, height, n_frames, profile, **kw):
+        rank, world = comm.rank, comm.world
+        per_rank = max(len(shard_cameras(n_cameras, world, r)) for r in range(world))
         super().__init__(ctx, shard_cameras(n_cameras, world, rank), width, height, n_frames,
-                         profile, **kw)
+                         profile, comm=comm, cameras_per_rank=per_rank, **kw)
         self.all_cameras = list(range(n_cameras))
-        self.rank, self.world, self.dist, self.device = rank, world, dist, device
-        mine = [(c, ctx.ipc_export(r.base)) for c, r in zip(self.cameras, self.rings)]
-        every = [None] * world
-        dist.all_gather_object(every, mine)
+        self.rank = rank
+        # (camera id, IPC handle of its ring) per owned camera, padded to the
+        # largest shard so every rank sends the same number of bytes
+        rec = np.zeros(per_rank, [("camera", "<i4"), ("handle", "u1", 64)])
+        rec["camera"] = -1
+        for k, (c, r) in enumerate(zip(self.cameras, self.rings)):
+            rec[k] = (c, np.frombuffer(ctx.ipc_export(r.base), np.uint8))
         base, self._imported = {}, []
-        for r, owned in enumerate(every):
-            for c, h in owned:
+        for r, raw in enumerate(comm.allgather_bytes(rec.tobytes())):
+            for c, h in np.frombuffer(raw, rec.dtype):
+                c = int(c)
+                if c < 0:
+                    continue
                 if r == rank:
                     base[c] = self.rings[self.cameras.index(c)].base
                 else:
-                    base[c] = ctx.ipc_import(h)
+                    base[c] = ctx.ipc_import(h.tobytes())
                     self._imported.append(base[c])
         fb = self.rings[0].frame_bytes if self.rings else 3 * width * height
         ptrs = np.array([base[c] + s * fb for c in self.all_cameras for s in range(n_frames + 1)],
@@ -278,9 +347,6 @@ class GlobalCameraPath(MultiCameraPath):
         self._imported = []
         self.ctx.free(self.d_frames_global)
         super().close()
-
-    def exchange(self, desc: np.ndarray) -> np.ndarray:
-        return gather_descriptors(desc, self.dist, device=self.device)
 
     def schedule(self, desc: np.ndarray):
         """`desc`: the all-gathered list of every camera."""
@@ -301,16 +367,6 @@ class GlobalCameraPath(MultiCameraPath):
         if join:
             self.join()
         return n.value
-
-    def step(self):
-        self.run_planes()
-        desc = self.exchange(self.descriptors())
-        n_events = self.schedule(desc)
-        n_canvases = self.gather()
-        return desc, n_events, n_canvases
-
-    def run_pipelined(self, steps: int, exchange=None) -> int:
-        return super().run_pipelined(steps, exchange or self.exchange)
 
 
 def schedule_descriptors(sched, desc: np.ndarray, cameras, n_frames: int, bandwidth_mbps: float,
@@ -338,26 +394,3 @@ def schedule_descriptors(sched, desc: np.ndarray, cameras, n_frames: int, bandwi
     # is already behind its arrival (a metrics flag; scheduling is unchanged)
     infeasible = patches[:k]["deadline_us"] - sched.profile.slack_us(1) < arrival[:k]
     return n_ev.value, arrival[:k], dict(patches=patches[:k], src=src[:k], infeasible=infeasible)
-
-
-def gather_descriptors(local: np.ndarray, dist, device=None) -> np.ndarray:
-    """All-gathers every rank's DESC_DTYPE records (variable counts) and
-    returns them camera-major -- the global patch list in reference order.
-    `dist` is torch.distributed (NCCL on GPUs, gloo on CPU)."""
-    import torch
-    world = dist.get_world_size()
-    raw = torch.from_numpy(local.view(np.uint8).copy())
-    if device is not None:
-        raw = raw.to(device)
-    n = torch.tensor([raw.numel()], dtype=torch.int64, device=raw.device)
-    sizes = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n)
-    cap = int(max(s.item() for s in sizes))
-    buf = torch.zeros(cap, dtype=torch.uint8, device=raw.device)
-    buf[:raw.numel()] = raw
-    parts = [torch.zeros_like(buf) for _ in range(world)]
-    dist.all_gather(parts, buf)
-    recs = [p[:int(s.item())].cpu().numpy().view(DESC_DTYPE) for p, s in zip(parts, sizes)]
-    allrec = np.concatenate(recs) if recs else np.zeros(0, DESC_DTYPE)
-    order = np.lexsort((np.arange(len(allrec)), allrec["camera"]))  # stable, camera-major
-    return allrec[order]

@@ -1,7 +1,7 @@
 // pipeline_test.cpp -- the hot path driven from C++ through the C ABI alone
 // (no Python): synthetic camera frames on the device -> tg_pipeline_run ->
-// descriptors -> SLO batcher (tg_batcher_schedule) -> event canvases
-// (tg_batcher_gather_all).  Every per-frame result and canvas byte is checked
+// device descriptor block -> NCCL all-gather (world size 1) -> SLO batcher
+// (tg_batcher_schedule) -> event canvases (tg_batcher_gather_all).  Every per-frame result and canvas byte is checked
 // against the plain-C oracle (oracle/tangram_oracle.c, test infrastructure)
 // on the same frames; the batcher's canvases against a host fill of its own
 // placements.  Built by tests/cpp/Makefile; run by tests/test_gpu_parity.py.
@@ -89,7 +89,29 @@ int main() {
   OK(tg_malloc_device(ctx, cb * pp.max_canvases, reinterpret_cast<void**>(&d_canv)));
   OK(tg_memcpy_async(ctx, d_ids, ids.data(), 8 * n, 0, nullptr));
   OK(tg_memcpy_async(ctx, d_gen, t_us.data(), 8 * n, 0, nullptr));
+  // the planner's dense device descriptor list
+  const int64_t dcap = static_cast<int64_t>(n) * pp.partition.zones_x * pp.partition.zones_y;
+  const size_t bb = tg_descriptor_block_bytes(dcap);
+  void *d_block = nullptr, *d_blocks = nullptr;
+  int32_t* d_cams = nullptr;
+  const int32_t cam_ids[1] = {7};
+  OK(tg_malloc_device(ctx, bb, &d_block));
+  OK(tg_malloc_device(ctx, bb, &d_blocks));
+  OK(tg_malloc_device(ctx, sizeof(cam_ids), reinterpret_cast<void**>(&d_cams)));
+  OK(tg_memcpy_async(ctx, d_cams, cam_ids, sizeof(cam_ids), 0, nullptr));
+  OK(tg_pipeline_set_descriptor_output(pipe, d_block, dcap, d_cams, n));
   OK(tg_pipeline_run(pipe, n, d_slots + 1, d_slots, d_ids, d_gen, 0, d_canv, nullptr));
+  // the collective: NCCL all-gather of the descriptor blocks (one rank here)
+  tg_comm_id cid;
+  OK(tg_comm_get_unique_id(&cid));
+  tg_comm* comm = nullptr;
+  OK(tg_comm_create(ctx, &cid, 0, 1, &comm));
+  int32_t c_rank = -1, c_world = 0, c_dev = 0;
+  OK(tg_comm_info(comm, &c_rank, &c_world, &c_dev));
+  CHECK(c_rank == 0 && c_world == 1 && c_dev == 1);
+  OK(tg_descriptors_allgather(comm, d_block, dcap, d_blocks, tg_ctx_stream(ctx)));
+  std::vector<uint8_t> hblocks(bb);
+  OK(tg_memcpy_async(ctx, hblocks.data(), d_blocks, bb, 1, nullptr));
 
   tg_pipeline_views v;
   OK(tg_pipeline_device_views(pipe, &v));
@@ -154,12 +176,17 @@ int main() {
   }
   CHECK(std::memcmp(canv.data(), o_canv.data(), canv.size()) == 0);
 
-  // ---- SLO batcher over the descriptors, canvases on the device -----------
-  std::vector<tg_descriptor> desc(static_cast<size_t>(n) * Z);
-  int64_t nd = 0;
-  const int32_t cams[1] = {0};
+  // ---- SLO batcher over the gathered descriptors, canvases on the device ---
+  // the device list equals the host compaction of the per-frame slots
+  std::vector<tg_descriptor> desc(static_cast<size_t>(n) * Z), hdesc(desc.size());
+  int64_t nd = 0, nh = 0;
+  const int32_t* cams = cam_ids;
+  OK(tg_descriptor_blocks_flatten(hblocks.data(), 1, dcap, desc.data(),
+                                  static_cast<int64_t>(desc.size()), &nd));
   OK(tg_descriptors_compact(patches.data(), n_patches.data(), admitted.data(), Z, cams, 1, n,
-                            desc.data(), static_cast<int64_t>(desc.size()), &nd));
+                            hdesc.data(), static_cast<int64_t>(hdesc.size()), &nh));
+  CHECK(nd == nh && nd > 0);
+  CHECK(std::memcmp(desc.data(), hdesc.data(), sizeof(tg_descriptor) * nd) == 0);
   const tg_profile_entry prof[4] = {{1, 60.0, 3.0}, {2, 85.0, 4.0}, {4, 135.0, 6.0},
                                     {8, 235.0, 10.0}};
   tg_batcher* b = nullptr;
@@ -205,11 +232,13 @@ int main() {
   CHECK(k == nbc);
 
   tg_batcher_destroy(b);
+  tg_comm_destroy(comm);
   tg_pipeline_destroy(pipe);
   for (void* ptr : {static_cast<void*>(ring), static_cast<void*>(d_rects),
                     static_cast<void*>(d_offs), static_cast<void*>(d_slots),
                     static_cast<void*>(d_ids), static_cast<void*>(d_gen),
-                    static_cast<void*>(d_canv), static_cast<void*>(d_bcanv)})
+                    static_cast<void*>(d_canv), static_cast<void*>(d_bcanv), d_block, d_blocks,
+                    static_cast<void*>(d_cams)})
     OK(tg_free_device(ctx, ptr));
   tg_ctx_destroy(ctx);
   std::printf("%lld per-frame canvases, %d invoke events, %lld event canvases: %s\n",

@@ -3,7 +3,9 @@
 Each rank owns a contiguous block of cameras, builds its cameras' patch
 descriptors (here from the oracle partition of the generator's rects, which
 the device partition equals bit for bit -- test_gpu_parity), all-gathers them
-and checks that every rank holds the global camera-major list; then each
+as descriptor blocks through the C ABI's communicator with a host transport
+(tg_comm_create_host; gloo moves the bytes) and checks that every rank holds
+the global camera-major list (block layout, headers, flattening); then each
 rank batches its shard with the SLO batcher and must reproduce the
 reference simulator (tangram::run) run on exactly that shard's scenes.
 """
@@ -51,13 +53,27 @@ def descriptors(cameras):
     return np.array(recs, MC.DESC_DTYPE)
 
 
+def gloo_comm(rank, world):
+    """api.Comm over a host transport: gloo all-gathers the byte strings."""
+    import torch
+
+    def allgather(data: bytes):
+        t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        return [p.numpy().tobytes() for p in parts]
+    return A.Comm.host(rank, world, allgather)
+
+
 def _worker(rank, world, port, q):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
         mine = MC.shard_cameras(N_CAMS, world, rank)
         local = descriptors(mine)
-        glob = MC.gather_descriptors(local, dist)
+        comm = gloo_comm(rank, world)
+        per_rank = max(len(MC.shard_cameras(N_CAMS, world, r)) for r in range(world))
+        glob = MC.allgather_descriptors(comm, local, per_rank * N_FRAMES * 16)
         full = descriptors(range(N_CAMS))
         same = (glob.tobytes() == full.tobytes())
         sched = A.SloScheduler(A.CanvasSpec(1024, 1024), A.LatencyProfile(1024, 1024, PROFILE),
@@ -96,6 +112,7 @@ def _worker(rank, world, port, q):
             ref_inf = [f for f, a in zip(r["infeasible"], r["admitted"]) if a]
             same = same and [bool(x) for x in plan_all["infeasible"]] == [bool(x) for x in ref_inf]
         q.put((rank, mine, same, len(glob), evs, ref))
+        comm.close()
         dist.destroy_process_group()
     except Exception as e:  # surface worker failures in the parent
         q.put((rank, None, repr(e), 0, None, None))
@@ -136,3 +153,39 @@ def test_two_rank_descriptor_allgather_and_shard_batching():
         if ref is not None:
             assert evs == ref, f"rank {rank}: shard batching differs from the reference simulator"
     assert sorted(c for _, mine, *_ in res for c in mine) == list(range(N_CAMS))
+
+
+def test_descriptor_blocks_round_trip():
+    """Host blocks: header (count, cap) + records; flattening concatenates
+    the valid records of every block and rejects corrupt headers."""
+    import ctypes as C
+    recs = descriptors([0, 1])
+    a, b = recs[:7], recs[7:20]
+    buf = np.concatenate([MC.descriptor_block(a, 32), MC.descriptor_block(b, 32)])
+    assert buf.nbytes == 2 * MC.block_bytes(32) == 2 * 80 * 33
+    got = MC.flatten_blocks(buf.ctypes.data, 2, 32)
+    assert got.tobytes() == np.concatenate([a, b]).tobytes()
+    assert len(MC.flatten_blocks(MC.descriptor_block(recs[:0], 4).ctypes.data, 1, 4)) == 0
+    bad = MC.descriptor_block(a, 32)
+    bad[:8].view(np.int64)[0] = 33
+    with pytest.raises(A.InvalidArgument, match="holds 33 records"):
+        MC.flatten_blocks(bad.ctypes.data, 1, 32)
+    with pytest.raises(A.CapacityError):
+        MC.flatten_blocks(buf.ctypes.data, 2, 32, out=np.zeros(10, MC.DESC_DTYPE))
+    with pytest.raises(ValueError):
+        MC.descriptor_block(recs, 4)
+    del C
+
+
+def test_host_comm_single_rank_and_failing_transport():
+    comm = A.Comm.host(0, 1, lambda data: [data])
+    recs = descriptors([3])
+    assert MC.allgather_descriptors(comm, recs, len(recs)).tobytes() == recs.tobytes()
+    assert comm.allgather_bytes(b"abc") == [b"abc"]
+    comm.close()
+    broken = A.Comm.host(0, 2, lambda data: [data])  # returns one part for two ranks
+    with pytest.raises(A.TangramError, match="host transport failed"):
+        broken.allgather_bytes(b"xy")
+    broken.close()
+    with pytest.raises(A.InvalidArgument):
+        A.Comm.host(2, 2, lambda d: [d, d])

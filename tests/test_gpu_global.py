@@ -30,7 +30,15 @@ def _worker(rank, world, port, q):
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
         ctx = A.Context(0)
-        path = MC.GlobalCameraPath(ctx, N_CAMS, rank, world, dist, W, H, N_FRAMES, PROFILE,
+        import torch
+
+        def allgather(data: bytes):  # host transport: NCCL refuses two ranks on one GPU
+            t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+            parts = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(parts, t)
+            return [p.numpy().tobytes() for p in parts]
+        comm = A.Comm.host(rank, world, allgather)
+        path = MC.GlobalCameraPath(ctx, N_CAMS, comm, W, H, N_FRAMES, PROFILE,
                                    bandwidth_mbps=BW, trace_kw=dict(roi_proportion_mean=0.15))
         desc, n_events, n_canv = path.step()
         ctx.stream_sync(path.stream)
@@ -75,6 +83,7 @@ def _worker(rank, world, port, q):
         q.put((rank, evs, scenes, k == n_canv, bad, n_canv))
         dist.barrier()
         path.close()
+        comm.close()
         ctx.close()
         dist.destroy_process_group()
     except Exception as e:  # surface worker failures in the parent

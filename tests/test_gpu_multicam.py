@@ -113,3 +113,55 @@ def test_event_subsets_partition_the_canvases(ctx):
             assert n.value == len(want)
             assert np.array_equal(path.canvases(n.value), want)
     path.close()
+
+
+def test_device_descriptor_list_equals_host_compaction(ctx):
+    """The planner's dense device descriptors (look-back prefix as the
+    compaction scan) equal the host compaction of the per-frame slots,
+    record for record, for a multi-camera shard."""
+    import ctypes as C
+
+    from paper_2404_09267_b200 import _native as N
+    cams = [4, 5, 6]
+    path = MC.MultiCameraPath(ctx, cams, 1920, 1080, 9, PROFILE, bandwidth_mbps=40.0,
+                              trace_kw=dict(roi_proportion_mean=0.2))
+    path.run_planes()
+    desc = path.descriptors().copy()
+    F, Z = len(cams) * 9, path.zones
+    res = path.pipe.results(F, path.stream)
+    patches = np.ctypeslib.as_array(C.cast(res["patches"], C.POINTER(C.c_uint8)),
+                                    shape=(F * Z * 64,)).copy()
+    out = np.zeros(F * Z, MC.DESC_DTYPE)
+    n = C.c_int64()
+    A.check(N.lib().tg_descriptors_compact(patches.ctypes.data, res["n_patches"].ctypes.data,
+                                           np.ascontiguousarray(res["admitted"]).ctypes.data, Z,
+                                           np.array(cams, np.int32).ctypes.data, len(cams), 9,
+                                           out.ctypes.data, len(out), C.byref(n)))
+    assert n.value == len(desc) > 0
+    assert out[:n.value].tobytes() == desc.tobytes()
+    assert list(np.unique(desc["camera"])) == cams
+    path.close()
+
+
+def test_nccl_single_rank_comm_matches_local_path(ctx):
+    """With an NCCL communicator (one rank) the descriptor blocks go through
+    ncclAllGather on the device; events and canvases equal the local path."""
+    cams = [0, 1]
+    local = MC.MultiCameraPath(ctx, cams, 1920, 1080, 8, PROFILE, bandwidth_mbps=40.0,
+                               trace_kw=dict(roi_proportion_mean=0.15))
+    _, ne, nc = local.step()
+    ctx.stream_sync(local.stream)
+    want_ev = [(e.fire_time_us, e.trigger, e.batch_size, e.patch_ids) for e in local.events()]
+    want = local.canvases(nc)
+    local.close()
+    comm = A.Comm.nccl(ctx, A.Comm.unique_id(), 0, 1)
+    path = MC.MultiCameraPath(ctx, cams, 1920, 1080, 8, PROFILE, bandwidth_mbps=40.0,
+                              trace_kw=dict(roi_proportion_mean=0.15), comm=comm)
+    assert path.d_blocks is not None
+    got_n = path.run_pipelined(2)
+    ctx.stream_sync(path.stream)
+    assert got_n == nc
+    assert [(e.fire_time_us, e.trigger, e.batch_size, e.patch_ids) for e in path.events()] == want_ev
+    assert np.array_equal(path.canvases(nc), want)
+    path.close()
+    comm.close()

@@ -675,3 +675,21 @@ def test_chunked_runs_continue_patch_ids_on_device(ctx):
     assert got_pl == whole["placement_list"]
     assert np.array_equal(np.concatenate(got_canv), want_canv)
     run.close()
+
+
+def test_plan_look_back_survives_epoch_wrap(ctx):
+    """Look-back words carry a 16-bit launch epoch and are zeroed every 32768
+    launches: after more than 65536 plan launches on one pipeline, patch ids
+    and canvas numbering are still exact (a stale word from 65536 launches
+    ago must never pass for a fresh one)."""
+    from paper_2404_09267_b200 import _native as N
+    run = GpuRun(ctx, 640, 368, 12, seed=77, keep_mask=False, trace_kw=dict(roi_max_dim=200))
+    want = run.run()
+    lib = N.lib()
+    for _ in range(65536 + 7):  # plan stage alone, one frame: every launch moves the epoch
+        A.check(lib.tg_pipeline_stage_plan(run.pipe.handle, 1, run.d_ids, run.d_gen, 0, None))
+    got = run.run()
+    assert got["patch_list"] == want["patch_list"]
+    assert got["placement_list"] == want["placement_list"]
+    assert got["total_canvases"] == want["total_canvases"]
+    run.close()
