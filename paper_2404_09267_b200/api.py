@@ -846,6 +846,34 @@ class SloScheduler:
     def idle(self) -> bool:
         return self._status()[0] == 0
 
+    def _current(self):
+        lib, info = N.lib(), N.tg_invoke_info()
+        check(lib.tg_batcher_current(self.handle, C.byref(info), None, None, None))
+        q = (N.tg_patch_meta * max(1, info.n_patches))()
+        pl = (N.tg_placement * max(1, info.n_patches))()
+        fr = (N.tg_free_rect * max(1, info.n_free))()
+        check(lib.tg_batcher_current(self.handle, C.byref(info), q, pl, fr))
+        return info, q, pl, fr
+
+    def queue(self) -> list[PatchMeta]:
+        """The queued patches in arrival order (scheduler.hpp:137)."""
+        info, q, _, _ = self._current()
+        return [_py_patch(q[i]) for i in range(info.n_patches)]
+
+    def current_stitch(self) -> StitchResult:
+        """The live batch's packing (scheduler.hpp:138)."""
+        info, _, pl, fr = self._current()
+        res = StitchResult(spec=self.spec, canvases=[CanvasState() for _ in range(info.batch_size)])
+        for k in range(info.n_patches):
+            p = Placement(pl[k].patch_id, pl[k].canvas_index, _py_rect(pl[k].position))
+            cs = res.canvases[p.canvas_index]
+            cs.placements.append(p)
+            cs.used_area += area(p.position)
+            res.placement_index[p.patch_id] = p
+        for k in range(info.n_free):
+            res.canvases[fr[k].canvas_index].free_rects.append(_py_rect(fr[k].rect))
+        return res
+
     def queue_size(self) -> int:
         return self._status()[0]
 

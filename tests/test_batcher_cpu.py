@@ -47,6 +47,7 @@ def test_second_arrival_rearms_with_batch_slack():
     stale = s.pending_timer().epoch
     assert s.on_patch_arrival(full_patch(2, 100_000, 500_000), 100_000) == []
     assert s.queue_size() == 2 and s.current_canvas_count() == 2
+    assert [p.patch_id for p in s.queue()] == [1, 2] and s.current_stitch().canvas_count() == 2
     assert s.remaining_time_us() == 300_000 and s.pending_timer().fire_at_us == 300_000
     assert s.on_timer(370_000, stale) is None
     ev = s.on_timer(300_000, s.pending_timer().epoch)
