@@ -114,6 +114,9 @@ def load(lib: str = "port") -> C.CDLL:
         dll.orc_synth_frame.restype = None
         dll.orc_synth_frame.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int32, P(Rect),
                                         C.c_int, C.c_void_p]
+        dll.orc_synth_rect.restype = None
+        dll.orc_synth_rect.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int32, P(Rect), C.c_int,
+                                       Rect, C.c_void_p, C.c_int]
         dll.orc_mask.restype = None
         dll.orc_mask.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                  C.c_int, C.c_void_p]
@@ -265,6 +268,30 @@ def synth_frame(width, height, pixel_seed, t, rects, pitch=None):
     arr = (Rect * max(1, len(rects)))(*[Rect(*r) for r in rects])
     dll.orc_synth_frame(width, height, pitch, pixel_seed, t, arr, len(rects), out.ctypes.data)
     return out
+
+
+def synth_rect(width, height, pixel_seed, t, rects, region, out=None):
+    """Pixels (h, 3w) of `region` = (x, y, w, h) of synthetic frame t: the
+    bytes synth_frame would write there."""
+    dll = load("port")
+    x, y, w, h = region
+    if out is None:
+        out = np.empty((h, 3 * w), np.uint8)
+    arr = (Rect * max(1, len(rects)))(*[Rect(*r) for r in rects])
+    dll.orc_synth_rect(width, height, pixel_seed, t, arr, len(rects), Rect(x, y, w, h),
+                       out.ctypes.data, out.strides[0])
+    return out
+
+
+def synth_frames(width, height, pixel_seed, rects_per_frame, threads=None):
+    """Background frame (t = -1) then frames 0..n-1, synthesized in parallel."""
+    from concurrent.futures import ThreadPoolExecutor
+    threads = threads or os.cpu_count() or 1
+    n = len(rects_per_frame)
+    with ThreadPoolExecutor(threads) as ex:
+        return list(ex.map(lambda i: synth_frame(width, height, pixel_seed, i,
+                                                 rects_per_frame[i] if i >= 0 else []),
+                           range(-1, n)))
 
 
 def mask(cur, prev, width, height, threshold=25, radius=2):

@@ -426,6 +426,50 @@ void orc_synth_frame(int W, int H, int pitch, uint64_t pixel_seed, int32_t t,
   }
 }
 
+/* The pixels of `region` of synthetic frame t, exactly as orc_synth_frame
+ * would write them, without materializing the frame: a pixel is foreground
+ * iff it lies in one of frame t's rects.  Used to compose batched canvases
+ * from many cameras' frames (configs 3/4) without holding every frame. */
+void orc_synth_rect(int W, int H, uint64_t pixel_seed, int32_t t, const orc_rect* rects,
+                    int n_rects, orc_rect region, uint8_t* out, int out_pitch) {
+  const uint32_t s_bg = (uint32_t)pixel_seed;
+  const uint32_t s_fg = orc_hash32(s_bg ^ 0x5bd1e995u);
+  const uint32_t tn = orc_hash32((uint32_t)(pixel_seed >> 32) + (uint32_t)t);
+  const uint32_t tf = s_fg ^ ((uint32_t)t * 0x9E3779B9u);
+  uint8_t* fg = (uint8_t*)calloc((size_t)(region.w > 0 ? region.w : 1), 1);
+  (void)H;
+  for (int yy = 0; yy < region.h; ++yy) {
+    const int y = region.y + yy;
+    memset(fg, 0, (size_t)(region.w > 0 ? region.w : 1));
+    if (t >= 0) {
+      for (int k = 0; k < n_rects; ++k) {
+        const orc_rect r = rects[k];
+        if (y < r.y || y >= r.y + r.h) continue;
+        const int a = r.x > region.x ? r.x : region.x;
+        const int b = (r.x + r.w) < (region.x + region.w) ? (r.x + r.w) : (region.x + region.w);
+        for (int x = a; x < b; ++x) fg[x - region.x] = 1;
+      }
+    }
+    uint8_t* row = out + (size_t)yy * (size_t)out_pitch;
+    for (int xx = 0; xx < region.w; ++xx) {
+      const int x = region.x + xx;
+      for (int c = 0; c < 3; ++c) {
+        const uint32_t idx = (uint32_t)(((uint32_t)y * (uint32_t)W + (uint32_t)x) * 3u + (uint32_t)c);
+        int base;
+        if (fg[xx]) {
+          const int h = (int)(orc_hash32(idx ^ tf) & 15u);
+          base = (t & 1) ? 224 - h : 32 + h;
+        } else {
+          base = 96 + (int)(orc_hash32(idx ^ s_bg) & 63u);
+        }
+        const int v = base + (int)(orc_hash32(idx ^ tn) % 7u) - 3;
+        row[xx * 3 + c] = (uint8_t)(v < 0 ? 0 : (v > 255 ? 255 : v));
+      }
+    }
+  }
+  free(fg);
+}
+
 /* fg0(x,y) = max_c |cur-prev| > T; fg = square (2r+1)^2 dilation of fg0 with
  * everything outside the frame counted as background. */
 void orc_mask(const uint8_t* cur, const uint8_t* prev, int W, int H, int pitch, int T, int r,

@@ -106,6 +106,10 @@ uint32_t orc_hash32(uint32_t x);
 /* Frame t of a synthetic camera; t = -1 is the background-only frame. */
 void orc_synth_frame(int width, int height, int pitch, uint64_t pixel_seed, int32_t t,
                      const orc_rect* rects, int n_rects, uint8_t* out);
+/* Pixels of `region` of frame t (same bytes as orc_synth_frame), rows of
+ * out_pitch bytes. */
+void orc_synth_rect(int width, int height, uint64_t pixel_seed, int32_t t, const orc_rect* rects,
+                    int n_rects, orc_rect region, uint8_t* out, int out_pitch);
 /* Dilated foreground mask, one bit per pixel, rows of ceil(W/32) words. */
 void orc_mask(const uint8_t* cur, const uint8_t* prev, int width, int height, int pitch,
               int threshold, int radius, uint32_t* mask);
