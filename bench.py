@@ -2,23 +2,27 @@
 """Headline benchmark: 4K frames/s through Tangram's frame->canvas path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg4|cfg2|cfg3|cfg5]
 
-Workload (BASELINE.json configs[1]): per GPU one synthetic 3840x2160 RGB
-camera, 300 frames, moderate RoI density (generate_trace defaults with
-roi_proportion_mean=0.10, roi_max_dim=480, fps=30, seed 1000+camera), 4x4
-zone grid, 1024x1024 canvases.  A step is one pass of the whole path over the
-camera's 300 device-resident frames: K1 mask + cells -> K2-K4 planner with the
-frame-order prefix -> K5 canvas gather (three launches).  Per-frame stitching
-has no cross-camera exchange, so at N>1 every rank runs its own camera with
-no collective in the step.  Inputs (7.5 GB per GPU) are far larger than L2,
-so no flush is needed.  --config cfg3|cfg4|cfg5 run the other BASELINE
-configurations (multi-camera SLO batching with the NCCL descriptor
-all-gather at N>1, and the density sweep).
+Default workload (BASELINE.json configs[3], the configuration the metric's
+1/2/4/8-GPU scaling is quoted on): 64 synthetic 3840x2160 RGB cameras, 30
+frames each (generate_trace with roi_proportion_mean=0.10, roi_max_dim=480,
+fps=30, seed 1000+camera), 4x4 zones, 1024x1024 canvases, camera c on rank
+floor(c*N/64).  A step is one pass over the shard: K1 mask + cells for every
+camera's frames (one launch), K2-K4 planner writing the dense device
+descriptor list (one launch), the NCCL all-gather of the ranks' descriptor
+blocks (N > 1), the host SLO batcher (the reference's SloScheduler, shard-
+local canvases) and one K5 launch writing every invoke event's canvases.
+The host batcher of pass i overlaps the device planes of pass i+1.  Frames
+(49 GB at N=1) are far larger than L2: no flush is needed.
 
-`value` is whole-job device throughput (frames/s, max-over-ranks time),
-`e2e` the same through the public API with pinned host frames copied in and
-descriptors copied out every step, `roofline` K1 against measured HBM
-bandwidth, `cpu_baseline` the CPU path on the box's cores.
+`value` is whole-job device throughput (frames/s over every rank's frames,
+max-over-ranks time), `e2e` the same through the public API with the frames
+copied in from pinned host memory every step, `roofline` K1 (the dominant
+kernel) against the measured HBM bandwidth, `path` the step's unique bytes
+against the same peak, `cpu_baseline` the CPU path on the box's cores, and
+`secondary.cfg2` the per-frame path of configs[1] (one camera x 300 frames
+per GPU).  --config selects the other BASELINE configurations as the line.
 """
 from __future__ import annotations
 
@@ -38,31 +42,44 @@ sys.path.insert(0, ROOT)
 
 W, H, C = 3840, 2160, 3
 FRAME_BYTES = W * H * C
+CANVAS_BYTES = 1024 * 1024 * 3
 METRIC = "4K frames/sec (RoI->patch->stitched canvas)"
-WORKLOAD = ("BASELINE configs[1]: synthetic 3840x2160 RGB camera per GPU, 300 frames, moderate "
-            "RoI density (roi_proportion_mean=0.10, roi_max_dim=480), 4x4 zones, 1024x1024 canvases")
+TRACE = dict(roi_proportion_mean=0.10, roi_max_dim=480)
+# SURVEY Appendix P3 batcher setting: mu = 60 + 25 k ms, sigma = 0.05 mu,
+# 1e6 Mbps links, 80 GB GPU with a 4 GB model (76 canvases per batch).
+SIM_PROFILE = [(k, 60.0 + 25.0 * k, 0.05 * (60.0 + 25.0 * k)) for k in (1, 2, 4, 8, 16, 32, 64)]
+SIM = dict(bandwidth_mbps=1e6, gpu_memory_gb=80.0, model_size_gb=4.0)
+SAMPLE_EVERY = 4  # stage events on every 4th timed step (an event costs a few us)
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--frames", type=int, default=300)
+    ap.add_argument("--config", default="cfg4", choices=["cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="cfg4 (default, the headline): 64 cameras x 30 frames sharded over the "
+                         "ranks, SLO batcher; cfg2: per-frame path, 1 camera x 300 frames per GPU; "
+                         "cfg3: 5 cameras x 300 frames batched on 1 GPU; cfg5: RoI-density sweep")
+    ap.add_argument("--frames", type=int, default=None, help="frames per camera (config default)")
+    ap.add_argument("--cams", type=int, default=None, help="cameras (config default)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"],
-                    help="cfg2 (default, the headline): per-frame path, 1 camera x 300 frames per "
-                         "GPU; cfg3: 5 cameras batched across cameras on 1 GPU; cfg4: 64 cameras "
-                         "sharded over the ranks; cfg5: RoI-density sweep")
+    ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--global-batching", action="store_true",
                     help="cfg3/cfg4 at N>1: one batcher over every camera (the reference's single "
                          "scheduler), replicated per rank; rank r writes invoke events r, r+N, ... "
                          "reading peer frames over CUDA IPC / NVLink (default: shard-local)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    dflt = {"cfg2": (1, 300), "cfg3": (5, 300), "cfg4": (64, 30), "cfg5": (8, 60)}[a.config]
+    a.cams = a.cams or dflt[0]
+    a.frames = a.frames or dflt[1]
+    return a
 
 
+# ================================================================ plumbing
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -109,11 +126,20 @@ def make_comm(A, ctx, dist, rank: int, world: int):
 
 def reduce_max(dist, value: float, local: int) -> float:
     """Max over ranks (device tensor on NCCL, host tensor on gloo)."""
+    if dist is None:
+        return value
     import torch
     dev = "cpu" if dist.get_backend() == "gloo" else f"cuda:{gpu_of(local)}"
-    t = torch.tensor([value], device=dev)
+    t = torch.tensor([value], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        import torch
+        torch.cuda.synchronize()
+        dist.barrier()
 
 
 def bind_to_gpu_numa(local: int) -> None:
@@ -135,6 +161,30 @@ def peaks():
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def host_cpu() -> dict:
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"lscpu_model": model, "nproc": os.cpu_count() or 1}
+
+
+def ncu_traffic(name: str, units: int):
+    """DRAM bytes of one launch from a committed ncu capture (profiles/),
+    scaled by the launch's units (frames); None when absent."""
+    p = os.path.join(ROOT, "profiles", name)
+    try:
+        with open(p) as f:
+            return json.load(f)["dram_bytes_per_frame"] * units
+    except Exception:
+        return None
 
 
 class Clocks:
@@ -185,28 +235,215 @@ class Clocks:
                 "samples": len(sm)}
 
 
-# ================================================================== ours
-def run_ours(args):
+def roofline(kernel: str, bytes_per_launch: float, launch_ms: float, traffic, note: str) -> dict:
+    peak, src = peaks()
+    achieved = bytes_per_launch / (launch_ms / 1e3) / 1e9
+    return {"bound": "hbm", "kernel": kernel, "achieved": round(achieved, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "traffic": traffic, "algorithmic_bytes_per_launch": int(bytes_per_launch),
+            "launch_ms": round(launch_ms, 4), "peak_source": src, "bytes": note}
+
+
+def path_record(unique_bytes: int, ms_step: float, b_run: int, stage_ms: dict, extra: dict) -> dict:
+    peak, _ = peaks()
+    gbps = unique_bytes / (ms_step / 1e3) / 1e9
+    rec = {"unique_bytes_per_step": int(unique_bytes), "unique_GBps": round(gbps, 1),
+           "unique_frac": round(gbps / peak, 4),
+           "unique_bytes_def": "frames read once each (cur chains, one background per camera) + "
+                               "admitted patch pixels read + every canvas byte written",
+           "B_run_model_bytes": int(b_run),
+           "B_run_def": "SURVEY §8(d) model: 2*W*H*C per frame (cur + prev counted separately) + "
+                        "patch bytes + canvas bytes; a model figure, not a roofline fraction "
+                        "(K1 reads each frame once)",
+           "stage_ms": stage_ms}
+    rec.update(extra)
+    return rec
+
+
+# ============================================================ configs 3/4
+def run_multicam(args):
+    """Configs 3/4 on N ranks: cameras sharded in contiguous blocks, the
+    device descriptor blocks all-gathered over NCCL (N > 1), the SLO batcher
+    per shard, every invoke event's canvases written by K5."""
     rank, world, local = dist_env()
     if world > 1:
         bind_to_gpu_numa(gpu_of(local))
-    dist = None
-    if world > 1:
-        import torch
-        dist = init_dist(local)
+    dist = init_dist(local) if world > 1 else None
     from paper_2404_09267_b200 import api as A
-    from paper_2404_09267_b200 import _native as N
-
-    n = args.frames
+    from paper_2404_09267_b200 import multicam as MC
+    n_cams_total, n = args.cams, args.frames
+    cams = MC.shard_cameras(n_cams_total, world, rank)
     ctx = A.Context(gpu_of(local))
-    camera = rank
-    seed = 1000 + camera
+    comm = make_comm(A, ctx, dist, rank, world)
+    per_rank = max(len(MC.shard_cameras(n_cams_total, world, r)) for r in range(world))
+    kw = dict(trace_kw=dict(TRACE), **SIM)
+    glob = args.global_batching and dist is not None
+    if glob:
+        path = MC.GlobalCameraPath(ctx, n_cams_total, comm, W, H, n, SIM_PROFILE, **kw)
+    else:
+        path = MC.MultiCameraPath(ctx, cams, W, H, n, SIM_PROFILE, comm=comm,
+                                  cameras_per_rank=per_rank, **kw)
+    K = args.steps
+    path.run_pipelined(args.warmup)
+    ctx.stream_sync(path.stream)
+    mask_ev = [(ctx.event(), ctx.event()) if k % SAMPLE_EVERY == 0 else None for k in range(K)]
+    e0, e1 = ctx.event(), ctx.event()
+    clocks = Clocks(gpu_of(local))
+    barrier(dist)
+    ctx.synchronize()
+    clocks.start()
+    ctx.record(e0, path.stream)
+    n_canv = path.run_pipelined(K, mask_ev)
+    ctx.record(e1, path.stream)
+    ctx.stream_sync(path.stream)
+    clk = clocks.stop()
+    ms = reduce_max(dist, ctx.elapsed_ms(e0, e1), local)
+    ms_step = ms / K
+    k1_ms = statistics.mean(ctx.elapsed_ms(a, b) for a, b in filter(None, mask_ev))
+    value = n_cams_total * n * K / (ms / 1e3)
+
+    # bytes of this rank's pass
+    F_local = len(cams) * n
+    k1_bytes = len(cams) * (n + 1) * FRAME_BYTES  # every frame once + one background per camera
+    pats = path._last["patches"]
+    patch_bytes = int((pats["w"].astype(np.int64) * pats["h"]).sum()) * C
+    canvas_bytes = n_canv * CANVAS_BYTES
+    unique = k1_bytes + patch_bytes + canvas_bytes
+    b_run = 2 * F_local * FRAME_BYTES + patch_bytes + canvas_bytes
+    traffic = ncu_traffic("r02_k1_cfg4_traffic.json", F_local)
+    cfg_idx = 2 if args.config == "cfg3" else 3
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": "frames/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (generate_trace rects, frozen pixel spec, device-resident frames)",
+        "config": {"workload": f"BASELINE configs[{cfg_idx}]: {n_cams_total} synthetic 3840x2160 "
+                               f"cameras x {n} frames, SLO batcher across each shard's cameras "
+                               "(" + ("one global batcher, events split over the ranks, peer "
+                                      "frames over CUDA IPC" if glob else "shard-local canvases")
+                               + "), 4x4 zones, 1024x1024 canvases",
+                   "cameras": n_cams_total, "cameras_per_gpu": len(cams), "frames_per_camera": n,
+                   "sharding": "camera c on rank floor(c*N/cameras)",
+                   "parallelism": f"cameras sharded over {world} GPU(s)" +
+                                  (", NCCL all-gather of device descriptor blocks per step"
+                                   if world > 1 else ", no collective at N=1"),
+                   "batcher": {"profile_mu_sigma_ms": SIM_PROFILE,
+                               "max_canvases_per_batch": path.max_canvases, **SIM},
+                   "l2": f"inputs larger than L2 ({len(cams) * (n + 1) * FRAME_BYTES / 1e9:.1f} GB "
+                         "per GPU), no flush",
+                   "pipelining": "host batcher of pass i overlaps device K1-K4 of pass i+1; K5 on "
+                                 "its own stream; timed region = K whole passes"},
+        "roofline": roofline("mask_fg_kernel (K1, K1b fused), one launch per step", k1_bytes,
+                             k1_ms, traffic,
+                             "frame bytes only: each camera's 30 frames + its background read "
+                             "once (masks, cell grids, the raw-bitmap round trip not credited)"),
+        "path": path_record(unique, ms_step, b_run, {"k1_mask_fused": round(k1_ms, 4)},
+                            {"events": path._nev, "canvases": n_canv,
+                             "patches_admitted": int(len(pats)),
+                             "canvas_efficiency_mean": round(patch_bytes / max(1, canvas_bytes), 4),
+                             "rank": rank}),
+        "clocks": clk,
+        "gpu_launches": 3 * K,  # K1 (+K1b), planner (+descriptors), K5 per step
+        "mask_path": path.pipe.stats(),
+    }
+    if not args.no_e2e:
+        out["e2e"] = e2e_multicam(ctx, path, args, dist, local, n_cams_total)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline_multicam(path, n)
+    path.close()
+    if comm is not None:
+        comm.close()
+    if not args.no_secondary and args.config == "cfg4":
+        sec = measure_cfg2(args, rank, world, local, dist, ctx, secondary=True)
+        out["secondary"] = {"cfg2": sec}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e_multicam(ctx, path, args, dist, local, n_cams_total):
+    """The same metric through the public API with host frames: every step
+    copies every camera ring of the shard (background + frames) from pinned
+    host memory, then runs one pass (planes, descriptor all-gather and read-
+    back, batcher, K5)."""
+    rings = path.rings
+    host = [ctx.malloc_host(r.frame_bytes * (r.n + 1)) for r in rings]
+    for h, r in zip(host, rings):
+        ctx.memcpy(h, r.base, r.frame_bytes * (r.n + 1), 1, path.stream)
+    ctx.stream_sync(path.stream)
+    h2d = sum(r.frame_bytes * (r.n + 1) for r in rings)
+    d2h = path._hslot
+
+    def one():
+        for h, r in zip(host, rings):
+            ctx.memcpy(r.base, h, r.frame_bytes * (r.n + 1), 0, path.stream)
+        path.run_pipelined(1)
+
+    one()
+    ctx.stream_sync(path.stream)
+    e0, e1 = ctx.event(), ctx.event()
+    steps = max(1, args.e2e_steps)
+    barrier(dist)
+    ctx.record(e0, path.stream)
+    for _ in range(steps):
+        one()
+    ctx.record(e1, path.stream)
+    ctx.stream_sync(path.stream)
+    ms = reduce_max(dist, ctx.elapsed_ms(e0, e1), local)
+    for h in host:
+        ctx.free_host(h)
+    return {"value": round(n_cams_total * path.n * steps / (ms / 1e3), 1), "unit": "frames/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+            "h2d_GBps_per_gpu": round(h2d * steps / (ms / 1e3) / 1e9, 1),
+            "note": "pinned host frames of every camera -> device rings, then one pass through "
+                    "the public API (MultiCameraPath: planes, descriptor block read-back, "
+                    "batcher, K5); PCIe-bound"}
+
+
+def cpu_baseline_multicam(path, n):
+    """The CPU path of the same workload on a bounded sample: the first 8
+    cameras (one N=8 shard, their frames downloaded from the device rings):
+    restated pixel stages with every host thread, the reference tangram::run
+    (oracle/_ref) over the extracted RoIs, every invoke event's canvas pixels."""
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    k = min(8, len(path.rings))
+    frames = [[r.download_frame(s) for s in range(n + 1)] for r in path.rings[:k]]
+    t_us = [path.t_us[i] for i in range(k)]
+    canv = np.zeros((k * n * 16, 1024, 3072), np.uint8)
+    kind = "reference" if O.have_ref() else "port"
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < 3 or (time.perf_counter() - t_start < 10.0 and len(times) < 10):
+        t0 = time.perf_counter()
+        O.multicam_cpu(frames, t_us, W, H, SIM_PROFILE, threads, canvases=canv, **SIM)
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    return {"value": round(k * n / med, 2), "unit": "frames/s", "cores": threads, "kind": kind,
+            **host_cpu(),
+            "sample": f"cameras 0-{k - 1} (one N=8 shard) x {n} 4K frames, full path per pass: "
+                      "restated pixel stages (absent from the reference), the reference "
+                      "tangram::run compiled as-is (oracle/_ref) on the extracted RoIs, every "
+                      f"event canvas materialized; median of {len(times)} passes"}
+
+
+# ================================================================ config 2
+def measure_cfg2(args, rank, world, local, dist, ctx, secondary=False):
+    """Config 2: one camera x 300 frames per GPU, per-frame stitching (no
+    cross-camera step, so no collective).  Returns the line (or, as the
+    default run's secondary record, its device figures)."""
+    from paper_2404_09267_b200 import _native as N
+    from paper_2404_09267_b200 import api as A
+    n = 300 if secondary else args.frames
+    seed = 1000 + rank
     t_us, rects = A.generate_trace(n_frames=n, fps=30.0, frame_width=W, frame_height=H,
-                                   roi_proportion_mean=0.10, roi_max_dim=480, seed=seed)
+                                   seed=seed, **TRACE)
     ring = A.FrameRing(ctx, W, H, n)
     ring.synthesize(A.derive_seed(seed, "pixels"), rects)
-    zones = 16
-    max_canv = n * zones
+    max_canv = n * 16
     pipe = A.Pipeline(ctx, W, H, max_frames=n, max_canvases=max_canv)
     d_cur, d_prev = ring.tables()
     d_ids, d_gen = ctx.malloc(8 * n), ctx.malloc(8 * n)
@@ -233,18 +470,11 @@ def run_ours(args):
         step()
     ctx.stream_sync(stream)
     res = pipe.results(n, stream)
-
     K = args.steps
-    # Stage events on every 4th step of the timed region (an event between
-    # two kernels costs the step a few us; sampling keeps the launch
-    # durations live without taxing every step).
-    SAMPLE = 4
-    evs = [[ctx.event() for _ in range(4)] if k % SAMPLE == 0 else None for k in range(K)]
+    evs = [[ctx.event() for _ in range(4)] if k % SAMPLE_EVERY == 0 else None for k in range(K)]
     e0, e1 = ctx.event(), ctx.event()
     clocks = Clocks(gpu_of(local))
-    if dist is not None:
-        torch.cuda.synchronize()
-        dist.barrier()
+    barrier(dist)
     ctx.synchronize()
     clocks.start()
     ctx.record(e0, stream)
@@ -252,99 +482,88 @@ def run_ours(args):
         step(evs[k])
     ctx.record(e1, stream)
     ctx.stream_sync(stream)
-    if dist is not None:
-        torch.cuda.synchronize()
     clk = clocks.stop()
-    total_ms = ctx.elapsed_ms(e0, e1)
+    total_ms = reduce_max(dist, ctx.elapsed_ms(e0, e1), local)
     sampled = [e for e in evs if e]
-    k1 = [ctx.elapsed_ms(e[0], e[1]) for e in sampled]
-    plan = [ctx.elapsed_ms(e[1], e[2]) for e in sampled]
-    gat = [ctx.elapsed_ms(e[2], e[3]) for e in sampled]
-    if dist is not None:
-        total_ms = reduce_max(dist, total_ms, local)
-        dist.barrier()
+    k1 = statistics.mean(ctx.elapsed_ms(e[0], e[1]) for e in sampled)
+    plan = statistics.mean(ctx.elapsed_ms(e[1], e[2]) for e in sampled)
+    gat = statistics.mean(ctx.elapsed_ms(e[2], e[3]) for e in sampled)
     ms_step = total_ms / K
-    frames_total = n * K * world
-    value = frames_total / (total_ms / 1e3)
+    value = n * K * world / (total_ms / 1e3)
 
-    # algorithmic bytes.  Path: B_run = 2*W*H*C per frame +
-    # admitted patch bytes + every canvas byte.  K1 (the dominant kernel,
-    # launched fused with K1b): the frames it must read -- the n frames plus
-    # the first frame's prev, each once -- the raw foreground bitmap's one
-    # HBM round trip (written by K1, read back by the K1b tasks) and the cell
-    # grids it writes.
     adm_bytes = 0
     for f in range(n):
         for j, p in enumerate(res["patch_list"][f]):
             if res["admitted"][f, j]:
                 adm_bytes += p.rect.w * p.rect.h * C
     ncanv = int(res["total_canvases"])
-    raw_bytes = n * H * ((W + 31) // 32) * 4
-    cx, cy = (W + 15) // 16, (H + 15) // 16
-    cell_bytes = n * cy * (cx + (cx + 31) // 32) * 4
-    k1_bytes = (n + 1) * FRAME_BYTES + 2 * raw_bytes + cell_bytes
-    b_run = n * 2 * FRAME_BYTES + adm_bytes + ncanv * pipe.canvas_bytes
-    b_unique = (n + 1) * FRAME_BYTES + 2 * raw_bytes + adm_bytes + ncanv * pipe.canvas_bytes
-    peak, peak_src = peaks()
-    k1_ms = statistics.mean(k1)
-    achieved = k1_bytes / (k1_ms / 1e3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "k1_traffic.json")
-    if os.path.exists(tp):
-        try:
-            tj = json.load(open(tp))
-            traffic = tj["dram_bytes_per_frame"] * n
-        except Exception:
-            traffic = None
+    k1_bytes = (n + 1) * FRAME_BYTES
+    unique = k1_bytes + adm_bytes + ncanv * CANVAS_BYTES
+    b_run = n * 2 * FRAME_BYTES + adm_bytes + ncanv * CANVAS_BYTES
+    rf = roofline("mask_fg_kernel (K1, K1b fused)", k1_bytes, k1, ncu_traffic("k1_traffic.json", n),
+                  "frame bytes only: the 300 frames + the first frame's predecessor, each read "
+                  "once (masks, cell grids, the raw-bitmap round trip not credited)")
+    pth = path_record(unique, ms_step, b_run,
+                      {"k1_mask_fused": round(k1, 4), "plan+prefix": round(plan, 4),
+                       "gather": round(gat, 4)},
+                      {"rois": int(res["n_rois"].sum()), "patches": int(res["n_patches"].sum()),
+                       "admitted": int(res["admitted"].sum()), "canvases": ncanv,
+                       "canvas_efficiency_mean": round(adm_bytes / max(1, ncanv * CANVAS_BYTES), 4)})
+    workload = ("BASELINE configs[1]: synthetic 3840x2160 RGB camera per GPU, 300 frames, moderate "
+                "RoI density (roi_proportion_mean=0.10, roi_max_dim=480), 4x4 zones, 1024x1024 "
+                "canvases")
+    if secondary:
+        out = {"workload": workload, "value": round(value, 1), "unit": "frames/s",
+               "ms_per_step": round(ms_step, 4), "steps": K, "roofline": rf, "path": pth,
+               "clocks": clk, "mask_path": pipe.stats()}
+    else:
+        out = {
+            "metric": METRIC, "value": round(value, 1), "unit": "frames/s", "n_gpus": world,
+            "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (generate_trace rects, frozen pixel spec, device-resident)",
+            "config": {"workload": workload, "frames_per_gpu": n, "width": W, "height": H,
+                       "zones": "4x4", "canvas": "1024x1024", "threshold": 25, "dilate_radius": 2,
+                       "l2": "inputs larger than L2 (7.5 GB/GPU), no flush",
+                       "parallelism": f"one camera per GPU, {world} GPU(s); per-frame stitching "
+                                      "has no cross-camera exchange, so no collective"},
+            "roofline": rf, "path": pth, "clocks": clk, "gpu_launches": 3 * K,
+            "mask_path": pipe.stats()}
+        if not args.no_e2e:
+            out["e2e"] = e2e_cfg2(ctx, pipe, ring, n, d_ids, d_gen, d_canv, stream, args, world,
+                                  dist, local)
+        if rank == 0 and world == 1 and not args.no_cpu:
+            out["cpu_baseline"] = cpu_baseline_cfg2(ring, t_us, n)
+    pipe.close()
+    ring.close()
+    for p in (d_ids, d_gen, d_canv):
+        ctx.free(p)
+    return out
 
-    out = {
-        "metric": METRIC, "value": round(value, 1), "unit": "frames/s", "n_gpus": world,
-        "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (generate_trace rects, frozen pixel spec, device-resident)",
-        "config": {"workload": WORKLOAD, "frames_per_gpu": n, "width": W, "height": H,
-                   "zones": "4x4", "canvas": "1024x1024", "threshold": 25, "dilate_radius": 2,
-                   "l2": "inputs larger than L2 (7.5 GB/GPU), no flush",
-                   "parallelism": f"one camera per GPU, {world} GPU(s); per-frame stitching "
-                                  "has no cross-camera exchange, so no collective in the step"},
-        "roofline": {"bound": "hbm", "kernel": "mask_fg_kernel (K1, K1b fused)",
-                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "algorithmic_bytes_per_launch": k1_bytes, "peak_source": peak_src,
-                     "launch_ms": round(k1_ms, 4)},
-        "path": {"B_run_bytes_per_step": b_run, "path_GBps": round(b_run / (ms_step / 1e3) / 1e9, 1),
-                 "path_frac": round(b_run / (ms_step / 1e3) / 1e9 / peak, 4),
-                 "B_unique_bytes_per_step": b_unique,
-                 "unique_GBps": round(b_unique / (ms_step / 1e3) / 1e9, 1),
-                 "unique_frac": round(b_unique / (ms_step / 1e3) / 1e9 / peak, 4),
-                 "stage_ms": {"k1_mask_fused": round(k1_ms, 4),
-                              "plan+scan": round(statistics.mean(plan), 4),
-                              "gather": round(statistics.mean(gat), 4)},
-                 "rois": int(res["n_rois"].sum()), "patches": int(res["n_patches"].sum()),
-                 "admitted": int(res["admitted"].sum()), "canvases": ncanv,
-                 "canvas_efficiency_mean": round(adm_bytes / max(1, ncanv * pipe.canvas_bytes), 4)},
-        "clocks": clk,
-        "gpu_launches": 3 * K,  # K1 (+K1b), plan (+scan), gather
-    }
 
-    if not args.no_e2e:
-        out["e2e"] = e2e(ctx, pipe, ring, n, d_ids, d_gen, d_canv, stream, args, world, dist)
-    if rank == 0 and world == 1 and not args.no_cpu:
-        out["cpu_baseline"] = cpu_baseline(ring, t_us, n)
+def run_cfg2(args):
+    rank, world, local = dist_env()
+    if world > 1:
+        bind_to_gpu_numa(gpu_of(local))
+    dist = init_dist(local) if world > 1 else None
+    from paper_2404_09267_b200 import api as A
+    ctx = A.Context(gpu_of(local))
+    out = measure_cfg2(args, rank, world, local, dist, ctx)
     if rank == 0:
         print(json.dumps(out), flush=True)
+    ctx.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def e2e(ctx, pipe, ring, n, d_ids, d_gen, d_canv, stream, args, world, dist):
+def e2e_cfg2(ctx, pipe, ring, n, d_ids, d_gen, d_canv, stream, args, world, dist, local):
     """Same metric through the public API with host buffers: every step
     copies the camera's frames from pinned host memory (chunked on a copy
     stream, overlapped with compute) and reads back the patch/placement
     descriptors the batcher consumes."""
-    from paper_2404_09267_b200 import api as A
     from paper_2404_09267_b200 import _native as N
+    from paper_2404_09267_b200 import api as A
     lib = N.lib()
     slots = n + 1
     host = ctx.malloc_host(FRAME_BYTES * slots)
@@ -397,215 +616,69 @@ def e2e(ctx, pipe, ring, n, d_ids, d_gen, d_canv, stream, args, world, dist):
     ctx.stream_sync(stream)
     e0, e1 = ctx.event(), ctx.event()
     ctx.synchronize()
+    barrier(dist)
     ctx.record(e0, cstream)
     for _ in range(args.steps):
         h2d, d2h = one()
     ctx.record(e1, stream)
     ctx.stream_sync(stream)
-    ms = ctx.elapsed_ms(e0, e1)
-    if dist is not None:
-        import torch
-        ms = reduce_max(dist, ms, ctx.device)
+    ms = reduce_max(dist, ctx.elapsed_ms(e0, e1), local)
     ctx.free_host(host)
     ctx.free_host(hdesc)
     return {"value": round(n * args.steps * world / (ms / 1e3), 1), "unit": "frames/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "h2d_GBps_per_gpu": round(h2d * args.steps / (ms / 1e3) / 1e9, 1),
             "note": "pinned host frames -> device in 30-frame chunks overlapped with compute; "
-                    "patch + placement descriptors read back; PCIe-bound (tools/pcie_probe.py: "
-                    "55.6 GB/s pinned H2D on the box)"}
+                    "patch + placement descriptors read back; PCIe-bound"}
 
 
-def cpu_baseline(ring, t_us, n, sample=None):
-    """The CPU path (reference partition/stitch_all from oracle/_ref when
-    built, else the oracle port) over a bounded sample of this workload."""
+def cfg2_params(threads):
+    return dict(width=W, height=H, pitch=W * C, threshold=25, radius=2, zones_x=4, zones_y=4,
+                canvas_w=1024, canvas_h=1024, bytes_per_pixel=1.5, slo_us=1_000_000, max_rois=1024,
+                threads=threads)
+
+
+def cpu_baseline_cfg2(ring, t_us, n):
+    """The CPU path on a bounded sample of the same frames: restated pixel
+    stages + the reference partition / stitch_all (oracle/_ref), canvases
+    materialized into a buffer allocated once, all host threads."""
     from oracle import oracle as O
     threads = os.cpu_count() or 1
-    sample = sample or min(n, max(8, min(48, 2 * threads)))
+    sample = min(n, 96)
     frames = [ring.download_frame(i) for i in range(sample + 1)]
-    out = cpu_measure(frames, t_us[:sample], threads)
-    # SURVEY §8(d): also one core (a few frames, a few passes)
-    one = cpu_measure(frames[:5], t_us[:4], 1, passes=3)
-    out["single_core_value"] = one["value"]
-    return out
-
-
-def cpu_measure(frames, t_us, threads, passes=None):
-    from oracle import oracle as O
     lib = "ref" if O.have_ref() else "port"
-    sample = len(frames) - 1
-    params = dict(width=W, height=H, pitch=W * C, threshold=25, radius=2, zones_x=4, zones_y=4,
-                  canvas_w=1024, canvas_h=1024, bytes_per_pixel=1.5, slo_us=1_000_000, max_rois=1024,
-                  threads=threads)
+    canv = np.zeros((sample * 16, 1024, 3072), np.uint8)
     times = []
     t_start = time.perf_counter()
-    while True:
+    while len(times) < 3 or (time.perf_counter() - t_start < 10.0 and len(times) < 20):
         t0 = time.perf_counter()
-        O.process_frames(params, frames[1:], frames[:-1], list(range(sample)), t_us, lib=lib,
-                         want_canvases=True, canvas_cap=sample * 16)
+        O.process_frames(cfg2_params(threads), frames[1:], frames[:-1], list(range(sample)),
+                         t_us[:sample], lib=lib, canvas_out=canv)
         times.append(time.perf_counter() - t0)
-        if (passes and len(times) >= passes) or (not passes and time.perf_counter() - t_start > 10.0) \
-                or len(times) >= 20:
-            break
-    best = statistics.median(times)
-    return {"value": round(sample / best, 2), "unit": "frames/s", "cores": threads,
-            "kind": "reference" if lib == "ref" else "port",
-            "sample": f"{sample} frames of the same 4K workload, {len(times)} passes, median; pixel "
-                      f"stages restated (absent from the reference), partition/stitch_all "
-                      f"{'= reference code (oracle/_ref)' if lib == 'ref' else '= oracle port'}; "
-                      "canvases materialized"}
-
-
-# ============================================================= reference
-def run_reference(args):
-    rank, world, _ = dist_env()
-    if rank != 0:
-        return
-    from concurrent.futures import ThreadPoolExecutor
-
-    from oracle import oracle as O
-    threads = os.cpu_count() or 1
-    sample = min(args.frames, max(8, min(32, threads)))
-    cfg = O.gen_cfg(seed=1000, n_frames=args.frames, fps=30.0, frame_width=W, frame_height=H,
-                    roi_proportion_mean=0.10, roi_max_dim=480)
-    t_us, rects = O.generate_trace(cfg)
-    ps = O.derive_seed(1000, "pixels")
-    with ThreadPoolExecutor(threads) as ex:
-        frames = list(ex.map(lambda i: O.synth_frame(W, H, ps, i, rects[i] if i >= 0 else []),
-                             range(-1, sample)))
-    lib = "ref" if O.have_ref() else "port"
-    params = dict(width=W, height=H, pitch=W * C, threshold=25, radius=2, zones_x=4, zones_y=4,
-                  canvas_w=1024, canvas_h=1024, bytes_per_pixel=1.5, slo_us=1_000_000, max_rois=1024,
-                  threads=threads)
-
-    def step():
-        O.process_frames(params, frames[1:], frames[:-1], list(range(sample)), t_us[:sample],
-                         lib=lib, want_canvases=True, canvas_cap=sample * 16)
-
-    for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    dt = time.perf_counter() - t0
-    value = sample * args.steps / dt
-    out = {
-        "metric": METRIC, "value": round(value, 2), "unit": "frames/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (generate_trace rects, frozen pixel spec, host memory)",
-        "config": {"workload": WORKLOAD, "frames_per_step": sample, "width": W, "height": H},
-        "impl": "reference",
-        "cpu_baseline": {"value": round(value, 2), "unit": "frames/s", "cores": threads,
-                         "kind": "reference" if lib == "ref" else "port",
-                         "sample": f"{sample} frames of the workload per step; reference "
-                                   "partition()/stitch_all() compiled as-is (oracle/_ref), pixel "
-                                   "stages restated (absent from the reference)"},
-        "e2e": {"value": round(value, 2), "unit": "frames/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(out), flush=True)
-
-
-# ============================================== configs 3/4: batched cameras
-# SURVEY Appendix P3 setting: mu = 60 + 25 k ms, sigma = 0.05 mu, 1e6 Mbps
-# links, 80 GB GPU (a 4 GB model leaves room for 76 canvases per batch).
-SIM_PROFILE = [(k, 60.0 + 25.0 * k, 0.05 * (60.0 + 25.0 * k)) for k in (1, 2, 4, 8, 16, 32, 64)]
-SIM_BANDWIDTH_MBPS = 1e6
-SIM_GPU_MEMORY_GB = 80.0
-
-
-def run_multicam(args):
-    """Config 3 (5 cameras, cross-camera batching on 1 GPU) / config 4 (64
-    cameras sharded over the ranks, descriptors all-gathered).  A step:
-    K1-K4 for every camera, descriptors to the host, SLO batcher replay,
-    one K5 launch for every invoke event's canvases."""
-    rank, world, local = dist_env()
-    dist = None
-    if world > 1:
-        import torch
-        dist = init_dist(local)
-    from paper_2404_09267_b200 import api as A
-    from paper_2404_09267_b200 import multicam as MC
-    n_cams_total = 5 if args.config == "cfg3" else 64
-    frames = min(args.frames, 300 if args.config == "cfg3" else 30)
-    cams = MC.shard_cameras(n_cams_total, world, rank)
-    ctx = A.Context(gpu_of(local))
-    kw = dict(bandwidth_mbps=SIM_BANDWIDTH_MBPS, gpu_memory_gb=SIM_GPU_MEMORY_GB, model_size_gb=4.0,
-              trace_kw=dict(roi_proportion_mean=0.10, roi_max_dim=480))
-    glob = args.global_batching and dist is not None
-    comm = make_comm(A, ctx, dist, rank, world)
-    per_rank = max(len(MC.shard_cameras(n_cams_total, world, r)) for r in range(world))
-    if glob:
-        path = MC.GlobalCameraPath(ctx, n_cams_total, comm, W, H, frames, SIM_PROFILE, **kw)
-    else:
-        path = MC.MultiCameraPath(ctx, cams, W, H, frames, SIM_PROFILE, comm=comm,
-                                  cameras_per_rank=per_rank, **kw)
-    e0, e1 = ctx.event(), ctx.event()
-    # K steps = K passes over the shard's frames; the host batcher of pass i
-    # overlaps the device planes of pass i+1 (MultiCameraPath.run_pipelined)
-    n_canv = path.run_pipelined(args.warmup)
-    ctx.stream_sync(path.stream)
-    clocks = Clocks(gpu_of(local))
-    if dist is not None:
-        dist.barrier()
-    ctx.synchronize()
-    clocks.start()
-    ctx.record(e0, path.stream)
-    n_canv = path.run_pipelined(args.steps)
-    ctx.record(e1, path.stream)
-    ctx.stream_sync(path.stream)
-    clk = clocks.stop()
-    ms = ctx.elapsed_ms(e0, e1)
-    if dist is not None:
-        import torch
-        ms = reduce_max(dist, ms, local)
-    n_events = path._nev
-    out = {
-        "metric": METRIC, "value": round(len(cams) * frames * args.steps * world / (ms / 1e3), 1),
-        "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (generate_trace rects, frozen pixel spec, device-resident)",
-        "config": {"workload": f"BASELINE configs[{2 if args.config == 'cfg3' else 3}]: "
-                               f"{n_cams_total} synthetic 4K cameras, {frames} frames each, "
-                               "SLO batcher across cameras, " +
-                               ("one global batcher, events split over the ranks, peer frames "
-                                "over CUDA IPC" if glob else "shard-local canvases"),
-                   "cameras_per_gpu": len(cams), "frames_per_camera": frames,
-                   "bandwidth_mbps": SIM_BANDWIDTH_MBPS, "profile": SIM_PROFILE,
-                   "max_canvases_per_batch": path.max_canvases,
-                   "parallelism": f"cameras sharded over {world} GPU(s)" +
-                                  (", NCCL all-gather of patch descriptors" if world > 1 else ""),
-                   "pipelining": "host batcher of pass i overlaps device K1-K4 of pass i+1; "
-                                 "K5 on its own stream; timed region = K whole passes"},
-        "batching": {"events": n_events, ("canvases_rank0" if glob else "canvases"): n_canv,
-                     "patches_admitted": int(len(path._last["patches"]))},
-        "clocks": clk, "gpu_launches": 3 * args.steps,  # K1 (+K1b), plan (+scan), gather
-    }
-    if rank == 0:
-        print(json.dumps(out), flush=True)
-    path.close()
-    if dist is not None:
-        dist.barrier()
-        dist.destroy_process_group()
+    med = statistics.median(times)
+    return {"value": round(sample / med, 2), "unit": "frames/s", "cores": threads,
+            "kind": "reference" if lib == "ref" else "port", **host_cpu(),
+            "sample": f"frames 0-{sample - 1} of the same camera, median of {len(times)} passes; "
+                      "pixel stages restated (absent from the reference), partition/stitch_all "
+                      "= reference code (oracle/_ref); canvases materialized"}
 
 
 # =================================================== config 5: density sweep
 def run_density(args):
-    """Config 5: 8 cameras (one pipeline run over all their frames), per-frame path,
-    roi_proportion_mean in {0.01 .. 0.59}, roi_max_dim 1024; reports frames/s,
-    measured active-cell fraction, stitch efficiency and path GB/s."""
-    from paper_2404_09267_b200 import api as A
+    """Config 5: 8 cameras x 60 frames as one per-frame pipeline run,
+    roi_proportion_mean in {0.01 .. 0.59}, roi_max_dim 1024, roi_count_max
+    24; per density: frames/s, the measured active-cell fraction, stitch
+    efficiency, K1 roofline and path bytes; clocks over the whole sweep."""
     from paper_2404_09267_b200 import _native as N
+    from paper_2404_09267_b200 import api as A
     ctx = A.Context(0)
-    n = min(args.frames, 60)
-    lines = []
+    lib = N.lib()
+    n, cams = args.frames, args.cams
+    lines, clk_all = [], []
+    keep = None
     for rho in (0.01, 0.05, 0.10, 0.20, 0.40, 0.59):
-        # the 8 cameras' frames run as ONE per-frame pipeline launch sequence,
-        # camera-major (each camera's first frame restarts the K1 frame chain)
-        rings, cur, prev, ids, gen = [], [], [], [], []
-        for cam in range(8):
+        rings, cur, prev, ids, gen, ts = [], [], [], [], [], []
+        for cam in range(cams):
             t_us, rects = A.generate_trace(n_frames=n, fps=30.0, frame_width=W, frame_height=H,
                                            roi_proportion_mean=rho, roi_max_dim=1024,
                                            roi_count_max=24, seed=1000 + cam)
@@ -616,6 +689,7 @@ def run_density(args):
             prev += ring.slots[0:n]
             ids += list(range(n))
             gen += list(t_us)
+            ts.append(t_us)
         F = len(cur)
         pipe = A.Pipeline(ctx, W, H, max_frames=F, max_canvases=F * 16)
         tabs = [ctx.malloc(8 * F) for _ in range(4)]
@@ -624,44 +698,155 @@ def run_density(args):
             ctx.upload(d, arr)
         d_cur, d_prev, d_ids, d_gen = tabs
         d_canv = ctx.malloc(pipe.canvas_bytes * F * 16)
-        for _ in range(3):
+        for _ in range(args.warmup):
             pipe.run(F, d_cur, d_prev, d_ids, d_gen, 0, d_canv)
+        K = args.steps
+        evs = [(ctx.event(), ctx.event()) if k % SAMPLE_EVERY == 0 else None for k in range(K)]
         e0, e1 = ctx.event(), ctx.event()
         ctx.synchronize()
+        clocks = Clocks(0)
+        clocks.start()
         ctx.record(e0)
-        for _ in range(args.steps):
-            pipe.run(F, d_cur, d_prev, d_ids, d_gen, 0, d_canv)
+        for k in range(K):
+            if evs[k]:
+                ctx.record(evs[k][0])
+            A.check(lib.tg_pipeline_stage_mask(pipe.handle, F, d_cur, d_prev, None))
+            if evs[k]:
+                ctx.record(evs[k][1])
+            A.check(lib.tg_pipeline_stage_plan(pipe.handle, F, d_ids, d_gen, 0, None))
+            A.check(lib.tg_pipeline_stage_gather(pipe.handle, F, d_cur, d_canv, None))
         ctx.record(e1)
         ctx.stream_sync()
-        tot_ms = ctx.elapsed_ms(e0, e1) / args.steps
+        clk_all.append(clocks.stop())
+        ms_step = ctx.elapsed_ms(e0, e1) / K
+        k1_ms = statistics.mean(ctx.elapsed_ms(a, b) for a, b in filter(None, evs))
         res = pipe.results(F)
         c = pipe.cells(F)
-        act, cells = int((c != 0).sum()), c.size
         adm_bytes = 0
         for f in range(F):
             for j, p in enumerate(res["patch_list"][f]):
                 if res["admitted"][f, j]:
-                    adm_bytes += p.rect.w * p.rect.h * 3
-        canv_bytes = res["total_canvases"] * pipe.canvas_bytes
-        frames = F
+                    adm_bytes += p.rect.w * p.rect.h * C
+        canv_bytes = res["total_canvases"] * CANVAS_BYTES
+        k1_bytes = cams * (n + 1) * FRAME_BYTES
+        unique = k1_bytes + adm_bytes + canv_bytes
+        peak, _ = peaks()
+        lines.append({"roi_proportion_mean": rho, "frames_per_s": round(F / (ms_step / 1e3), 1),
+                      "ms_per_step": round(ms_step, 4),
+                      "active_cell_fraction": round(float((c != 0).mean()), 4),
+                      "stitch_efficiency": round(adm_bytes / max(1, canv_bytes), 4),
+                      "canvases_per_frame": round(res["total_canvases"] / F, 3),
+                      "k1_frac": round(k1_bytes / (k1_ms / 1e3) / 1e9 / peak, 4),
+                      "k1_ms": round(k1_ms, 4),
+                      "unique_GBps": round(unique / (ms_step / 1e3) / 1e9, 1),
+                      "unique_frac": round(unique / (ms_step / 1e3) / 1e9 / peak, 4),
+                      "B_run_model_GBps": round((2 * F * FRAME_BYTES + adm_bytes + canv_bytes)
+                                                / (ms_step / 1e3) / 1e9, 1)})
+        if rho == 0.10:
+            keep = (k1_bytes, k1_ms, unique, ms_step, F)
+            if not args.no_cpu:
+                cpu = cpu_baseline_cfg2(rings[0], ts[0], n)
         pipe.close()
         for r in rings:
             r.close()
         for p in tabs + [d_canv]:
             ctx.free(p)
-        b_run = frames * 2 * FRAME_BYTES + adm_bytes + canv_bytes
-        lines.append({"roi_proportion_mean": rho, "frames_per_s": round(frames / (tot_ms / 1e3), 1),
-                      "active_cell_fraction": round(act / cells, 4),
-                      "stitch_efficiency": round(adm_bytes / max(1, canv_bytes), 4),
-                      "canvases_per_frame": round(canv_bytes / pipe.canvas_bytes / frames, 3),
-                      "path_GBps": round(b_run / (tot_ms / 1e3) / 1e9, 1)})
-    peak, _ = peaks()
+    k1_bytes, k1_ms, unique, ms_step, F = keep
+    reasons = sorted({r for c_ in clk_all for r in c_.get("reasons", [])})
+    sm = [c_["sm_mhz"] for c_ in clk_all if c_.get("sm_mhz")]
     out = {"metric": METRIC, "value": lines[2]["frames_per_s"], "unit": "frames/s", "n_gpus": 1,
-           "steps": args.steps, "warmup": 3, "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "u8", "data": "synthetic", "gpu_launches_per_step": 3,
-           "config": {"workload": "BASELINE configs[4]: RoI-density sweep, 8 synthetic 4K cameras, "
-                                  f"{n} frames each, roi_max_dim 1024", "peak_GBps": peak},
-           "sweep": lines}
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": lines[2]["ms_per_step"],
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+           "data": "synthetic (generate_trace rects, frozen pixel spec, device-resident)",
+           "config": {"workload": f"BASELINE configs[4]: RoI-density sweep, {cams} synthetic 4K "
+                                  f"cameras x {n} frames as one per-frame pipeline run, "
+                                  "roi_max_dim 1024, roi_count_max 24; value = the 0.10 point",
+                      "l2": "inputs larger than L2, no flush"},
+           "roofline": roofline("mask_fg_kernel (K1, K1b fused) at rho=0.10", k1_bytes, k1_ms, None,
+                                "frame bytes only, each read once"),
+           "path": {"unique_GBps": lines[2]["unique_GBps"], "unique_frac": lines[2]["unique_frac"]},
+           "clocks": {"sm_mhz": statistics.median(sm) if sm else None,
+                      "sm_max_mhz": max((c_["sm_max_mhz"] or 0) for c_ in clk_all) or None,
+                      "reasons": reasons, "per_density": clk_all},
+           "gpu_launches": 3 * args.steps, "sweep": lines}
+    if not args.no_cpu and keep:
+        out["cpu_baseline"] = cpu
+    print(json.dumps(out), flush=True)
+    ctx.close()
+
+
+# ============================================================= reference
+def run_reference(args):
+    """The reference's CPU implementation of the path on the box's host
+    cores, on this arm's config: the restated pixel stages (the reference
+    has none) with the reference's own partition / stitch_all / tangram::run
+    compiled as-is (oracle/_ref).  Under torchrun only rank 0 runs."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    kind = "reference" if O.have_ref() else "port"
+    cams = args.cams if args.config in ("cfg3", "cfg4") else (8 if args.config == "cfg5" else 1)
+    n = args.frames
+    trace = dict(TRACE) if args.config != "cfg5" else dict(roi_proportion_mean=0.10,
+                                                           roi_max_dim=1024, roi_count_max=24)
+    scenes = []
+    for c in range(cams):
+        cfg = O.gen_cfg(seed=1000 + c, n_frames=n, fps=30.0, frame_width=W, frame_height=H,
+                        **trace)
+        t_us, rects = O.generate_trace(cfg)
+        scenes.append((t_us, O.synth_frames(W, H, O.derive_seed(1000 + c, "pixels"), rects,
+                                            threads)))
+    if args.config in ("cfg3", "cfg4"):
+        frames = [fr for _, fr in scenes]
+        t_all = [t for t, _ in scenes]
+        first = O.multicam_cpu(frames, t_all, W, H, SIM_PROFILE, threads, canvases=None, **SIM)
+        canv = np.zeros((first["n_canvases"], 1024, 3072), np.uint8)  # allocated once
+
+        def step():
+            O.multicam_cpu(frames, t_all, W, H, SIM_PROFILE, threads, canvases=canv, **SIM)
+        what = (f"all {cams} cameras x {n} frames per step: restated pixel stages, the reference "
+                "tangram::run (sim.hpp:206-552) on the extracted RoIs, every invoke event's "
+                "canvas pixels")
+    else:
+        cur = [fr[i + 1] for _, fr in scenes for i in range(n)]
+        prev = [fr[i] for _, fr in scenes for i in range(n)]
+        ids = [i for _ in scenes for i in range(n)]
+        gen = [t for ts, _ in scenes for t in ts]
+        canv = np.zeros((len(cur) * 16, 1024, 3072), np.uint8)  # allocated once
+
+        def step():
+            O.process_frames(cfg2_params(threads), cur, prev, ids, gen,
+                             lib="ref" if kind == "reference" else "port", canvas_out=canv)
+        what = (f"all {cams * n} frames per step: restated pixel stages + the reference "
+                "partition / stitch_all per frame, every canvas materialized")
+    warm = min(args.warmup, 1)  # CPU code has nothing to warm beyond the first pass
+    for _ in range(warm):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    dt = sum(times)
+    frames_step = cams * n
+    value = frames_step * args.steps / dt
+    cfg_idx = {"cfg2": 1, "cfg3": 2, "cfg4": 3, "cfg5": 4}[args.config]
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (generate_trace rects, frozen pixel spec, host memory)",
+        "config": {"workload": f"BASELINE configs[{cfg_idx}] on the host CPU: {cams} camera(s) x "
+                               f"{n} 3840x2160 frames", "cameras": cams, "frames_per_camera": n,
+                   "frames_per_step": frames_step, "warmup_steps_run": warm},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 2), "unit": "frames/s", "cores": threads,
+                         "kind": kind, **host_cpu(), "sample": what},
+        "e2e": {"value": round(value, 2), "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
     print(json.dumps(out), flush=True)
 
 
@@ -674,7 +859,7 @@ def main():
     elif args.config == "cfg5":
         run_density(args)
     else:
-        run_ours(args)
+        run_cfg2(args)
 
 
 if __name__ == "__main__":

@@ -43,6 +43,11 @@ class FreeRect(C.Structure):
     _fields_ = [("r", Rect), ("canvas", C.c_int32)]
 
 
+class FillJob(C.Structure):
+    _fields_ = [("frame", C.c_int32), ("sx", C.c_int32), ("sy", C.c_int32), ("dx", C.c_int32),
+                ("dy", C.c_int32), ("w", C.c_int32), ("h", C.c_int32)]
+
+
 class GenCfg(C.Structure):
     _fields_ = [("n_frames", C.c_int32), ("fps", C.c_double), ("frame_width", C.c_int32),
                 ("frame_height", C.c_int32), ("roi_proportion_mean", C.c_double),
@@ -126,6 +131,9 @@ def load(lib: str = "port") -> C.CDLL:
         dll.orc_extract_rois.argtypes = [C.c_void_p, C.c_int, C.c_int, P(Rect), C.c_int]
         dll.orc_hash32.restype = C.c_uint32
         dll.orc_hash32.argtypes = [C.c_uint32]
+        dll.orc_fill_jobs.restype = None
+        dll.orc_fill_jobs.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                      C.c_int, C.c_void_p, C.c_int]
         dll.orc_rng_seed.restype = None
         dll.orc_rng_seed.argtypes = [C.c_void_p, C.c_uint64]
         for n, r in (("orc_rng_next", C.c_uint64), ("orc_rng_uniform01", C.c_double)):
@@ -325,9 +333,11 @@ def extract_rois(cell_grid, cap=4096):
 
 
 def process_frames(params: dict, cur_frames, prev_frames, frame_ids, gen_us, first_patch_id=0,
-                   want_canvases=True, want_cells=False, canvas_cap=None, lib="port"):
+                   want_canvases=True, want_cells=False, canvas_cap=None, lib="port",
+                   canvas_out=None):
     """Runs the whole per-frame CPU path.  cur_frames/prev_frames are lists
-    of (H, pitch) uint8 arrays.  Returns a dict of per-frame results."""
+    of (H, pitch) uint8 arrays.  Returns a dict of per-frame results.
+    canvas_out: a preallocated (cap, N, 3M) uint8 buffer for the canvases."""
     dll = load(lib)
     p = PathParams(**params)
     n = len(cur_frames)
@@ -340,7 +350,10 @@ def process_frames(params: dict, cur_frames, prev_frames, frame_ids, gen_us, fir
         placements=(Placement * max(1, n * nz))(), n_placements=np.zeros(n, np.int32))
     if canvas_cap is None:
         canvas_cap = n * nz if want_canvases else 0
-    canv = np.zeros((canvas_cap, p.canvas_h, p.canvas_w * 3), np.uint8) if want_canvases else None
+    if want_canvases and canvas_out is not None:
+        canv, canvas_cap = canvas_out, len(canvas_out)
+    else:
+        canv = np.zeros((canvas_cap, p.canvas_h, p.canvas_w * 3), np.uint8) if want_canvases else None
     cells_arr = np.zeros((n, cy, cx), np.uint32) if want_cells else None
     out = PathOut(res["n_rois"].ctypes.data, res["rois"].ctypes.data, res["n_patches"].ctypes.data,
                   C.cast(res["patches"], C.c_void_p), res["admitted"].ctypes.data,
@@ -519,3 +532,57 @@ class RefScheduler:
         if self.dll.ref_sched_pending(C.c_void_p(self.h), C.byref(at), C.byref(ep)):
             return at.value, ep.value
         return None
+
+
+# ------------------------------------------------- configs 3/4 on the CPU
+def multicam_cpu(cam_frames, cam_t_us, width, height, profile, threads, canvases=None,
+                 zones=(4, 4), canvas=(1024, 1024), **sim):
+    """The CPU path of configs 3/4 (bench cpu legs): the restated pixel
+    stages on every frame of every camera (`threads` workers; the reference's
+    own partition / stitch_all inside), the reference simulator tangram::run
+    (sim.hpp:206-552, tangram policy) over the extracted RoIs, and every
+    invoke event's canvas pixels -- the reference stitch_all of the event's
+    patches (= the scheduler's repack, scheduler.hpp:146-160), copied from
+    the frames into `canvases` ((K, N, 3M) uint8, preallocated by the caller;
+    None skips the pixels).  cam_frames[c] = [background, frame 0, ...].
+    Returns dict(events, n_canvases, rois)."""
+    lib = "ref"
+    n_cams, n = len(cam_frames), len(cam_t_us[0])
+    cur = [fr[i + 1] for fr in cam_frames for i in range(n)]
+    prev = [fr[i] for fr in cam_frames for i in range(n)]
+    params = dict(width=width, height=height, pitch=cam_frames[0][0].shape[1], threshold=25,
+                  radius=2, zones_x=zones[0], zones_y=zones[1], canvas_w=canvas[0],
+                  canvas_h=canvas[1], bytes_per_pixel=1.5, slo_us=1_000_000, max_rois=1024,
+                  threads=threads)
+    res = process_frames(params, cur, prev, [i for _ in range(n_cams) for i in range(n)],
+                         [t for ts in cam_t_us for t in ts], 0, want_canvases=False, lib=lib)
+    rois = [[[tuple(r) for r in res["rois"][c * n + f, :res["n_rois"][c * n + f]].tolist()]
+             for f in range(n)] for c in range(n_cams)]
+    ref = run_tangram([(cam_t_us[c], rois[c]) for c in range(n_cams)], width, height, profile,
+                      zones=zones, canvas=canvas, **sim)
+    # the path's patches carry run()'s ids: scene-major, frame order (sim.hpp:249-251)
+    where = {}
+    for f, plist in enumerate(res["patch_list"]):
+        for p in plist:
+            where[p["patch_id"]] = (f, p["rect"])
+    jobs, offsets = [], [0]
+    for e in ref["events"]:
+        q = [(i, where[i][1][2], where[i][1][3]) for i in e["patch_ids"]]
+        pl, nc, _ = stitch_all(q, canvas[0], canvas[1], lib=lib)
+        per = [[] for _ in range(nc)]
+        for (i, ci, x, y, w, h) in pl:
+            f, r = where[i]
+            per[ci].append((f, r[0], r[1], x, y, w, h))
+        for lst in per:
+            jobs += lst
+            offsets.append(len(jobs))
+    k = len(offsets) - 1
+    if canvases is not None:
+        if len(canvases) < k:
+            raise OracleError(f"canvas buffer holds {len(canvases)} < {k} canvases")
+        jarr = (FillJob * max(1, len(jobs)))(*[FillJob(*j) for j in jobs])
+        oarr = (C.c_int64 * len(offsets))(*offsets)
+        fptr = (C.c_void_p * max(1, len(cur)))(*[f.ctypes.data for f in cur])
+        load("port").orc_fill_jobs(fptr, params["pitch"], jarr, oarr, k, canvas[0], canvas[1],
+                                   canvases.ctypes.data, threads)
+    return dict(events=ref["events"], n_canvases=k, rois=rois)

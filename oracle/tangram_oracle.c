@@ -593,6 +593,52 @@ void orc_fill_canvas(const uint8_t* frame, int pitch, const orc_patch* patches,
   }
 }
 
+/* Canvases of batched invoke events (configs 3/4): canvas k is zero-filled
+ * and gets jobs[offsets[k] .. offsets[k+1]) copied in, each job a patch
+ * rect of frames[job.frame] placed at (dx, dy).  Canvases are split over
+ * `threads` workers. */
+typedef struct {
+  const uint8_t* const* frames;
+  int pitch, M, N, n_canvases, stride, start;
+  const orc_fill_job* jobs;
+  const int64_t* offsets;
+  uint8_t* out;
+} fill_jobs_arg;
+
+static void* fill_jobs_worker(void* v) {
+  const fill_jobs_arg* a = (const fill_jobs_arg*)v;
+  const size_t cb = (size_t)a->M * (size_t)a->N * 3;
+  for (int k = a->start; k < a->n_canvases; k += a->stride) {
+    uint8_t* canvas = a->out + (size_t)k * cb;
+    memset(canvas, 0, cb);
+    for (int64_t j = a->offsets[k]; j < a->offsets[k + 1]; ++j) {
+      const orc_fill_job J = a->jobs[j];
+      const uint8_t* src = a->frames[J.frame];
+      for (int v = 0; v < J.h; ++v)
+        memcpy(canvas + ((size_t)(J.dy + v) * a->M + J.dx) * 3,
+               src + (size_t)(J.sy + v) * a->pitch + (size_t)J.sx * 3, (size_t)J.w * 3);
+    }
+  }
+  return NULL;
+}
+
+void orc_fill_jobs(const uint8_t* const* frames, int pitch, const orc_fill_job* jobs,
+                   const int64_t* offsets, int n_canvases, int M, int N, uint8_t* out,
+                   int threads) {
+  const int nt = threads > 0 ? threads : 1;
+  fill_jobs_arg* args = (fill_jobs_arg*)calloc((size_t)nt, sizeof(fill_jobs_arg));
+  pthread_t* th = (pthread_t*)calloc((size_t)nt, sizeof(pthread_t));
+  for (int k = 0; k < nt; ++k) {
+    args[k] = (fill_jobs_arg){frames, pitch, M, N, n_canvases, nt, k, jobs, offsets, out};
+    if (nt == 1) fill_jobs_worker(&args[k]);
+    else pthread_create(&th[k], NULL, fill_jobs_worker, &args[k]);
+  }
+  if (nt > 1)
+    for (int k = 0; k < nt; ++k) pthread_join(th[k], NULL);
+  free(th);
+  free(args);
+}
+
 /* ======================================================================== */
 /* Per-frame path: sim.hpp:241-272 (partition + admission :262) and          */
 /* sim.hpp:302-332 (one stitch_all per frame, canvases in frame order).      */

@@ -124,6 +124,17 @@ void orc_fill_canvas(const uint8_t* frame, int pitch, const orc_patch* patches,
                      const orc_placement* placements, int n, int canvas_index, int canvas_w,
                      int canvas_h, uint8_t* canvas);
 
+/* Batched event canvases: canvas k = zeros + jobs[offsets[k]..offsets[k+1]). */
+typedef struct {
+  int32_t frame;      /* index into frames[] */
+  int32_t sx, sy;     /* source rect origin in that frame */
+  int32_t dx, dy;     /* destination in the canvas */
+  int32_t w, h;
+} orc_fill_job;
+void orc_fill_jobs(const uint8_t* const* frames, int pitch, const orc_fill_job* jobs,
+                   const int64_t* offsets, int n_canvases, int canvas_w, int canvas_h, uint8_t* out,
+                   int threads);
+
 /* ---- whole per-frame path (sim.hpp:241-332 per-frame items) ------------- */
 typedef struct {
   int32_t width, height, pitch;

@@ -184,9 +184,15 @@ class MultiCameraPath:
         self.sched.close()
 
     # ---- 1. device: K1-K4 for every camera, descriptors on the device -------
-    def run_planes(self):
+    def run_planes(self, mask_events=None):
+        """`mask_events` (optional (start, stop) CUDA events) bracket the
+        mask launch (K1 + K1b) on `stream`."""
         lib, F = N.lib(), len(self.cameras) * self.n
+        if mask_events:
+            self.ctx.record(mask_events[0], self.stream)
         check(lib.tg_pipeline_stage_mask(self.pipe.handle, F, self.d_cur, self.d_prev, self.stream))
+        if mask_events:
+            self.ctx.record(mask_events[1], self.stream)
         check(lib.tg_pipeline_stage_plan(self.pipe.handle, F, self.d_ids, self.d_gen, 0,
                                          self.stream))
 
@@ -253,19 +259,21 @@ class MultiCameraPath:
         self.ctx.record(self._gdone, self.gstream)
         check(N.lib().tg_stream_wait_event(self.ctx.handle, self.stream, self._gdone))
 
-    def run_pipelined(self, steps: int) -> int:
+    def run_pipelined(self, steps: int, mask_events=None) -> int:
         """`steps` passes over the shard's frames with the host batcher of
         pass i overlapping the device planes (K1-K4) of pass i+1, which are
         queued behind pass i's descriptor all-gather and read-back
         (double-buffered pinned memory), so the device never waits for the
-        host; K5 of pass i runs on `gstream`.  Returns the last pass's canvas
-        count; `stream` is joined with every gather."""
+        host; K5 of pass i runs on `gstream`.  mask_events[i] (optional
+        (start, stop) pair or None) brackets pass i's mask launch.  Returns
+        the last pass's canvas count; `stream` is joined with every gather."""
         n_canv = 0
-        self.run_planes()
+        ev = (lambda i: mask_events[i] if mask_events else None)
+        self.run_planes(ev(0))
         self.fetch_descriptors(0)
         for i in range(steps):
             if i + 1 < steps:  # queued behind pass i's read-back: no host wait in between
-                self.run_planes()
+                self.run_planes(ev(i + 1))
                 self.fetch_descriptors((i + 1) % 2)
             desc = self.compact_descriptors(i % 2)
             self.schedule(desc)
