@@ -86,15 +86,6 @@ struct tg_pipeline {
   uint32_t* psync = nullptr;  // [3] plan frame ticket, finished CTAs, epoch
   int last_frames = 0;
   tg_pipeline_stats stats{};
-  // K1b task order of the fused mask launch, one table per frame count
-  // (mask_task_order), built on first use and kept: a captured graph's copy
-  // node reads its host table at every replay
-  struct TaskTable {
-    int frames;
-    uint32_t* d;
-    uint32_t* h;
-  };
-  std::vector<TaskTable> task_tables;
   // optional dense descriptor output (tg_pipeline_set_descriptor_output)
   tg_descriptor_header* desc_head = nullptr;
   int64_t desc_cap = 0;
@@ -688,39 +679,13 @@ void tg_pipeline_destroy(tg_pipeline* p) {
                   p->id_state, p->look, p->psync};
   for (void* b : bufs)
     if (b) cudaFree(b);
-  for (auto& t : p->task_tables) {
-    cudaFree(t.d);
-    cudaFreeHost(t.h);
-  }
   delete p;
-}
-
-// The mask stage keeps the raw foreground rows its K1b tasks read back in L2
-// with an evict_last policy; that priority only holds within the device's
-// persisting-L2 set-aside, so a pipeline raises the set-aside to the device
-// maximum (TG_L2_PERSIST_MB overrides; 0 leaves it alone).
-static void ensure_l2_set_aside(int device) {
-  static EnvInt env{"TG_L2_PERSIST_MB"};
-  const int mb = env.get();
-  if (mb == 0) return;
-  int maxp = 0;
-  if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device) != cudaSuccess ||
-      maxp <= 0) {
-    cudaGetLastError();
-    return;
-  }
-  const size_t want = mb > 0 ? std::min<size_t>(static_cast<size_t>(mb) << 20, maxp) : maxp;
-  size_t cur = 0;
-  if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess && cur < want)
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-  cudaGetLastError();
 }
 
 tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_pipeline** out) {
   *out = nullptr;
   tg_status s = use_device(ctx);
   if (s) return s;
-  ensure_l2_set_aside(ctx->device);
   const tg_pipeline_params& q = *params;
   if (q.width < 16 || q.height < 1 || q.width % 16 != 0 || q.width > 32 * 256)
     return fail(TG_ERR_INVALID_ARGUMENT, "frame width must be a multiple of 16 in [16, 8192]");
@@ -761,9 +726,9 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
     return cudaMalloc(reinterpret_cast<void**>(ptr), std::max<size_t>(1, count) * sizeof(**ptr));
   };
   cudaError_t e = cudaSuccess;
-  if (!e) e = alloc(&p->raw, F * q.height * mask_raw_pitch(q.width));
+  if (!e) e = alloc(&p->raw, F * q.height * p->mask_words);
   // K1 counters followed by the activity bits (p->active): one memset per launch
-  const size_t sync_words = mask_sync_words(q.height, ctx->sms, q.max_frames);
+  const size_t sync_words = mask_sync_words(q.height, ctx->sms);
   if (!e) e = alloc(&p->mask_sync, sync_words + F * cy * p->act_words);
   if (!e) p->active = p->mask_sync + sync_words;
   if (!e) e = alloc(&p->cells, F * cx * cy);
@@ -821,27 +786,6 @@ tg_status tg_pipeline_stage_mask_cells(tg_pipeline* p, int32_t n_frames, void* s
   return TG_OK;
 }
 
-// The fused mask launch's task table for n_frames (built and uploaded on
-// first use; allocation is not capturable, so graph creation calls this
-// before capturing).
-static tg_status task_table(tg_pipeline* p, int n_frames, cudaStream_t st, const uint32_t** out) {
-  for (const auto& t : p->task_tables)
-    if (t.frames == n_frames) {
-      *out = t.d;
-      return TG_OK;
-    }
-  const size_t n = mask_task_count(p->p.height, n_frames);
-  tg_pipeline::TaskTable t{n_frames, nullptr, nullptr};
-  TG_CUDA(cudaMalloc(&t.d, std::max<size_t>(n, 1) * sizeof(uint32_t)));
-  TG_CUDA(cudaMallocHost(&t.h, std::max<size_t>(n, 1) * sizeof(uint32_t)));
-  p->task_tables.push_back(t);
-  TG_CUDA(mask_task_order(n_frames, p->p.width, p->p.height, p->p.dilate_radius, p->p.pitch,
-                          p->ctx->sms, t.h));
-  TG_CUDA(cudaMemcpyAsync(t.d, t.h, n * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-  *out = t.d;
-  return TG_OK;
-}
-
 tg_status tg_pipeline_stage_mask(tg_pipeline* p, int32_t n_frames, const uint8_t* const* d_cur,
                                  const uint8_t* const* d_prev, void* stream) {
   tg_status s = use_device(p->ctx);
@@ -852,12 +796,10 @@ tg_status tg_pipeline_stage_mask(tg_pipeline* p, int32_t n_frames, const uint8_t
     return fail(TG_ERR_INVALID_ARGUMENT, "null frame pointer table");
   // K1 + K1b in one cooperative launch; separate launches if the device
   // cannot co-schedule one K1 CTA per SM (e.g. a shared GPU).
-  const uint32_t* order = nullptr;
-  if (n_frames > 0 && (s = task_table(p, n_frames, pick(p->ctx, stream), &order))) return s;
   const cudaError_t e = launch_mask_fused(
       d_cur, d_prev, n_frames, p->p.width, p->p.height, p->p.pitch, p->p.threshold,
       p->p.dilate_radius, p->raw, p->cells, p->active, p->p.keep_mask ? p->mask : nullptr,
-      p->mask_sync, order, p->p.max_frames, p->ctx->sms, pick(p->ctx, stream));
+      p->mask_sync, p->ctx->sms, pick(p->ctx, stream));
   if (e == cudaSuccess) {
     p->last_frames = n_frames;
     if (n_frames > 0) ++p->stats.mask_fused_launches;
@@ -971,8 +913,6 @@ tg_status tg_pipeline_graph_create(tg_pipeline* p, int32_t n_frames, const uint8
   tg_status s = use_device(p->ctx);
   if (s) return s;
   cudaStream_t st = pick(p->ctx, stream);
-  const uint32_t* order = nullptr;
-  if (n_frames > 0 && (s = task_table(p, n_frames, st, &order))) return s;
   tg_graph* g = new tg_graph();
   TG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   s = tg_pipeline_run(p, n_frames, d_cur, d_prev, d_frame_ids, d_gen_us, first_patch_id,

@@ -47,17 +47,11 @@
 // written, plus per-row ballot masks) saved K1 15 us but cost K1b 60 us.
 #include <algorithm>
 #include <cstdlib>
-#include <utility>
-#include <vector>
 
 #include "kernels.cuh"
 
 namespace tg {
 
-
-#ifndef TG_K1_L2KEEP
-#define TG_K1_L2KEEP 1
-#endif
 
 constexpr int kK1MaxPartWords = 64;     // 32-pixel words per unit (one per consumer lane)
 constexpr int kK1Group = 2;             // warps per consumer group
@@ -67,23 +61,16 @@ constexpr int kK1MaxSlots = 8;          // ring slots per group
 #define TG_K1_DILATE_WARPS 0
 #endif
 constexpr int kK1DilateWarps = TG_K1_DILATE_WARPS;  // fused launch: extra warps running K1b tasks
-// consumer warps, the producer warp, the progress publisher warp (fused
-// launch), then optional K1b task warps
-constexpr int kK1PubWarp = kK1Groups * kK1Group + 1;
-constexpr int kK1Threads = (kK1Groups * kK1Group + 2 + kK1DilateWarps) * 32;
+constexpr int kK1Threads = (kK1Groups * kK1Group + 1 + kK1DilateWarps) * 32;
 constexpr int kK1bBands = 4;            // cell bands per K1b task (a 64-row strip)
 constexpr int kK1SmemBudget = 227 * 1024;
 constexpr int kK1GroupWords = 30;       // K1b: output words per warp (lanes 1..30)
 constexpr int kK1MaxActWords = 16;      // K1b: act words per cell row (W <= 8192)
-#ifndef TG_K1_PUB
-#define TG_K1_PUB 8
-#endif
-constexpr int kK1Pub = TG_K1_PUB;       // frames per published progress block
 
 // ---- K1b: dilation + cell summaries ---------------------------------------
 struct DilateArgs {
-  const uint32_t* raw;    // [F][H][rpitch]: rows padded to whole 128-byte L2 lines
-  int H, W, nwords, rpitch, cells_x, cells_y, act_words;
+  const uint32_t* raw;
+  int H, W, nwords, cells_x, cells_y, act_words;
   uint32_t* cells;
   uint32_t* active;
   uint32_t* mask_out;
@@ -113,12 +100,12 @@ __device__ __forceinline__ void dilate_strip(const DilateArgs& a, int f, int cy0
   const uint32_t keep = owns ? (w == a.nwords - 1 ? lastmask : 0xffffffffu) : 0u;
   const int wc = min(max(w, 0), a.nwords - 1);  // clamped column: loads stay in bounds
   const uint32_t cmask = col_ok ? 0xffffffffu : 0u;
-  const uint32_t* fr = a.raw + static_cast<size_t>(f) * a.H * a.rpitch + wc;
+  const uint32_t* fr = a.raw + static_cast<size_t>(f) * a.H * a.nwords + wc;
   auto ld = [](const uint32_t* q) -> uint32_t { return kFused ? __ldcg(q) : __ldg(q); };
   // rows outside [0, H) read a clamped row and are masked to zero
   auto raw_row = [&](int yy) -> uint32_t {
     const uint32_t m = (yy >= 0 && yy < a.H) ? cmask : 0u;
-    return ld(fr + static_cast<size_t>(min(max(yy, 0), a.H - 1)) * a.rpitch) & m;
+    return ld(fr + static_cast<size_t>(min(max(yy, 0), a.H - 1)) * a.nwords) & m;
   };
   // window of raw rows yb0 - R .. yb0 + 15 + R; consecutive bands share 2R rows
   constexpr int kWin = kCell + 2 * R;
@@ -129,9 +116,9 @@ __device__ __forceinline__ void dilate_strip(const DilateArgs& a, int f, int cy0
     const int yb0 = (cy0 + bi) * kCell, cy = cy0 + bi;
     const bool interior = yb0 + kCell + R <= a.H;  // uniform: no row past the frame
     if (interior) {
-      const uint32_t* q = fr + static_cast<size_t>(yb0 + R) * a.rpitch;
+      const uint32_t* q = fr + static_cast<size_t>(yb0 + R) * a.nwords;
 #pragma unroll
-      for (int i = 2 * R; i < kWin; ++i) win[i] = ld(q + static_cast<size_t>(i - 2 * R) * a.rpitch) & cmask;
+      for (int i = 2 * R; i < kWin; ++i) win[i] = ld(q + static_cast<size_t>(i - 2 * R) * a.nwords) & cmask;
     } else {
 #pragma unroll
       for (int i = 2 * R; i < kWin; ++i) win[i] = raw_row(yb0 - R + i);
@@ -211,7 +198,7 @@ struct MaskArgs {
   const uint8_t* const* cur;
   const uint8_t* const* prev;
   int n_frames, W, H, pitch, rowbytes, threshold;
-  int nwords, rpitch, part_words, nparts;
+  int nwords, part_words, nparts;
   int rows_per_item;  // units per item = rows_per_item * nparts <= kK1Groups
   int nrb;            // row blocks
   int kf, ntg;        // frames per run, runs
@@ -219,14 +206,10 @@ struct MaskArgs {
   int dctas;          // fused launch: CTAs 0..dctas-1 run only K1b tasks (stream on the rest)
   int nslots;         // ring slots per group
   int slot_bytes;
-  uint32_t* raw;      // [F][H][rpitch] raw foreground bits
-  // fused launch only (blk_done == nullptr otherwise)
-  uint32_t* blk_done;   // [total_items][nblk] 1 once every raw word of the item's
-                        // kK1Pub-frame block is written (zeroed)
-  int nblk;             // progress blocks per item
+  uint32_t* raw;      // [F][H][nwords] raw foreground bits
+  // fused launch only (item_done == nullptr otherwise)
+  uint32_t* item_done;  // [total_items] warps done per item (zeroed)
   uint32_t* task_next;  // K1b task queue head (zeroed)
-  const uint32_t* task_order;  // [n_tasks] strip << 22 | frame, in the order the stream
-                               // completes them (mask_task_order)
   int radius, dgroups, strips, n_tasks;
   DilateArgs d;
 };
@@ -319,10 +302,8 @@ struct ItemK1 {
   int f0, fend, y0;
 };
 
-// Items are run-major (item = run * nrb + row block), so the CTAs of one
-// wave stream consecutive row blocks -- whole strips -- of the same frames.
 __device__ __forceinline__ ItemK1 load_item(const MaskArgs& a, int item) {
-  const int t = item / a.nrb, rb = item - t * a.nrb;
+  const int t = item % a.ntg, rb = item / a.ntg;
   ItemK1 it;
   it.f0 = t * a.kf;
   it.fend = min(a.n_frames, it.f0 + a.kf);
@@ -336,54 +317,40 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   return v;
 }
 
-// Fused launch: a K1b task is (strip, frame), every column group of it.  It
-// waits until every row block covering the strip (and its halo) has
-// published the progress block holding that frame, so the tasks trail the
-// stream front by a few frames and read the raw rows back from L2.
-__device__ __forceinline__ void wait_dilate_task(const MaskArgs& a, int sg, int f, int lane) {
+// Fused launch: K1b tasks (strip, frame, column group) in strip order, each
+// after the K1 items that write its rows have published completion.
+// Waits until the K1 items writing the rows of task t have published.
+__device__ __forceinline__ void wait_dilate_task(const MaskArgs& a, int t, int lane) {
+  const int sf = t / a.dgroups;
+  const int f = sf % a.n_frames, sg = sf / a.n_frames;
   const int cy0 = sg * kK1bBands;
   const int y_lo = max(0, cy0 * kCell - a.radius);
   const int y_hi = min(a.H, (cy0 + kK1bBands) * kCell + a.radius) - 1;
-  const int run = f / a.kf, blk = (f - run * a.kf) / kK1Pub;
+  const int run = f / a.kf;
   for (int rb = y_lo / a.rows_per_item + lane; rb <= y_hi / a.rows_per_item; rb += 32) {
-    const uint32_t* flag = a.blk_done + static_cast<size_t>(run * a.nrb + rb) * a.nblk + blk;
-    while (ld_acquire(flag) == 0) __nanosleep(128);
+    const int rows = min(a.rows_per_item, a.H - rb * a.rows_per_item);
+    const uint32_t want = static_cast<uint32_t>(kK1Group * a.nparts * rows);
+    const uint32_t* flag = a.item_done + rb * a.ntg + run;
+    while (ld_acquire(flag) < want) __nanosleep(256);
   }
 }
 
-// After a (strip, frame) task the strip's interior raw rows -- read by no
-// other task -- are dead: their L2 lines are dropped instead of written back
-// to HBM.  Rows within R of a strip edge stay (the neighbouring strip reads
-// them as its halo).
-__device__ __forceinline__ void retire_strip_rows(const MaskArgs& a, int f, int cy0, int lane) {
-  const int y0 = cy0 == 0 ? 0 : cy0 * kCell + a.radius;
-  const int yend = (cy0 + kK1bBands) * kCell;
-  const int y1 = yend >= a.H ? a.H : yend - a.radius;
-  const int lpr = a.rpitch / 32;  // 128-byte lines per row
-  const uint32_t* base = a.raw + (static_cast<size_t>(f) * a.H + y0) * a.rpitch;
-  for (int i = lane; i < (y1 - y0) * lpr; i += 32) discard_l2(base + static_cast<size_t>(i) * 32);
-}
-
-__device__ __forceinline__ void run_dilate_task(const MaskArgs& a, int sg, int f, int lane) {
+__device__ __forceinline__ void run_dilate_task(const MaskArgs& a, int t, int lane) {
   __syncwarp();
-  const int cy0 = sg * kK1bBands;
-  for (int wi = 0; wi < a.dgroups; ++wi) {
-    switch (a.radius) {
+  __threadfence();
+  const int wi = t % a.dgroups, sf = t / a.dgroups;
+  const int f = sf % a.n_frames, cy0 = sf / a.n_frames * kK1bBands;
+  switch (a.radius) {
 #define TG_DILATE_TASK(R) \
   case R:                 \
     dilate_strip<R, true>(a.d, f, cy0, wi, lane, nullptr); \
     break;
-      TG_DILATE_TASK(0) TG_DILATE_TASK(1) TG_DILATE_TASK(2) TG_DILATE_TASK(3) TG_DILATE_TASK(4)
-      TG_DILATE_TASK(5) TG_DILATE_TASK(6) TG_DILATE_TASK(7) TG_DILATE_TASK(8)
+    TG_DILATE_TASK(0) TG_DILATE_TASK(1) TG_DILATE_TASK(2) TG_DILATE_TASK(3) TG_DILATE_TASK(4)
+    TG_DILATE_TASK(5) TG_DILATE_TASK(6) TG_DILATE_TASK(7) TG_DILATE_TASK(8)
 #undef TG_DILATE_TASK
-      default:
-        break;
-    }
+    default:
+      break;
   }
-#if TG_K1_L2KEEP
-  __syncwarp();  // every lane's loads of the strip are done
-  retire_strip_rows(a, f, cy0, lane);
-#endif
 }
 
 // Drains the queue, waiting for each claimed task's items.
@@ -393,11 +360,8 @@ __device__ void run_dilate_tasks(const MaskArgs& a, int lane) {
     if (lane == 0) t = static_cast<int>(atomicAdd(a.task_next, 1u));
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= a.n_tasks) return;
-    const uint32_t task = a.task_order[t];
-    const int sg = static_cast<int>(task >> 22), f = static_cast<int>(task & 0x3fffffu);
-    wait_dilate_task(a, sg, f, lane);
-    __threadfence();
-    run_dilate_task(a, sg, f, lane);
+    wait_dilate_task(a, t, lane);
+    run_dilate_task(a, t, lane);
   }
 }
 
@@ -411,9 +375,6 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
   uint64_t* empty = full + NS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = a.rows_per_item * a.nparts;
-  // consumer warp w's progress: (item sequence number << 20) | diffs done in it
-  __shared__ uint32_t s_prog[kK1Groups * kK1Group];
-  if (threadIdx.x < kK1Groups * kK1Group) s_prog[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
@@ -430,37 +391,9 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
     run_dilate_tasks(a, lane);
     return;
   }
-  const bool fused = a.blk_done != nullptr;
+  const bool fused = a.item_done != nullptr;
 
-  if (warp == kK1PubWarp) {
-    // ===== publisher: a progress block of an item is out once every live
-    // consumer warp has passed it; one gpu-scope fence per block and CTA
-    // (consumers only fence at CTA scope) =====
-    if (!fused) return;
-    for (int item = scta, seq = 0; item < a.total_items; item += nscta, ++seq) {
-      const ItemK1 it = load_item(a, item);
-      const int nfr = it.fend - it.f0;
-      // lane w watches consumer warp w if its unit lies inside the frame
-      const int g = lane / kK1Group;
-      const bool live = lane < kK1Groups * kK1Group && g < units && it.y0 + g / a.nparts < a.H;
-      for (int b = 0; b * kK1Pub < nfr; ++b) {
-        const uint32_t target = static_cast<uint32_t>(seq) << 20 |
-                                static_cast<uint32_t>(min((b + 1) * kK1Pub, nfr));
-        while (!__all_sync(0xffffffffu,
-                           !live || *reinterpret_cast<volatile uint32_t*>(&s_prog[lane]) >= target))
-          __nanosleep(64);
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        if (lane == 0)
-          asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(
-                           a.blk_done + static_cast<size_t>(item) * a.nblk + b),
-                       "r"(1u)
-                       : "memory");
-      }
-    }
-    run_dilate_tasks(a, lane);
-    return;
-  }
-  if (warp > kK1PubWarp) {  // K1b task warps (fused launch)
+  if (warp > kK1Groups * kK1Group) {  // K1b task warps (fused launch)
     if (fused) run_dilate_tasks(a, lane);
     return;
   }
@@ -470,11 +403,6 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
     const bool mine = g < units;
     uint32_t used = 0, fills = 0;  // per ring slot: filled before; fill-count parity
     int k = 0;                     // ring slot of the next stage
-#if TG_K1_L2KEEP
-    // frames stream through once: their lines go first, so the raw rows
-    // the K1b tasks read back stay in L2
-    const uint64_t pol_stream = l2_evict_first();
-#endif
     for (int item = scta; item < a.total_items; item += nscta) {
       const ItemK1 it = load_item(a, item);
       const int row = it.y0 + g / a.nparts, part = g % a.nparts;
@@ -493,13 +421,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
             int out;
             const uint8_t* src = ch.next(a, &out) + off;
             mbar_arrive_expect_tx(&full[slot], bytes);
-#if TG_K1_L2KEEP
-            if (fused)
-              bulk_g2s_hint(slots + static_cast<size_t>(slot) * a.slot_bytes, src, bytes,
-                            &full[slot], pol_stream);
-            else
-#endif
-              bulk_g2s(slots + static_cast<size_t>(slot) * a.slot_bytes, src, bytes, &full[slot]);
+            bulk_g2s(slots + static_cast<size_t>(slot) * a.slot_bytes, src, bytes, &full[slot]);
             used |= bit;
             fills ^= bit;
             if (++k == S) k = 0;
@@ -522,9 +444,6 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
   const int col = (warp - g * kK1Group) * 32 + lane;  // word within the part
   const bool in_slot = 96 * (col + 1) <= a.slot_bytes;  // lane's bytes inside a slot
   uint32_t fpar = 0;  // bit k: parity of the next full phase of ring slot k
-#if TG_K1_L2KEEP
-  const uint64_t pol_keep = l2_evict_last();  // raw words: read back by K1b soon
-#endif
   int k = 0;
   for (int item = scta; g < units && item < a.total_items; item += nscta) {
     const ItemK1 it = load_item(a, item);
@@ -532,8 +451,8 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
     if (row >= a.H) continue;
     const int w = part * a.part_words + col;
     const bool valid = col < a.part_words && w < a.nwords;
-    uint32_t* out = a.raw + static_cast<size_t>(row) * a.rpitch + w;
-    const size_t fstride = static_cast<size_t>(a.H) * a.rpitch;
+    uint32_t* out = a.raw + static_cast<size_t>(row) * a.nwords + w;
+    const size_t fstride = static_cast<size_t>(a.H) * a.nwords;
     Chain ch{it.f0, it.fend, true};
     uint4 P[6] = {}, C[6] = {};
     while (!ch.done()) {
@@ -549,26 +468,15 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
       if (f >= 0) {
         uint32_t fw = fg_word<kLow>(C, P, t1);
         if (w == a.nwords - 1) fw &= lastmask;
-#if TG_K1_L2KEEP
-        if (valid) {
-          if (fused)
-            st_hint(out + static_cast<size_t>(f) * fstride, fw, pol_keep);
-          else
-            out[static_cast<size_t>(f) * fstride] = fw;
-        }
-#else
         if (valid) out[static_cast<size_t>(f) * fstride] = fw;
-#endif
-        if (fused) {  // progress for the publisher: this diff's raw words are written
-          __threadfence_block();
-          __syncwarp();
-          if (lane == 0)
-            *reinterpret_cast<volatile uint32_t*>(&s_prog[warp]) =
-                static_cast<uint32_t>((item - scta) / nscta) << 20 | static_cast<uint32_t>(f - it.f0 + 1);
-        }
       }
 #pragma unroll
       for (int q = 0; q < 6; ++q) P[q] = C[q];
+    }
+    if (fused) {  // publish: this warp's raw words of the item are written
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(&a.item_done[item], 1u);
     }
   }
   if (fused) run_dilate_tasks(a, lane);
@@ -592,7 +500,6 @@ static DilateArgs dilate_args(const uint32_t* d_raw, int W, int H, uint32_t* d_c
   d.H = H;
   d.W = W;
   d.nwords = ceil_div(W, 32);
-  d.rpitch = mask_raw_pitch(W);
   d.cells_x = ceil_div(W, kCell);
   d.cells_y = ceil_div(H, kCell);
   d.act_words = ceil_div(d.cells_x, 32);
@@ -616,7 +523,6 @@ static cudaError_t plan_k1(MaskArgs& a, const uint8_t* const* d_cur, const uint8
   a.rowbytes = 3 * W;
   a.threshold = threshold;
   a.nwords = ceil_div(W, 32);
-  a.rpitch = mask_raw_pitch(W);
   a.nparts = ceil_div(a.nwords, kK1MaxPartWords);
   if (a.nparts > kK1Groups) return cudaErrorInvalidConfiguration;  // W > 16384
   a.part_words = ceil_div(a.nwords, a.nparts);
@@ -656,99 +562,49 @@ cudaError_t launch_mask_fg(const uint8_t* const* d_cur, const uint8_t* const* d_
   return cudaGetLastError();
 }
 
-// The task queue head + the progress blocks (total_items = runs x row blocks
-// <= (8 sms / row blocks + 1) x row blocks <= 8 sms + H, plan_k1; blocks per
-// item <= ceil(frames / kK1Pub)).
-size_t mask_sync_words(int H, int sms, int max_frames) {
-  return 2 + (static_cast<size_t>(8) * sms + H) * static_cast<size_t>(ceil_div(max_frames, kK1Pub));
-}
-
-size_t mask_task_count(int H, int n_frames) {
-  return static_cast<size_t>(ceil_div(ceil_div(H, kCell), kK1bBands)) * n_frames;
-}
-
-// Dedicated K1b CTAs: about 9 % of the SMs (the K1b share of the work),
-// rounded so every streaming CTA gets the same number of items -- the
-// stream then ends on all SMs at once (4K x 300: 1,620 items on 135 CTAs,
-// 13 K1b CTAs; 14 K1b CTAs leave some streaming CTAs a 13th item).
-static void fused_split(int total_items, int sms, int* dctas, int* grid) {
-  const int reserve = (sms * 9 + 50) / 100;
-  const int per_cta = ceil_div(total_items, std::max(1, sms - reserve));
-  const int streaming = ceil_div(total_items, per_cta);
-  *dctas = std::max(0, std::min(sms - 1, env_or(g_env_dctas, sms - streaming)));
-  *grid = std::min(total_items + *dctas, sms);
-}
-
-// K1b task order of a fused launch: (strip, frame) tasks sorted by when the
-// stream completes their rows -- the wave of the strip's last row-block item
-// (items are run-major and the streaming CTAs take them round-robin), then
-// the frame's offset in its run, then the strip.
-cudaError_t mask_task_order(int n_frames, int W, int H, int radius, int pitch, int sms,
-                            uint32_t* out) {
-  MaskArgs a;
-  size_t smem = 0;
-  cudaError_t e = plan_k1(a, nullptr, nullptr, n_frames, W, H, pitch, 25, nullptr, sms, &smem);
-  if (e != cudaSuccess) return e;
-  int dctas = 0, grid = 0;
-  fused_split(a.total_items, sms, &dctas, &grid);
-  const long long nscta = std::max(1, grid - dctas);
-  const int strips = ceil_div(ceil_div(H, kCell), kK1bBands);
-  std::vector<std::pair<unsigned long long, uint32_t>> tasks;
-  tasks.reserve(static_cast<size_t>(strips) * n_frames);
-  for (int t = 0; t < a.ntg; ++t) {
-    const int f0 = t * a.kf, f1 = std::min(n_frames, f0 + a.kf);
-    for (int sg = 0; sg < strips; ++sg) {
-      const int y_hi = std::min(H, (sg + 1) * kK1bBands * kCell + radius) - 1;
-      const long long item = static_cast<long long>(t) * a.nrb + y_hi / a.rows_per_item;
-      const unsigned long long wave = static_cast<unsigned long long>(item / nscta);
-      for (int f = f0; f < f1; ++f)
-        tasks.emplace_back(wave << 44 | static_cast<unsigned long long>(f - f0) << 20 |
-                               static_cast<unsigned long long>(sg),
-                           static_cast<uint32_t>(sg) << 22 | static_cast<uint32_t>(f));
-    }
-  }
-  std::sort(tasks.begin(), tasks.end());
-  for (size_t i = 0; i < tasks.size(); ++i) out[i] = tasks[i].second;
-  return cudaSuccess;
-}
+// The task queue head + item counters: total_items = runs x row blocks <=
+// (8 sms / row blocks + 1) x row blocks <= 8 sms + H (plan_k1).
+size_t mask_sync_words(int H, int sms) { return static_cast<size_t>(8) * sms + H + 2; }
 
 cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                               int n_frames, int W, int H, int pitch, int threshold, int radius,
                               uint32_t* d_raw, uint32_t* d_cells, uint32_t* d_active,
-                              uint32_t* d_mask, uint32_t* d_sync, const uint32_t* d_task_order,
-                              int n_frames_cap, int sms, cudaStream_t stream) {
+                              uint32_t* d_mask, uint32_t* d_sync, int sms, cudaStream_t stream) {
   if (n_frames <= 0) return cudaSuccess;
   if (radius < 0 || radius > kMaxRadius) return cudaErrorInvalidValue;
-  if (n_frames >= (1 << 22) || ceil_div(ceil_div(H, kCell), kK1bBands) >= (1 << 10))
-    return cudaErrorInvalidValue;  // task packing: strip << 22 | frame
   MaskArgs a;
   size_t smem = 0;
   cudaError_t e = plan_k1(a, d_cur, d_prev, n_frames, W, H, pitch, threshold, d_raw, sms, &smem);
   if (e != cudaSuccess) return e;
   a.d = dilate_args(d_raw, W, H, d_cells, d_active, d_mask);
   if (a.d.act_words > kK1MaxActWords) return cudaErrorInvalidConfiguration;
-  const size_t sync_words = mask_sync_words(H, sms, n_frames_cap);
-  a.strips = ceil_div(a.d.cells_y, kK1bBands);
-  a.nblk = ceil_div(a.kf, kK1Pub);
-  if (1 + static_cast<size_t>(a.total_items) * a.nblk > sync_words) return cudaErrorInvalidConfiguration;
+  const size_t sync_words = mask_sync_words(H, sms);
+  if (static_cast<size_t>(a.total_items) + 1 > sync_words) return cudaErrorInvalidConfiguration;
   a.radius = radius;
   a.dgroups = ceil_div(a.nwords, kK1GroupWords);
-  a.n_tasks = a.strips * n_frames;
+  a.strips = ceil_div(a.d.cells_y, kK1bBands);
+  a.n_tasks = a.strips * n_frames * a.dgroups;
   a.task_next = d_sync;
-  a.blk_done = d_sync + 1;
-  a.task_order = d_task_order;
-  const size_t used = 1 + static_cast<size_t>(a.total_items) * a.nblk;
+  a.item_done = d_sync + 1;
   const size_t act_words = static_cast<size_t>(n_frames) * a.d.cells_y * a.d.act_words;
-  if (d_active == d_sync + sync_words && used * 4 >= sync_words) {  // one memset clears both
+  if (d_active == d_sync + sync_words) {  // one allocation: one memset clears both
     e = cudaMemsetAsync(d_sync, 0, sizeof(uint32_t) * (sync_words + act_words), stream);
   } else {
-    e = cudaMemsetAsync(d_sync, 0, sizeof(uint32_t) * used, stream);
+    e = cudaMemsetAsync(d_sync, 0, sizeof(uint32_t) * (a.total_items + 1), stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_active, 0, sizeof(uint32_t) * act_words, stream);
   }
   if (e != cudaSuccess) return e;
   // every CTA must be resident: task warps wait on items of other CTAs
-  int grid = 0;
-  fused_split(a.total_items, sms, &a.dctas, &grid);
+  // Dedicated K1b CTAs: about 9 % of the SMs (the K1b share of the work),
+  // rounded so every streaming CTA gets the same number of items -- the
+  // stream then ends on all SMs at once (4K x 300: 1,620 items on 135 CTAs,
+  // 13 K1b CTAs; mask stage 1.276 -> 1.255 ms, while 14 K1b CTAs leave some
+  // streaming CTAs a 13th item: 1.306 ms).
+  const int reserve = (sms * 9 + 50) / 100;
+  const int per_cta = ceil_div(a.total_items, std::max(1, sms - reserve));
+  const int streaming = ceil_div(a.total_items, per_cta);
+  a.dctas = std::max(0, std::min(sms - 1, env_or(g_env_dctas, sms - streaming)));
+  const int grid = std::min(a.total_items + a.dctas, sms);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kK1Threads);

@@ -6,20 +6,6 @@
 namespace tg {
 
 // ---- K1 (k_mask.cu) --------------------------------------------------------
-// Words per raw-bitmap row: ceil(W/32) rounded up to whole 128-byte lines,
-// an odd number of them, so consecutive rows do not all start on the same
-// L2 slices / HBM channels (a 512-byte pitch measured +11 % on K1).
-// (TG_RAW_PITCH 0: unpadded ceil(W/32) words -- probes only: lines then
-// straddle rows; 2: whole lines, even counts allowed.)
-#ifndef TG_RAW_PITCH
-#define TG_RAW_PITCH 1
-#endif
-inline int mask_raw_pitch(int W) {
-  if (TG_RAW_PITCH == 0) return (W + 31) / 32;
-  int lines = (W + 1023) / 1024;
-  if (TG_RAW_PITCH == 1 && lines % 2 == 0) ++lines;
-  return lines * 32;
-}
 cudaError_t launch_mask_fg(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                            int n_frames, int W, int H, int pitch, int threshold, uint32_t* d_raw,
                            int sms, cudaStream_t stream);
@@ -27,19 +13,13 @@ cudaError_t launch_dilate_cells(const uint32_t* d_raw, int n_frames, int W, int 
                                 uint32_t* d_cells, uint32_t* d_active, uint32_t* d_mask,
                                 cudaStream_t stream);
 // K1 + K1b in one cooperative launch (K1b tasks run beside the stream);
-// d_sync: mask_sync_words(H, sms, n_frames_cap) u32 of scratch; when d_active
-// follows it directly (one allocation) a single memset clears both.
-size_t mask_sync_words(int H, int sms, int max_frames);
-// K1b tasks of a fused launch over n_frames frames (mask_task_count entries,
-// host array) in the order the stream completes their rows.
-size_t mask_task_count(int H, int n_frames);
-cudaError_t mask_task_order(int n_frames, int W, int H, int radius, int pitch, int sms,
-                            uint32_t* out);
+// d_sync: mask_sync_words(H, sms) u32 of scratch; when d_active follows it
+// directly (one allocation) a single memset clears both.
+size_t mask_sync_words(int H, int sms);
 cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                               int n_frames, int W, int H, int pitch, int threshold, int radius,
                               uint32_t* d_raw, uint32_t* d_cells, uint32_t* d_active,
-                              uint32_t* d_mask, uint32_t* d_sync, const uint32_t* d_task_order,
-                              int n_frames_cap, int sms, cudaStream_t stream);
+                              uint32_t* d_mask, uint32_t* d_sync, int sms, cudaStream_t stream);
 
 // ---- K2-K4 per-frame planner + frame-order prefix (k_plan.cu) --------------
 struct PlanArgs {
