@@ -7,6 +7,8 @@
 // there is no CPU fallback: every compute entry point returns
 // TG_ERR_NO_DEVICE when no CUDA device is usable.
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdarg>
@@ -56,6 +58,12 @@ struct tg_ctx {
   // grow-only scratch for the blocking drop-in calls
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
+  // pinned, device-mapped staging of the blocking drop-in calls: the host
+  // writes inputs the kernel reads in place and reads outputs the kernel
+  // wrote (zero copy), so a call is one launch + one synchronization
+  uint8_t* h_stage = nullptr;
+  uint8_t* d_stage = nullptr;
+  size_t stage_bytes = 0;
   // stream-ordered staging for explicit gather plans (tg_stitch_gather,
   // tg_batcher_gather)
   Job* g_jobs = nullptr;
@@ -110,12 +118,18 @@ cudaStream_t pick(tg_ctx* ctx, void* stream) {
   return stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
 }
 
+tg_status device_error_status(const DevError& e);
+
 // Reads and clears the device error latch.
 tg_status check_device_error(tg_ctx* ctx) {
   DevError e;
   TG_CUDA(cudaMemcpy(&e, ctx->d_err, sizeof(e), cudaMemcpyDeviceToHost));
   if (e.code == 0) return TG_OK;
   TG_CUDA(cudaMemset(ctx->d_err, 0, sizeof(DevError)));
+  return device_error_status(e);
+}
+
+tg_status device_error_status(const DevError& e) {
   switch (e.kind) {
     case kErrRoiOutside:  // partition.hpp:106-108
       return fail(static_cast<tg_status>(e.code), "roi outside frame (roi index %lld)", e.a);
@@ -152,6 +166,40 @@ tg_status scratch(tg_ctx* ctx, size_t bytes, void** out) {
 }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Waits until a kernel of the blocking drop-in path has written its result
+// flag (its last store, after a system-scope fence) into mapped host memory:
+// a spin on host memory instead of a stream synchronization.  After 20 ms it
+// synchronizes the stream instead, which also reports a failed launch.
+tg_status await_flag(tg_ctx* ctx, const int32_t* flag, int32_t sentinel) {
+  const volatile int32_t* f = flag;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (uint32_t it = 1; *f == sentinel; ++it) {
+    if ((it & 1023u) == 0 &&
+        std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(20)) {
+      TG_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (*f == sentinel) return fail(TG_ERR_CUDA, "device call finished without a result");
+      break;
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  return TG_OK;
+}
+
+tg_status stage(tg_ctx* ctx, size_t bytes, uint8_t** h, uint8_t** d) {
+  if (bytes > ctx->stage_bytes) {
+    if (ctx->h_stage) TG_CUDA(cudaFreeHost(ctx->h_stage));
+    ctx->h_stage = ctx->d_stage = nullptr;
+    ctx->stage_bytes = 0;
+    const size_t want = std::max<size_t>(align_up(bytes, 4096), 64 << 10);
+    TG_CUDA(cudaHostAlloc(&ctx->h_stage, want, cudaHostAllocMapped));
+    TG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->d_stage), ctx->h_stage, 0));
+    ctx->stage_bytes = want;
+  }
+  *h = ctx->h_stage;
+  *d = ctx->d_stage;
+  return TG_OK;
+}
 
 // Lays out several arrays in one scratch allocation.
 struct Carver {
@@ -267,6 +315,7 @@ void tg_ctx_destroy(tg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->d_scratch) cudaFree(ctx->d_scratch);
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   if (ctx->g_jobs) cudaFree(ctx->g_jobs);
   if (ctx->g_ranges) cudaFree(ctx->g_ranges);
   if (ctx->g_units) cudaFree(ctx->g_units);
@@ -497,19 +546,17 @@ tg_status tg_assign_rois(tg_ctx* ctx, const tg_rect* rois, int32_t n_rois, const
   Carver cv;
   const size_t o_r = cv.take<tg_rect>(n_rois), o_z = cv.take<tg_rect>(std::max(1, n_zones)),
                o_o = cv.take<int32_t>(n_rois);
-  void* base;
-  if ((s = scratch(ctx, cv.off, &base))) return s;
-  char* b = static_cast<char*>(base);
+  uint8_t *h, *d;
+  if ((s = stage(ctx, cv.off, &h, &d))) return s;
+  memcpy(h + o_r, rois, sizeof(tg_rect) * n_rois);
+  if (n_zones > 0) memcpy(h + o_z, zones, sizeof(tg_rect) * n_zones);
   cudaStream_t st = ctx->stream;
-  TG_CUDA(cudaMemcpyAsync(b + o_r, rois, sizeof(tg_rect) * n_rois, cudaMemcpyHostToDevice, st));
-  if (n_zones > 0)
-    TG_CUDA(cudaMemcpyAsync(b + o_z, zones, sizeof(tg_rect) * n_zones, cudaMemcpyHostToDevice, st));
   assign_kernel<<<(n_rois + 127) / 128, 128, 0, st>>>(
-      reinterpret_cast<tg_rect*>(b + o_r), n_rois, reinterpret_cast<tg_rect*>(b + o_z), n_zones,
-      reinterpret_cast<int32_t*>(b + o_o));
+      reinterpret_cast<tg_rect*>(d + o_r), n_rois, reinterpret_cast<tg_rect*>(d + o_z), n_zones,
+      reinterpret_cast<int32_t*>(d + o_o));
   TG_CUDA(cudaGetLastError());
-  TG_CUDA(cudaMemcpyAsync(zone_of, b + o_o, sizeof(int32_t) * n_rois, cudaMemcpyDeviceToHost, st));
   TG_CUDA(cudaStreamSynchronize(st));
+  memcpy(zone_of, h + o_o, sizeof(int32_t) * n_rois);
   for (int i = 0; i < n_rois; ++i)
     if (zone_of[i] < 0) return fail(TG_ERR_INVALID_ARGUMENT, "roi outside frame (roi index %d)", i);
   return TG_OK;
@@ -528,42 +575,40 @@ tg_status tg_partition(tg_ctx* ctx, const tg_frame_spec* frame, tg_partition_con
                o_r = cv.take<tg_rect>(std::max(1, n_rois)), o_id = cv.take<uint64_t>(1),
                o_p = cv.take<tg_patch_meta>(nz), o_n = cv.take<int32_t>(1),
                o_z = cv.take<int32_t>(std::max(1, n_rois));
-  void* base;
-  if ((s = scratch(ctx, cv.off, &base))) return s;
-  char* b = static_cast<char*>(base);
-  cudaStream_t st = ctx->stream;
+  uint8_t *h, *d;
+  if ((s = stage(ctx, cv.off, &h, &d))) return s;
   const int32_t offs[2] = {0, n_rois};
-  TG_CUDA(cudaMemcpyAsync(b + o_f, frame, sizeof(tg_frame_spec), cudaMemcpyHostToDevice, st));
-  TG_CUDA(cudaMemcpyAsync(b + o_off, offs, sizeof(offs), cudaMemcpyHostToDevice, st));
-  if (n_rois > 0)
-    TG_CUDA(cudaMemcpyAsync(b + o_r, rois, sizeof(tg_rect) * n_rois, cudaMemcpyHostToDevice, st));
-  TG_CUDA(cudaMemcpyAsync(b + o_id, &first_patch_id, 8, cudaMemcpyHostToDevice, st));
+  memcpy(h + o_f, frame, sizeof(tg_frame_spec));
+  memcpy(h + o_off, offs, sizeof(offs));
+  if (n_rois > 0) memcpy(h + o_r, rois, sizeof(tg_rect) * n_rois);
+  memcpy(h + o_id, &first_patch_id, 8);
+  const int32_t pending = -1;
+  memcpy(h + o_n, &pending, 4);
+  cudaStream_t st = ctx->stream;
   PartitionBatchArgs a;
   a.n_frames = 1;
   a.X = cfg.zones_x;
   a.Y = cfg.zones_y;
   a.bpp = bytes_per_pixel;
-  a.frames = reinterpret_cast<tg_frame_spec*>(b + o_f);
-  a.roi_offsets = reinterpret_cast<int32_t*>(b + o_off);
-  a.rois = reinterpret_cast<tg_rect*>(b + o_r);
-  a.first_ids = reinterpret_cast<uint64_t*>(b + o_id);
-  a.patches = reinterpret_cast<tg_patch_meta*>(b + o_p);
-  a.n_patches = reinterpret_cast<int32_t*>(b + o_n);
-  a.zone_of = reinterpret_cast<int32_t*>(b + o_z);
+  a.frames = reinterpret_cast<tg_frame_spec*>(d + o_f);
+  a.roi_offsets = reinterpret_cast<int32_t*>(d + o_off);
+  a.rois = reinterpret_cast<tg_rect*>(d + o_r);
+  a.first_ids = reinterpret_cast<uint64_t*>(d + o_id);
+  a.patches = reinterpret_cast<tg_patch_meta*>(d + o_p);
+  a.n_patches = reinterpret_cast<int32_t*>(d + o_n);
+  a.zone_of = reinterpret_cast<int32_t*>(d + o_z);
   a.err = ctx->d_err;
   TG_CUDA(launch_partition_batch(a, st));
-  int32_t np = 0;
-  std::vector<int32_t> zone_of(std::max(1, n_rois));
-  TG_CUDA(cudaMemcpyAsync(&np, b + o_n, 4, cudaMemcpyDeviceToHost, st));
-  if (n_rois > 0)
-    TG_CUDA(cudaMemcpyAsync(zone_of.data(), b + o_z, 4 * n_rois, cudaMemcpyDeviceToHost, st));
-  TG_CUDA(cudaStreamSynchronize(st));
-  if ((s = check_device_error(ctx))) return s;
+  // with zone_of the kernel latches no error: an RoI outside the frame shows
+  // as zone -1, reported below at the lowest index like the reference
+  if ((s = await_flag(ctx, reinterpret_cast<const int32_t*>(h + o_n), pending))) return s;
+  const int32_t* zone_of = reinterpret_cast<const int32_t*>(h + o_z);
   for (int i = 0; i < n_rois; ++i)  // the reference throws at the first bad index
     if (zone_of[i] < 0) return fail(TG_ERR_INVALID_ARGUMENT, "roi outside frame (roi index %d)", i);
+  int32_t np = 0;
+  memcpy(&np, h + o_n, 4);
   if (np > patches_cap) return fail(TG_ERR_CAPACITY, "patches buffer too small (%d patches)", np);
-  if (np > 0)
-    TG_CUDA(cudaMemcpy(patches, b + o_p, sizeof(tg_patch_meta) * np, cudaMemcpyDeviceToHost));
+  if (np > 0) memcpy(patches, h + o_p, sizeof(tg_patch_meta) * np);
   *n_patches = np;
   return TG_OK;
 }
@@ -605,47 +650,61 @@ tg_status tg_stitch_all(tg_ctx* ctx, const tg_patch_meta* queue, int32_t n, tg_c
     if (n_free) *n_free = 0;
     return TG_OK;
   }
-  // Staging for the blocking call: queue, offsets, placements, counts, free list.
+  // queue in, placements, counts and the final free list out through the
+  // mapped staging; the kernel builds a short queue's free list in shared
+  // memory (a long one's in device scratch, copied back after a sync)
+  const bool staged = n <= kStitchStage;
+  const size_t nfr = 2 * static_cast<size_t>(n) + 1;
   Carver cv;
   const size_t o_q = cv.take<tg_patch_meta>(n), o_off = cv.take<int32_t>(2),
                o_pl = cv.take<tg_placement>(n), o_nc = cv.take<int32_t>(1),
-               o_nf = cv.take<int32_t>(1), o_fr = cv.take<tg_free_rect>(2 * static_cast<size_t>(n) + 1);
-  void* base;
-  if ((s = scratch(ctx, cv.off, &base))) return s;
-  char* b = static_cast<char*>(base);
-  cudaStream_t st = ctx->stream;
+               o_nf = cv.take<int32_t>(1), o_fh = cv.take<tg_free_rect>(nfr);
+  uint8_t *h, *d;
+  if ((s = stage(ctx, cv.off, &h, &d))) return s;
+  void* fr_dev = d + o_fh;
+  if (!staged && (s = scratch(ctx, nfr * sizeof(tg_free_rect), &fr_dev))) return s;
   const int32_t offs[2] = {0, n};
-  TG_CUDA(cudaMemcpyAsync(b + o_q, queue, sizeof(tg_patch_meta) * n, cudaMemcpyHostToDevice, st));
-  TG_CUDA(cudaMemcpyAsync(b + o_off, offs, sizeof(offs), cudaMemcpyHostToDevice, st));
+  const int32_t pending = INT_MIN;
+  memcpy(h + o_q, queue, sizeof(tg_patch_meta) * n);
+  memcpy(h + o_off, offs, sizeof(offs));
+  memcpy(h + o_nc, &pending, 4);
+  cudaStream_t st = ctx->stream;
   StitchBatchArgs a;
   a.n_queues = 1;
   a.M = spec.width;
   a.N = spec.height;
-  a.offsets = reinterpret_cast<int32_t*>(b + o_off);
-  a.queue = reinterpret_cast<tg_patch_meta*>(b + o_q);
-  a.placements = reinterpret_cast<tg_placement*>(b + o_pl);
-  a.n_canvases = reinterpret_cast<int32_t*>(b + o_nc);
-  a.free_ws = reinterpret_cast<FreeRect*>(b + o_fr);
-  a.n_free = reinterpret_cast<int32_t*>(b + o_nf);
+  a.offsets = reinterpret_cast<int32_t*>(d + o_off);
+  a.queue = reinterpret_cast<tg_patch_meta*>(d + o_q);
+  a.placements = reinterpret_cast<tg_placement*>(d + o_pl);
+  a.n_canvases = reinterpret_cast<int32_t*>(d + o_nc);
+  a.free_ws = static_cast<FreeRect*>(fr_dev);
+  a.n_free = reinterpret_cast<int32_t*>(d + o_nf);
   a.err = ctx->d_err;
   TG_CUDA(launch_stitch_batch(a, st));
+  if (staged) {
+    if ((s = await_flag(ctx, reinterpret_cast<const int32_t*>(h + o_nc), pending))) return s;
+  } else {
+    if (free_rects)
+      TG_CUDA(cudaMemcpyAsync(h + o_fh, fr_dev, nfr * sizeof(tg_free_rect), cudaMemcpyDeviceToHost, st));
+    TG_CUDA(cudaStreamSynchronize(st));
+  }
   int32_t nc = 0, nf = 0;
-  TG_CUDA(cudaMemcpyAsync(&nc, b + o_nc, 4, cudaMemcpyDeviceToHost, st));
-  TG_CUDA(cudaMemcpyAsync(&nf, b + o_nf, 4, cudaMemcpyDeviceToHost, st));
-  TG_CUDA(cudaStreamSynchronize(st));
-  if ((s = check_device_error(ctx))) return s;
-  TG_CUDA(cudaMemcpy(placements, b + o_pl, sizeof(tg_placement) * n, cudaMemcpyDeviceToHost));
+  memcpy(&nc, h + o_nc, 4);
+  if (nc < 0) {  // the kernel latched an error (oversize patch / capacity)
+    if ((s = check_device_error(ctx))) return s;
+    return fail(TG_ERR_CUDA, "stitch failed without a latched error");
+  }
+  memcpy(&nf, h + o_nf, 4);
+  memcpy(placements, h + o_pl, sizeof(tg_placement) * n);
   *n_canvases = nc;
   if (n_free) *n_free = nf;
   if (free_rects) {
     if (nf > free_cap) return fail(TG_ERR_CAPACITY, "free rect buffer too small (%d rects)", nf);
-    std::vector<tg_free_rect> fr(std::max(1, nf));
-    if (nf > 0)
-      TG_CUDA(cudaMemcpy(fr.data(), b + o_fr, sizeof(tg_free_rect) * nf, cudaMemcpyDeviceToHost));
-    std::sort(fr.begin(), fr.begin() + nf, [](const tg_free_rect& x, const tg_free_rect& y) {
+    tg_free_rect* fr = reinterpret_cast<tg_free_rect*>(h + o_fh);
+    std::sort(fr, fr + nf, [](const tg_free_rect& x, const tg_free_rect& y) {
       return x.canvas_index != y.canvas_index ? x.canvas_index < y.canvas_index : x.seq < y.seq;
     });
-    std::copy(fr.begin(), fr.begin() + nf, free_rects);
+    std::copy(fr, fr + nf, free_rects);
   }
   return TG_OK;
 }

@@ -478,6 +478,8 @@ cudaError_t launch_gather(const GatherArgs& a, int sms, cudaStream_t stream) {
                                                       kGatherSmem);
     if (e != cudaSuccess) return e;
     nb = nb > 0 ? nb : 1;
+    static EnvInt env_bps{"TG_K5_BPS"};  // tuning override (probes only)
+    if (env_bps.get() > 0) nb = std::min(nb, env_bps.get());
     if (dev >= 0 && dev < kMaxDevices) blocks_per_sm[dev].store(nb, std::memory_order_relaxed);
   }
   gather_kernel<<<sms * nb, kGatherThreads, kGatherSmem, stream>>>(a);

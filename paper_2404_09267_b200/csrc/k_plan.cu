@@ -389,20 +389,34 @@ __global__ void __launch_bounds__(256) partition_batch_kernel(const PartitionBat
   __syncthreads();
   partition_accumulate(a.rois + r0, r1 - r0, fs.width, fs.height, a.X, a.Y, zacc, a.err, f,
                        a.zone_of ? a.zone_of + r0 : nullptr, tid, blockDim.x);
+  __threadfence_system();  // zone_of may be host-mapped: visible before n_patches
   __syncthreads();
   if (tid >= 32) return;
   const int np = partition_emit(zacc, nz, fs.frame_id, fs.generation_time_us, fs.slo_us, a.bpp,
                                 a.first_ids[f], sp, tid);
   __syncwarp();
   for (int j = tid; j < np; j += 32) a.patches[static_cast<size_t>(f) * nz + j] = sp[j];
+  // n_patches is written last: the blocking drop-in waits on it in mapped
+  // host memory instead of synchronizing the stream
+  __threadfence_system();
+  __syncwarp();
   if (tid == 0) a.n_patches[f] = np;
 }
 
-// One warp per queue; the free set lives in the caller's workspace, the
-// queue is read and the placements written in place (no context scratch, so
+// One warp per queue; the free set ends in the caller's workspace.  A short
+// queue (<= kStitchStage patches) is first staged into shared memory by all
+// lanes at once -- the blocking drop-in passes it in mapped host memory,
+// where every dependent read would be a PCIe round trip -- and its free set
+// is kept in shared memory while it is built (copied out at the end); longer
+// queues are read in place and their free set lives in the workspace.  Placements are written in place (no context scratch, so
 // stream-ordered batches never share buffers with other calls).
+
 __global__ void __launch_bounds__(128) stitch_batch_kernel(const StitchBatchArgs a) {
-  const int q = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  __shared__ int2 s_wh[4][kStitchStage];
+  __shared__ unsigned long long s_id[4][kStitchStage];
+  __shared__ FreeRect s_fr[4][2 * kStitchStage + 1];
+  const int wq = threadIdx.x / 32;
+  const int q = blockIdx.x * (blockDim.x / 32) + wq;
   const int lane = threadIdx.x & 31;
   if (q >= a.n_queues) return;
   const int o0 = a.offsets[q], n = a.offsets[q + 1] - o0;
@@ -410,21 +424,48 @@ __global__ void __launch_bounds__(128) stitch_batch_kernel(const StitchBatchArgs
   tg_placement* pl = a.placements + o0;
   FreeRect* fl = a.free_ws + 2 * static_cast<size_t>(o0) + q;
   int nfree = 0;
-  const int nc = bssf_stitch_q(
-      [qu](int i) { return make_int2(qu[i].rect.w, qu[i].rect.h); },
-      [qu](int i) { return qu[i].patch_id; },
-      [qu, pl](int i, int c, int x, int y) {
-        tg_placement p;
-        p.patch_id = qu[i].patch_id;
-        p.canvas_index = c;
-        p.position = tg_rect{x, y, qu[i].rect.w, qu[i].rect.h};
-        p.reserved = 0;
-        pl[i] = p;
-      },
-      n, a.M, a.N, fl, 2 * n + 1, &nfree, a.err, q, lane);
+  int nc;
+  auto emit = [pl](int i, unsigned long long id, int2 wh, int c, int x, int y) {
+    tg_placement p;
+    p.patch_id = id;
+    p.canvas_index = c;
+    p.position = tg_rect{x, y, wh.x, wh.y};
+    p.reserved = 0;
+    pl[i] = p;
+  };
+  if (n <= kStitchStage) {
+    int2* wh = s_wh[wq];
+    unsigned long long* id = s_id[wq];
+    for (int i = lane; i < n; i += 32) {
+      const tg_patch_meta m = qu[i];
+      wh[i] = make_int2(m.rect.w, m.rect.h);
+      id[i] = m.patch_id;
+    }
+    __syncwarp();
+    // the free set too: every placement scans and rewrites it
+    FreeRect* sfl = s_fr[wq];
+    nc = bssf_stitch_q([wh](int i) { return wh[i]; }, [id](int i) { return id[i]; },
+                       [wh, id, emit](int i, int c, int x, int y) { emit(i, id[i], wh[i], c, x, y); },
+                       n, a.M, a.N, sfl, 2 * n + 1, &nfree, a.err, q, lane);
+    __syncwarp();
+    for (int i = lane; i < nfree; i += 32) fl[i] = sfl[i];
+  } else {
+    nc = bssf_stitch_q(
+        [qu](int i) { return make_int2(qu[i].rect.w, qu[i].rect.h); },
+        [qu](int i) { return qu[i].patch_id; },
+        [qu, emit](int i, int c, int x, int y) {
+          emit(i, qu[i].patch_id, make_int2(qu[i].rect.w, qu[i].rect.h), c, x, y);
+        },
+        n, a.M, a.N, fl, 2 * n + 1, &nfree, a.err, q, lane);
+  }
+  // n_canvases is written last: the blocking drop-in waits on it in mapped
+  // host memory instead of synchronizing the stream
+  __threadfence_system();
+  __syncwarp();
   if (lane == 0) {
-    a.n_canvases[q] = nc;
     if (a.n_free) a.n_free[q] = nfree;
+    __threadfence_system();
+    a.n_canvases[q] = nc;
   }
 }
 

@@ -86,6 +86,10 @@ struct StitchBatchArgs {
   DevError* err;
 };
 
+// stitch_batch_kernel stages queues of up to this many patches (and their
+// free sets) in shared memory.
+constexpr int kStitchStage = 128;
+
 size_t plan_smem_bytes(int cells_x, int cells_y, int max_rois);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
 cudaError_t launch_partition_batch(const PartitionBatchArgs& a, cudaStream_t stream);
