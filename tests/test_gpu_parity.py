@@ -693,3 +693,23 @@ def test_plan_look_back_survives_epoch_wrap(ctx):
     assert got["placement_list"] == want["placement_list"]
     assert got["total_canvases"] == want["total_canvases"]
     run.close()
+
+
+def test_cpp_dropin_per_frame_loop_matches_reference_build():
+    """A reference caller's per-frame loop (partition + stitch_all through
+    include/tangram, tests/cpp/dropin_bench.cpp) gives the same placements
+    as the same source built against the reference headers."""
+    cpp = os.path.join(ROOT, "tests", "cpp")
+    subprocess.check_call(["make", "-s", "-C", cpp, "dropin_bench"])
+    if os.path.isdir("/root/reference/proj/include"):
+        subprocess.check_call(["make", "-s", "-C", cpp, "dropin_bench_ref"])
+
+    def run(exe):
+        out = subprocess.run([os.path.join(cpp, exe), "120"], capture_output=True, text=True,
+                             timeout=300)
+        assert out.returncode == 0, out.stdout + out.stderr
+        return out.stdout.splitlines()[0]
+    ours = run("dropin_bench")
+    assert ours.startswith("checksum ")
+    if os.path.exists(os.path.join(cpp, "dropin_bench_ref")):
+        assert ours == run("dropin_bench_ref")
