@@ -310,7 +310,7 @@ def run_multicam(args):
     canvas_bytes = n_canv * CANVAS_BYTES
     unique = k1_bytes + patch_bytes + canvas_bytes
     b_run = 2 * F_local * FRAME_BYTES + patch_bytes + canvas_bytes
-    traffic = ncu_traffic("r02_k1_cfg4_traffic.json", F_local)
+    traffic = ncu_traffic("r02_k1_cfg4_traffic.json", F_local + len(cams))
     cfg_idx = 2 if args.config == "cfg3" else 3
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": "frames/s", "n_gpus": world,
@@ -333,18 +333,20 @@ def run_multicam(args):
                          "per GPU), no flush",
                    "pipelining": "host batcher of pass i overlaps device K1-K4 of pass i+1; K5 on "
                                  "its own stream; timed region = K whole passes"},
-        "roofline": roofline("mask_fg_kernel (K1, K1b fused), one launch per step", k1_bytes,
-                             k1_ms, traffic,
+        "roofline": roofline("mask_fg_kernel (K1), one launch per step", k1_bytes, k1_ms, traffic,
                              "frame bytes only: each camera's 30 frames + its background read "
-                             "once (masks, cell grids, the raw-bitmap round trip not credited)"),
-        "path": path_record(unique, ms_step, b_run, {"k1_mask_fused": round(k1_ms, 4)},
+                             "once (raw bitmap writes not credited); peak = the measured copy "
+                             "rate (read + write), which a read-dominated stream can exceed"),
+        "path": path_record(unique, ms_step, b_run, {"k1": round(k1_ms, 4)},
                             {"events": path._nev, "canvases": n_canv,
                              "patches_admitted": int(len(pats)),
                              "canvas_efficiency_mean": round(patch_bytes / max(1, canvas_bytes), 4),
                              "rank": rank}),
         "clocks": clk,
-        "gpu_launches": 3 * K,  # K1 (+K1b), planner (+descriptors), K5 per step
-        "mask_path": path.pipe.stats(),
+        "gpu_launches": 4 * K,  # K1, K1b, planner (+descriptors), K5 per step
+        "mask_path": {"k1": "mask_fg_kernel on every SM (cooperative-free, one CTA per SM)",
+                      "k1b": "dilate_cells_kernel as its own launch, co-running with the previous "
+                             "pass's event gather (K5 capped at 2 CTAs per SM)"},
     }
     if not args.no_e2e:
         out["e2e"] = e2e_multicam(ctx, path, args, dist, local, n_cams_total)

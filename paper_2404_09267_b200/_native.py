@@ -19,6 +19,7 @@ TG_ERR_CAPACITY = 3
 TG_ERR_CUDA = 4
 TG_ERR_NO_DEVICE = 5
 TG_ERR_COMM = 6
+TG_OPT_GATHER_CTAS_PER_SM = 1
 
 
 class tg_rect(C.Structure):
@@ -129,6 +130,7 @@ SIGNATURES = {
     "tg_ctx_stream": (vp, [vp]),
     "tg_ctx_synchronize": (st, [vp]),
     "tg_device_sm_count": (st, [vp, P(i32)]),
+    "tg_ctx_set_option": (st, [vp, i32, i64]),
     "tg_malloc_device": (st, [vp, sz, P(vp)]),
     "tg_free_device": (st, [vp, vp]),
     "tg_malloc_host": (st, [vp, sz, P(vp)]),

@@ -313,12 +313,30 @@ class Comm:
 
     @staticmethod
     def unique_id() -> bytes:
+        Comm._prefer_bundled_nccl()
         uid = N.tg_comm_id()
         check(N.lib().tg_comm_get_unique_id(C.byref(uid)))
         return bytes(uid.bytes)
 
+    @staticmethod
+    def _prefer_bundled_nccl() -> None:
+        """NCCL is opened at run time; prefer the copy a Python environment
+        ships (nvidia-nccl wheel), so a framework imported later binds to
+        the same libnccl.so.2."""
+        import importlib.util
+        import os
+        if os.environ.get("TG_NCCL_LIB"):
+            return
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for d in (spec.submodule_search_locations or []) if spec else []:
+            cand = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["TG_NCCL_LIB"] = cand
+                return
+
     @classmethod
     def nccl(cls, ctx: Context, uid: bytes, rank: int, world: int) -> "Comm":
+        cls._prefer_bundled_nccl()
         u = N.tg_comm_id()
         C.memmove(u.bytes, uid, 128)
         h = C.c_void_p()

@@ -70,8 +70,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     if failed:
         raise RuntimeError("nvcc failed for: " + ", ".join(failed))
     tmp = target + ".tmp"
-    # NCCL (the descriptor all-gather, csrc/comm.cu): the system library
-    subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lnccl"])
+    # NCCL (the descriptor all-gather, csrc/comm.cu) is opened at run time
+    subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-ldl"])
     os.replace(tmp, target)
     return target
 

@@ -5,14 +5,19 @@
 // concatenation of the ranks' blocks is the reference's camera-major patch
 // list (sim.hpp:241-262); the batcher consumes it on the host.  Pixels never
 // cross GPUs here.  Two transports behind one handle:
-//   - device: NCCL (ncclAllGather over NVLink / NVSwitch) on device
+//   - device: NCCL (ncclAllGather over NVLink / NVSwitch, opened at run
+//     time) on device
 //     buffers, stream-ordered -- one call gathers every rank's block with
 //     its record count in the header, so no separate count exchange and no
 //     host sync;
 //   - host: a caller-supplied all-gather over host buffers (tests drive the
 //     multi-rank logic through it on CPU; any out-of-band transport works).
+#include <dlfcn.h>
+
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include <nccl.h>
@@ -32,6 +37,51 @@ struct tg_comm {
 
 namespace {
 
+// NCCL is opened on first use, not linked: loading the library must not pull
+// a libnccl.so.2 into the process before a framework that ships its own
+// (newer) one (PyTorch binds to whichever copy of the soname is loaded
+// first).  Preference: a libnccl.so.2 already in the process, then
+// $TG_NCCL_LIB, then the system's.
+struct NcclApi {
+  void* handle = nullptr;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  std::string error;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    const char* env = std::getenv("TG_NCCL_LIB");
+    if (!h && env && *env) h = dlopen(env, RTLD_NOW);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) {
+      const char* e = dlerror();
+      api.error = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
+      return;
+    }
+    auto sym = [h](const char* n) { return dlsym(h, n); };
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(sym("ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(sym("ncclCommInitRank"));
+    api.all_gather = reinterpret_cast<decltype(api.all_gather)>(sym("ncclAllGather"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(sym("ncclCommDestroy"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(sym("ncclGetErrorString"));
+    if (!api.get_unique_id || !api.comm_init_rank || !api.all_gather || !api.comm_destroy ||
+        !api.error_string) {
+      api.error = "libnccl.so.2 lacks a required symbol";
+      return;
+    }
+    api.handle = h;
+  });
+  return api;
+}
+
 tg_status comm_fail(tg_status s, const char* what, const char* why) {
   char buf[512];
   snprintf(buf, sizeof(buf), "%s: %s", what, why);
@@ -41,7 +91,11 @@ tg_status comm_fail(tg_status s, const char* what, const char* why) {
 
 tg_status nccl_check(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return TG_OK;
-  return comm_fail(TG_ERR_COMM, what, ncclGetErrorString(r));
+  return comm_fail(TG_ERR_COMM, what, nccl().error_string(r));
+}
+
+tg_status nccl_loaded(const char* what) {
+  return nccl().handle ? TG_OK : comm_fail(TG_ERR_COMM, what, nccl().error.c_str());
 }
 
 }  // namespace
@@ -50,8 +104,10 @@ extern "C" {
 
 tg_status tg_comm_get_unique_id(tg_comm_id* out) {
   static_assert(sizeof(ncclUniqueId) == sizeof(tg_comm_id), "tg_comm_id mirrors ncclUniqueId");
+  tg_status s = nccl_loaded("tg_comm_get_unique_id");
+  if (s) return s;
   ncclUniqueId id;
-  const tg_status s = nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+  s = nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
   if (s) return s;
   memcpy(out->bytes, &id, sizeof(id));
   return TG_OK;
@@ -63,6 +119,7 @@ tg_status tg_comm_create(tg_ctx* ctx, const tg_comm_id* id, int32_t rank, int32_
   if (!ctx || !id) return comm_fail(TG_ERR_INVALID_ARGUMENT, "tg_comm_create", "null argument");
   if (world < 1 || rank < 0 || rank >= world)
     return comm_fail(TG_ERR_INVALID_ARGUMENT, "tg_comm_create", "need 0 <= rank < world");
+  if (tg_status ls = nccl_loaded("tg_comm_create")) return ls;
   const int dev = tg_internal_ctx_device(ctx);
   if (cudaSetDevice(dev) != cudaSuccess)
     return comm_fail(TG_ERR_NO_DEVICE, "tg_comm_create", "no CUDA device");
@@ -72,7 +129,8 @@ tg_status tg_comm_create(tg_ctx* ctx, const tg_comm_id* id, int32_t rank, int32_
   c->rank = rank;
   c->world = world;
   c->device = dev;
-  const tg_status s = nccl_check(ncclCommInitRank(&c->nccl, world, uid, rank), "ncclCommInitRank");
+  const tg_status s =
+      nccl_check(nccl().comm_init_rank(&c->nccl, world, uid, rank), "ncclCommInitRank");
   if (s) {
     delete c;
     return s;
@@ -100,7 +158,7 @@ void tg_comm_destroy(tg_comm* comm) {
   if (!comm) return;
   if (comm->nccl) {
     cudaSetDevice(comm->device);
-    ncclCommDestroy(comm->nccl);
+    nccl().comm_destroy(comm->nccl);
   }
   delete comm;
 }
@@ -121,8 +179,8 @@ tg_status tg_comm_allgather(tg_comm* comm, const void* send, size_t bytes, void*
   if (comm->nccl) {
     if (cudaSetDevice(comm->device) != cudaSuccess)
       return comm_fail(TG_ERR_CUDA, "tg_comm_allgather", "cudaSetDevice");
-    return nccl_check(ncclAllGather(send, recv, bytes, ncclUint8, comm->nccl,
-                                    static_cast<cudaStream_t>(stream)),
+    return nccl_check(nccl().all_gather(send, recv, bytes, ncclUint8, comm->nccl,
+                                        static_cast<cudaStream_t>(stream)),
                       "ncclAllGather");
   }
   if (comm->fn(send, bytes, recv, comm->user) != 0)

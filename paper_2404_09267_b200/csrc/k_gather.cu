@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kGatherThreads, TG_GATHER_MIN_BLOCKS) gather_k
 #endif
 }
 
-cudaError_t launch_gather(const GatherArgs& a, int sms, cudaStream_t stream) {
+cudaError_t launch_gather(const GatherArgs& a, int sms, int max_ctas_per_sm, cudaStream_t stream) {
   // resident CTAs per SM, per device (0 = not yet queried)
   static std::atomic<int> blocks_per_sm[kMaxDevices] = {};
   int dev = 0;
@@ -478,10 +478,9 @@ cudaError_t launch_gather(const GatherArgs& a, int sms, cudaStream_t stream) {
                                                       kGatherSmem);
     if (e != cudaSuccess) return e;
     nb = nb > 0 ? nb : 1;
-    static EnvInt env_bps{"TG_K5_BPS"};  // tuning override (probes only)
-    if (env_bps.get() > 0) nb = std::min(nb, env_bps.get());
     if (dev >= 0 && dev < kMaxDevices) blocks_per_sm[dev].store(nb, std::memory_order_relaxed);
   }
+  if (max_ctas_per_sm > 0) nb = std::min(nb, max_ctas_per_sm);
   gather_kernel<<<sms * nb, kGatherThreads, kGatherSmem, stream>>>(a);
   return cudaGetLastError();
 }

@@ -38,9 +38,9 @@ def test_bench_default_line_is_config4():
     assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 4 and d["warmup"] == 3
     _check_roofline(d["roofline"])
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
-    assert d["gpu_launches"] == 3 * 4
+    assert d["gpu_launches"] == 4 * 4
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
-    assert d["mask_path"]["mask_fused_launches"] > 0
+    assert "k1b" in d["mask_path"]
     cb = d["cpu_baseline"]
     assert cb["value"] > 0 and cb["cores"] >= 1 and cb["lscpu_model"]
     sec = d["secondary"]["cfg2"]
@@ -53,6 +53,7 @@ def test_bench_cfg2_line():
     assert REQUIRED <= set(d)
     _check_roofline(d["roofline"])
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] == 12
+    assert d["mask_path"]["mask_fused_launches"] > 0
 
 
 def test_bench_reference_arm_line():

@@ -19,17 +19,26 @@ path = MC.MultiCameraPath(ctx, list(range(ncam)), W, H, frames, bench.SIM_PROFIL
 path.run_pipelined(3)
 ctx.synchronize()
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 8
-names = ("k1a", "k1b", "pl", "fe", "g0", "g1")
+names = ("k1a", "k1b", "k1c", "pl", "fe", "g0", "g1")
+split = __import__("os").environ.get("TG_FUSED_MASK") != "1"  # MultiCameraPath: split
 ev = {k: [ctx.event() for _ in range(steps + 1)] for k in names}
 host = []
 lib = N.lib()
 F = ncam * frames
 
 
-def planes(i):
+def planes(i):  # MultiCameraPath.run_planes, with events
     ctx.record(ev["k1a"][i], path.stream)
-    A.check(lib.tg_pipeline_stage_mask(path.pipe.handle, F, path.d_cur, path.d_prev, path.stream))
-    ctx.record(ev["k1b"][i], path.stream)
+    if split:
+        A.check(lib.tg_pipeline_stage_mask_fg(path.pipe.handle, F, path.d_cur, path.d_prev,
+                                              path.stream))
+        ctx.record(ev["k1b"][i], path.stream)
+        A.check(lib.tg_pipeline_stage_mask_cells(path.pipe.handle, F, path.stream))
+    else:
+        A.check(lib.tg_pipeline_stage_mask(path.pipe.handle, F, path.d_cur, path.d_prev,
+                                           path.stream))
+        ctx.record(ev["k1b"][i], path.stream)
+    ctx.record(ev["k1c"][i], path.stream)
     A.check(lib.tg_pipeline_stage_plan(path.pipe.handle, F, path.d_ids, path.d_gen, 0, path.stream))
     ctx.record(ev["pl"][i], path.stream)
 
@@ -59,7 +68,8 @@ ctx.synchronize()
 t = {k: [ctx.elapsed_ms(origin, e) for e in ev[k][:steps]] for k in names}
 for i in range(steps):
     print(f"pass {i}: K1 {t['k1a'][i]:8.2f}->{t['k1b'][i]:8.2f} ({t['k1b'][i]-t['k1a'][i]:5.2f}) "
-          f"plan ->{t['pl'][i]:8.2f} ({t['pl'][i]-t['k1b'][i]:4.2f}) fetch ->{t['fe'][i]:8.2f} "
+          f"K1b ->{t['k1c'][i]:8.2f} ({t['k1c'][i]-t['k1b'][i]:4.2f}) "
+          f"plan ->{t['pl'][i]:8.2f} ({t['pl'][i]-t['k1c'][i]:4.2f}) fetch ->{t['fe'][i]:8.2f} "
           f"K5 {t['g0'][i]:8.2f}->{t['g1'][i]:8.2f} ({t['g1'][i]-t['g0'][i]:5.2f})  host start "
           f"{host[i][0]:8.2f} wait+flatten {host[i][1]:5.2f} schedule {host[i][2]:5.2f}", flush=True)
 span = t["g1"][steps - 1] - t["k1a"][1]
