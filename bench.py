@@ -502,7 +502,7 @@ def measure_cfg2(args, rank, world, local, dist, ctx, secondary=False):
     k1_bytes = (n + 1) * FRAME_BYTES
     unique = k1_bytes + adm_bytes + ncanv * CANVAS_BYTES
     b_run = n * 2 * FRAME_BYTES + adm_bytes + ncanv * CANVAS_BYTES
-    rf = roofline("mask_fg_kernel (K1, K1b fused)", k1_bytes, k1, ncu_traffic("k1_traffic.json", n),
+    rf = roofline("mask_fg_kernel (K1, K1b fused)", k1_bytes, k1, ncu_traffic("k1_traffic.json", n + 1),
                   "frame bytes only: the 300 frames + the first frame's predecessor, each read "
                   "once (masks, cell grids, the raw-bitmap round trip not credited)")
     pth = path_record(unique, ms_step, b_run,

@@ -47,7 +47,11 @@ namespace tg {
 #define TG_GATHER_DYNAMIC 1
 #endif
 
-constexpr int kGatherThreads = 256;
+#ifndef TG_GATHER_THREADS
+#define TG_GATHER_THREADS 256
+#endif
+
+constexpr int kGatherThreads = TG_GATHER_THREADS;
 constexpr int kGatherWarps = kGatherThreads / 32;
 constexpr int kGatherBand = TG_GATHER_BAND;      // rows per unit
 constexpr int kGatherMaxJobs = 192;              // jobs of one canvas cached in smem

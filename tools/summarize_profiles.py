@@ -1,13 +1,13 @@
 """Turns gpurun_out/ ncu artifacts into the committed profiles/ summaries.
 
-    python tools/summarize_profiles.py r01
+    python tools/summarize_profiles.py <tag> <frame reads per step> <traffic json> [title]
 
-Reads gpurun_out/launches.csv (ncu --metrics gpu__time_duration.sum,
-dram__bytes_read.sum,dram__bytes_write.sum launch list of
-`bench.py --steps 2 --warmup 1`) and gpurun_out/prof_<kernel>.ncu-rep (one
---set full capture per hot kernel), writes profiles/<tag>_launches.csv,
-profiles/<tag>_summary.md and profiles/k1_traffic.json (read by bench.py for
-roofline.traffic).
+Reads gpurun_out/<tag>_launches.csv (ncu --metrics gpu__time_duration.sum,
+dram__bytes_read.sum,dram__bytes_write.sum launch list of a short bench run,
+tools/gpu/r02_profile.sh) and gpurun_out/<tag>_prof_<kernel>.ncu-rep (one
+--set full capture per hot kernel); writes profiles/<tag>_launches.csv,
+profiles/<tag>_summary.md and the K1 traffic record bench.py reads for
+roofline.traffic (DRAM bytes of one mask_fg launch per frame read).
 """
 from __future__ import annotations
 
@@ -23,12 +23,12 @@ from collections import defaultdict
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
-FRAMES = 300
 FRAME_BYTES = 3840 * 2160 * 3
+KERNELS = ("mask_fg", "dilate_cells", "plan_kernel", "gather_kernel")
 
 
-def launches():
-    rows = list(csv.reader(open(os.path.join(OUT, "launches.csv"))))
+def launches(path):
+    rows = list(csv.reader(open(path)))
     hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr]
     ki, mi, vi, ii = (h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"),
@@ -49,78 +49,86 @@ def details(rep):
     return {r[mi]: f"{r[vi]} {r[ui]}".strip() for r in rows[1:]}
 
 
-def stalls(rep):
+def raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    h, v = rows[0], rows[2]
+    return dict(zip(rows[0], rows[2]))
+
+
+def stalls(r):
     res = []
-    for i, name in enumerate(h):
+    for name, v in r.items():
         m = re.match(r"smsp__average_warps_issue_stalled_(.*)_per_issue_active\.ratio", name)
         if m:
             try:
-                res.append((float(v[i].replace(",", "")), m.group(1)))
+                res.append((float(v.replace(",", "")), m.group(1)))
             except ValueError:
                 pass
     return sorted(res, reverse=True)[:5]
 
 
-def main(tag):
+def main(tag, reads, traffic_json, title):
     os.makedirs(PROF, exist_ok=True)
-    shutil.copy(os.path.join(OUT, "launches.csv"), os.path.join(PROF, f"{tag}_launches.csv"))
-    d = launches()
-    # steady-state launches: skip the synthesis kernels and the first (warm-up) step
+    src = os.path.join(OUT, f"{tag}_launches.csv")
+    shutil.copy(src, os.path.join(PROF, f"{tag}_launches.csv"))
     per = defaultdict(list)
-    for (i, name), m in sorted(d.items()):
+    for (_, name), m in sorted(launches(src).items()):
         per[name].append(m)
-    lines = [f"# ncu summary {tag}", "",
-             "Source: `bash tools/profile.sh` under gpurun (ncu --clock-control none; launch list of "
-             "`bench.py --steps 2 --warmup 1`, 300 4K frames per launch). ncu times are serialized "
-             "cold-cache replays: compare shares, not absolutes.", "",
-             "| kernel | launches | mean ms | DRAM read GB | DRAM write GB | DRAM GB/s |",
+    lines = [f"# ncu summary {tag}", "", title, "",
+             "Launch list: `tools/gpu/r02_profile.sh` under gpurun (`ncu --metrics "
+             "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control "
+             "none`). ncu times are serialized cold-cache replays: compare shares, not absolutes.",
+             "", "| kernel | launches | mean ms | DRAM read GB | DRAM write GB | DRAM GB/s |",
              "|---|---|---|---|---|---|"]
     k1 = None
+    total = 0.0
     for name, ms in per.items():
         if name.startswith("synth"):
             continue
         t = sum(m["gpu__time_duration.sum"] for m in ms) / len(ms) / 1e6
         rd = sum(m["dram__bytes_read.sum"] for m in ms) / len(ms)
         wr = sum(m["dram__bytes_write.sum"] for m in ms) / len(ms)
+        total += t
         lines.append(f"| {name} | {len(ms)} | {t:.4f} | {rd/1e9:.3f} | {wr/1e9:.3f} | "
                      f"{(rd+wr)/t/1e6:.0f} |")
         if name.startswith("mask_fg_kernel"):
             k1 = dict(ms=t, read=rd, write=wr)
-    total = sum(sum(m["gpu__time_duration.sum"] for m in ms) / len(ms)
-                for n, ms in per.items() if not n.startswith("synth"))
-    lines += ["", f"Step total (sum of mean kernel times): {total/1e6:.4f} ms", ""]
-    for kern in ("mask_fg", "plan_kernel", "gather_kernel"):
-        rep = os.path.join(OUT, f"prof_{kern}.ncu-rep")
+    lines += ["", f"Sum of mean kernel times per step: {total:.4f} ms", ""]
+    if k1:
+        alg = reads * FRAME_BYTES
+        lines += [f"K1 (mask_fg_kernel): {alg/1e9:.2f} GB of frames per launch ({reads} frame "
+                  f"reads); DRAM traffic {(k1['read']+k1['write'])/1e9:.2f} GB = "
+                  f"{(k1['read']+k1['write'])/alg:.3f}x the algorithmic bytes.", ""]
+    for kern in KERNELS:
+        rep = os.path.join(OUT, f"{tag}_prof_{kern}.ncu-rep")
         if not os.path.exists(rep):
             continue
-        det = details(rep)
+        det, r = details(rep), raw(rep)
         lines.append(f"## {kern} (ncu --set full)")
         for key in ("Duration", "DRAM Throughput", "Memory Throughput", "L2 Hit Rate",
                     "Compute (SM) Throughput", "Issue Slots Busy", "Achieved Occupancy",
                     "Registers Per Thread", "Dynamic Shared Memory Per Block"):
             if key in det:
                 lines.append(f"- {key}: {det[key]}")
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            if key in r:
+                lines.append(f"- {key}: {r[key]}")
         lines.append("- top stall reasons (warps per issue): " +
-                     ", ".join(f"{n} {v:.2f}" for v, n in stalls(rep)))
+                     ", ".join(f"{n} {v:.2f}" for v, n in stalls(r)))
         lines.append("")
     with open(os.path.join(PROF, f"{tag}_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
-    if k1:
+    if k1 and traffic_json:
         traffic = k1["read"] + k1["write"]
-        raw = 2160 * 120 * 4
-        cells = 135 * (240 + 8) * 4
-        json.dump({"kernel": "mask_fg_kernel (K1, K1b fused)", "frames_per_launch": FRAMES,
-                   "dram_bytes_per_launch": traffic, "dram_bytes_per_frame": traffic / FRAMES,
-                   "algorithmic_bytes_per_launch":
-                       (FRAMES + 1) * FRAME_BYTES + FRAMES * (2 * raw + cells),
+        json.dump({"kernel": "mask_fg_kernel", "frame_reads_per_launch": reads,
+                   "dram_bytes_per_launch": traffic, "dram_bytes_per_frame": traffic / reads,
+                   "algorithmic_bytes_per_launch": reads * FRAME_BYTES,
                    "source": f"profiles/{tag}_launches.csv"},
-                  open(os.path.join(PROF, "k1_traffic.json"), "w"), indent=1)
+                  open(os.path.join(ROOT, traffic_json), "w"), indent=1)
     print("\n".join(lines))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
+    main(sys.argv[1], int(sys.argv[2]), sys.argv[3] if len(sys.argv) > 3 else "",
+         sys.argv[4] if len(sys.argv) > 4 else "")
