@@ -301,6 +301,10 @@ def run_multicam(args):
     ms_step = ms / K
     k1_ms = statistics.mean(ctx.elapsed_ms(a, b) for a, b in filter(None, mask_ev))
     value = n_cams_total * n * K / (ms / 1e3)
+    # K1 alone (after the timed region): inside the pipeline its launches
+    # start while the previous pass's gather still drains, so the in-pipeline
+    # duration includes that wait
+    k1_iso = k1_isolated(ctx, path)
 
     # bytes of this rank's pass
     F_local = len(cams) * n
@@ -333,10 +337,15 @@ def run_multicam(args):
                          "per GPU), no flush",
                    "pipelining": "host batcher of pass i overlaps device K1-K4 of pass i+1; K5 on "
                                  "its own stream; timed region = K whole passes"},
-        "roofline": roofline("mask_fg_kernel (K1), one launch per step", k1_bytes, k1_ms, traffic,
-                             "frame bytes only: each camera's 30 frames + its background read "
-                             "once (raw bitmap writes not credited); peak = the measured copy "
-                             "rate (read + write), which a read-dominated stream can exceed"),
+        "roofline": dict(roofline("mask_fg_kernel (K1), one launch per step", k1_bytes, k1_ms,
+                                  traffic,
+                                  "frame bytes only: each camera's 30 frames + its background "
+                                  "read once (raw bitmap writes not credited); peak = the "
+                                  "measured copy rate (read + write), which a read-dominated "
+                                  "stream can exceed; launch_ms = in the pipeline (includes "
+                                  "waiting for the previous pass's gather to leave the SMs)"),
+                         launch_ms_isolated=round(k1_iso, 4),
+                         frac_isolated=round(k1_bytes / (k1_iso / 1e3) / 1e9 / peaks()[0], 4)),
         "path": path_record(unique, ms_step, b_run, {"k1": round(k1_ms, 4)},
                             {"events": path._nev, "canvases": n_canv,
                              "patches_admitted": int(len(pats)),
@@ -364,6 +373,22 @@ def run_multicam(args):
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def k1_isolated(ctx, path, reps=3):
+    """Mean duration of K1 (the shard's mask stream) launched alone."""
+    from paper_2404_09267_b200 import _native as N
+    from paper_2404_09267_b200 import api as A
+    F = len(path.cameras) * path.n
+    ctx.stream_sync(path.stream)
+    ev = [(ctx.event(), ctx.event()) for _ in range(reps)]
+    for a, b in ev:
+        ctx.record(a, path.stream)
+        A.check(N.lib().tg_pipeline_stage_mask_fg(path.pipe.handle, F, path.d_cur, path.d_prev,
+                                                  path.stream))
+        ctx.record(b, path.stream)
+    ctx.stream_sync(path.stream)
+    return statistics.mean(ctx.elapsed_ms(a, b) for a, b in ev)
 
 
 def e2e_multicam(ctx, path, args, dist, local, n_cams_total):

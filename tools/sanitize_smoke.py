@@ -40,7 +40,20 @@ _, n_ev, n_canv = path.step()
 ctx.synchronize()
 print("batcher", n_ev, "events", n_canv, "canvases")
 path.close()
+comm = A.Comm.nccl(ctx, A.Comm.unique_id(), 0, 1)  # device descriptor all-gather
+path = MC.MultiCameraPath(ctx, [0, 1], 640, 368, 4, [(1, 60.0, 3.0), (2, 85.0, 4.0)],
+                          bandwidth_mbps=40.0, trace_kw=dict(roi_max_dim=200), comm=comm)
+print("nccl pass", path.run_pipelined(2), "canvases")
+path.close()
+comm.close()
 q = [A.PatchMeta(i, 0, A.Rect(0, 0, 30 + 7 * i, 20 + 5 * i), 0, 1, 1, 1) for i in range(12)]
 res = A.stitch_all(q, A.CanvasSpec(128, 128), ctx=ctx)
 print("stitch", res.canvas_count(), "canvases")
+q = [A.PatchMeta(i, 0, A.Rect(0, 0, 20 + i % 50, 10 + i % 30), 0, 1, 1, 1) for i in range(300)]
+res = A.stitch_all(q, A.CanvasSpec(100, 100), ctx=ctx)  # longer than the staged queue
+print("stitch long", res.canvas_count(), "canvases")
+z = A.make_zones(A.FrameSpec(0, 640, 360), A.PartitionConfig(4, 4))
+print("partition", len(A.partition(A.FrameSpec(0, 640, 360), A.PartitionConfig(4, 4),
+                                    [A.Rect(10, 10, 100, 50), A.Rect(300, 200, 40, 40)], 1.5,
+                                    ctx=ctx)), "patches", len(z), "zones")
 ctx.close()
