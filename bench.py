@@ -277,6 +277,8 @@ def run_multicam(args):
     comm = make_comm(A, ctx, dist, rank, world)
     per_rank = max(len(MC.shard_cameras(n_cams_total, world, r)) for r in range(world))
     kw = dict(trace_kw=dict(TRACE), **SIM)
+    if os.environ.get("TG_BENCH_GATHER_GRID"):  # tuning probes only
+        kw["gather_grid"] = int(os.environ["TG_BENCH_GATHER_GRID"])
     glob = args.global_batching and dist is not None
     if glob:
         path = MC.GlobalCameraPath(ctx, n_cams_total, comm, W, H, n, SIM_PROFILE, **kw)

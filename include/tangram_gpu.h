@@ -114,11 +114,12 @@ void tg_ctx_destroy(tg_ctx* ctx);
 void* tg_ctx_stream(tg_ctx* ctx);
 tg_status tg_ctx_synchronize(tg_ctx* ctx); /* waits; reports latched device errors */
 tg_status tg_device_sm_count(tg_ctx* ctx, int32_t* sms);
-/* Context options.  TG_OPT_GATHER_CTAS_PER_SM caps the resident CTAs per SM
- * of the explicit-plan canvas gathers (tg_stitch_gather, tg_batcher_gather*;
- * 0 = occupancy limit): at 2 the next pass's K1b and planner co-run with the
- * event gather of configs 3/4 instead of queueing behind it. */
-typedef enum { TG_OPT_GATHER_CTAS_PER_SM = 1 } tg_option;
+/* Context options.  TG_OPT_GATHER_GRID sets the CTAs of the explicit-plan
+ * canvas gathers' persistent grid (tg_stitch_gather, tg_batcher_gather*;
+ * 0 = SMs x the occupancy limit): below that, the next pass's K1b and
+ * planner CTAs co-run with the event gather of configs 3/4 instead of
+ * queueing behind it. */
+typedef enum { TG_OPT_GATHER_GRID = 1 } tg_option;
 tg_status tg_ctx_set_option(tg_ctx* ctx, int32_t option, int64_t value);
 
 /* ---- memory / streams / events (plumbing for callers without a CUDA

@@ -71,7 +71,7 @@ struct tg_ctx {
   int32_t* g_units = nullptr;
   int32_t g_units_h[3] = {0, 0, 0};
   size_t g_job_cap = 0, g_range_cap = 0;
-  int32_t gather_ctas_per_sm = 0;  // TG_OPT_GATHER_CTAS_PER_SM (0: occupancy limit)
+  int32_t gather_grid = 0;  // TG_OPT_GATHER_GRID (0: SMs x the occupancy limit)
 };
 
 struct tg_pipeline {
@@ -278,7 +278,7 @@ tg_status tg_internal_run_gather(tg_ctx* ctx, const void* jobs, int32_t n_jobs, 
   g.ranges = ctx->g_ranges;
   g.units = ctx->g_units;
   g.out = d_out;
-  TG_CUDA(launch_gather(g, ctx->sms, ctx->gather_ctas_per_sm, st));
+  TG_CUDA(launch_gather(g, ctx->sms, ctx->gather_grid, st));
   return TG_OK;
 }
 
@@ -337,9 +337,9 @@ tg_status tg_ctx_synchronize(tg_ctx* ctx) {
 tg_status tg_ctx_set_option(tg_ctx* ctx, int32_t option, int64_t value) {
   if (!ctx) return fail(TG_ERR_INVALID_ARGUMENT, "null context");
   switch (option) {
-    case TG_OPT_GATHER_CTAS_PER_SM:
-      if (value < 0 || value > 32) return fail(TG_ERR_INVALID_ARGUMENT, "CTAs per SM must be in [0, 32]");
-      ctx->gather_ctas_per_sm = static_cast<int32_t>(value);
+    case TG_OPT_GATHER_GRID:
+      if (value < 0 || value > (1 << 20)) return fail(TG_ERR_INVALID_ARGUMENT, "gather grid out of range");
+      ctx->gather_grid = static_cast<int32_t>(value);
       return TG_OK;
     default:
       return fail(TG_ERR_INVALID_ARGUMENT, "unknown context option %d", option);

@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(kGatherThreads, TG_GATHER_MIN_BLOCKS) gather_k
 #endif
 }
 
-cudaError_t launch_gather(const GatherArgs& a, int sms, int max_ctas_per_sm, cudaStream_t stream) {
+cudaError_t launch_gather(const GatherArgs& a, int sms, int grid_ctas, cudaStream_t stream) {
   // resident CTAs per SM, per device (0 = not yet queried)
   static std::atomic<int> blocks_per_sm[kMaxDevices] = {};
   int dev = 0;
@@ -484,8 +484,8 @@ cudaError_t launch_gather(const GatherArgs& a, int sms, int max_ctas_per_sm, cud
     nb = nb > 0 ? nb : 1;
     if (dev >= 0 && dev < kMaxDevices) blocks_per_sm[dev].store(nb, std::memory_order_relaxed);
   }
-  if (max_ctas_per_sm > 0) nb = std::min(nb, max_ctas_per_sm);
-  gather_kernel<<<sms * nb, kGatherThreads, kGatherSmem, stream>>>(a);
+  const int grid = grid_ctas > 0 ? std::min(grid_ctas, sms * nb) : sms * nb;
+  gather_kernel<<<grid, kGatherThreads, kGatherSmem, stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -107,8 +107,8 @@ struct GatherArgs {
                           // counters (0 at launch; the last CTA resets them)
   uint8_t* out;
 };
-// max_ctas_per_sm: 0 = the occupancy limit (persistent grid of sms x that)
-cudaError_t launch_gather(const GatherArgs& a, int sms, int max_ctas_per_sm, cudaStream_t stream);
+// grid_ctas: 0 = the persistent grid of sms x the occupancy limit
+cudaError_t launch_gather(const GatherArgs& a, int sms, int grid_ctas, cudaStream_t stream);
 int gather_bands(int N);
 
 // ---- synthetic frames (k_synth.cu) -----------------------------------------

@@ -98,7 +98,7 @@ class MultiCameraPath:
     def __init__(self, ctx: Context, cameras, width, height, n_frames, profile, bandwidth_mbps=80.0,
                  gpu_memory_gb=6.0, model_size_gb=2.0, canvas=(1024, 1024), zones=(4, 4),
                  slo_us=1_000_000, fps=30.0, per_camera_link=True, trace_kw=None,
-                 canvas_capacity=None, comm=None, cameras_per_rank=None):
+                 canvas_capacity=None, comm=None, cameras_per_rank=None, gather_grid=None):
         """`comm` (api.Comm, optional): every pass all-gathers the ranks'
         descriptor blocks through it; blocks hold `cameras_per_rank` (the
         largest shard; equal on every rank) x n_frames x zones records."""
@@ -144,7 +144,11 @@ class MultiCameraPath:
         self.canvas_bytes = canvas[0] * canvas[1] * 3
         self.canvas_cap = canvas_capacity
         self.d_canvases = None
-        check(N.lib().tg_ctx_set_option(ctx.handle, N.TG_OPT_GATHER_CTAS_PER_SM, 2))
+        # the event gather's persistent grid (default 2 CTAs per SM) leaves room
+        # for the next pass's K1b and planner CTAs
+        check(N.lib().tg_ctx_set_option(ctx.handle, N.TG_OPT_GATHER_GRID,
+                                        gather_grid if gather_grid is not None
+                                        else 2 * ctx.sm_count()))
         # the planner's dense descriptor block (device), gathered per pass
         self.world = comm.world if comm is not None else 1
         self.cap = max(1, (cameras_per_rank or len(self.cameras))) * n_frames * self.zones
