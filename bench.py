@@ -775,6 +775,8 @@ def run_density(args):
             keep = (k1_bytes, k1_ms, unique, ms_step, F)
             if not args.no_cpu:
                 cpu = cpu_baseline_cfg2(rings[0], ts[0], n)
+            if not args.no_e2e:
+                e2e = e2e_density(ctx, pipe, rings, F, tabs, d_canv, max(1, args.e2e_steps))
         pipe.close()
         for r in rings:
             r.close()
@@ -800,8 +802,51 @@ def run_density(args):
            "gpu_launches": 3 * args.steps, "sweep": lines}
     if not args.no_cpu and keep:
         out["cpu_baseline"] = cpu
+    if not args.no_e2e and keep:
+        out["e2e"] = e2e
     print(json.dumps(out), flush=True)
     ctx.close()
+
+
+def e2e_density(ctx, pipe, rings, F, tabs, d_canv, steps):
+    """Config 5's e2e at one density: every camera ring copied in from pinned
+    host memory, then the per-frame pipeline run; patch and placement
+    descriptors read back."""
+    from paper_2404_09267_b200 import api as A
+    host = [ctx.malloc_host(r.frame_bytes * (r.n + 1)) for r in rings]
+    for h, r in zip(host, rings):
+        ctx.memcpy(h, r.base, r.frame_bytes * (r.n + 1), 1)
+    ctx.stream_sync()
+    h2d = sum(r.frame_bytes * (r.n + 1) for r in rings)
+    Z = pipe.zones
+    hdesc = ctx.malloc_host(F * Z * 96 + F * 8)
+    v = pipe.views
+    d_cur, d_prev, d_ids, d_gen = tabs
+
+    def one():
+        for h, r in zip(host, rings):
+            ctx.memcpy(r.base, h, r.frame_bytes * (r.n + 1), 0)
+        pipe.run(F, d_cur, d_prev, d_ids, d_gen, 0, d_canv)
+        ctx.memcpy(hdesc, v.placements, F * Z * 32, 1)
+        ctx.memcpy(hdesc + F * Z * 32, v.patches, F * Z * 64, 1)
+        ctx.memcpy(hdesc + F * Z * 96, v.n_placements, F * 4, 1)
+        ctx.memcpy(hdesc + F * Z * 96 + F * 4, v.n_patches, F * 4, 1)
+
+    one()
+    ctx.stream_sync()
+    e0, e1 = ctx.event(), ctx.event()
+    ctx.record(e0)
+    for _ in range(steps):
+        one()
+    ctx.record(e1)
+    ctx.stream_sync()
+    ms = ctx.elapsed_ms(e0, e1)
+    for h in host + [hdesc]:
+        ctx.free_host(h)
+    return {"value": round(F * steps / (ms / 1e3), 1), "unit": "frames/s", "density": 0.10,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": F * Z * 96 + F * 8, "steps": steps,
+            "note": "pinned host frames of the 8 cameras -> device rings, then the per-frame "
+                    "pipeline run through the public API; PCIe-bound"}
 
 
 # ============================================================= reference

@@ -165,3 +165,45 @@ def test_nccl_single_rank_comm_matches_local_path(ctx):
     assert np.array_equal(path.canvases(nc), want)
     path.close()
     comm.close()
+
+
+def test_descriptor_output_capacity_and_detach(ctx):
+    """A run with more patches than the attached block holds latches
+    TG_ERR_CAPACITY (the block keeps cap records); detaching stops the
+    output; the camera table maps frames to (camera, frame)."""
+    from paper_2404_09267_b200 import _native as N
+    from tests._helpers import GpuRun
+    run = GpuRun(ctx, 1920, 1080, 6, seed=11, keep_mask=False,
+                 trace_kw=dict(roi_proportion_mean=0.3))
+    run.run()
+    total = int(run.res["n_patches"].sum())
+    assert total > 4
+    cap = total - 3
+    blk = ctx.malloc(MC.block_bytes(cap))
+    cams = ctx.malloc(8)
+    ctx.upload(cams, np.array([5, 9], np.int32))
+    run.pipe.set_descriptor_output(blk, cap, cams, 3)  # frames 0-2: camera 5, 3-5: camera 9
+    with pytest.raises(A.CapacityError, match="descriptor capacity exceeded"):
+        run.run()
+    got = ctx.download(blk, (MC.block_bytes(cap),), np.uint8)
+    recs = MC.flatten_blocks(got.ctypes.data, 1, cap)
+    assert len(recs) == cap
+    assert list(recs["patch"]["patch_id"]) == list(range(cap))
+    n0 = int(run.res["n_patches"][:3].sum())
+    assert set(recs["camera"][:n0]) <= {5} and set(recs["camera"][n0:]) <= {9}
+    assert list(recs["frame"][:n0]) == sorted(recs["frame"][:n0])
+    run.pipe.set_descriptor_output(blk, total, cams, 3)
+    run.run()
+    recs = MC.flatten_blocks(ctx.download(blk, (MC.block_bytes(total),), np.uint8).ctypes.data,
+                             1, total)
+    assert len(recs) == total
+    ctx.memset(blk, 0, MC.block_bytes(cap))
+    run.pipe.set_descriptor_output(None)
+    run.run()  # detached: the block is not written
+    assert not ctx.download(blk, (MC.block_bytes(cap),), np.uint8).any()
+    with pytest.raises(A.InvalidArgument):
+        run.pipe.set_descriptor_output(blk + 4, 8)
+    for p in (blk, cams):
+        ctx.free(p)
+    run.close()
+    del N
