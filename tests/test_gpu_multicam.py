@@ -179,7 +179,7 @@ def test_descriptor_output_capacity_and_detach(ctx):
     total = int(run.res["n_patches"].sum())
     assert total > 4
     cap = total - 3
-    blk = ctx.malloc(MC.block_bytes(cap))
+    blk = ctx.malloc(MC.block_bytes(total))
     cams = ctx.malloc(8)
     ctx.upload(cams, np.array([5, 9], np.int32))
     run.pipe.set_descriptor_output(blk, cap, cams, 3)  # frames 0-2: camera 5, 3-5: camera 9
