@@ -194,8 +194,8 @@ def test_descriptor_output_capacity_and_detach(ctx):
     assert list(recs["frame"][:n0]) == sorted(recs["frame"][:n0])
     run.pipe.set_descriptor_output(blk, total, cams, 3)
     run.run()
-    recs = MC.flatten_blocks(ctx.download(blk, (MC.block_bytes(total),), np.uint8).ctypes.data,
-                             1, total)
+    got = ctx.download(blk, (MC.block_bytes(total),), np.uint8)  # kept alive while read
+    recs = MC.flatten_blocks(got.ctypes.data, 1, total)
     assert len(recs) == total
     ctx.memset(blk, 0, MC.block_bytes(cap))
     run.pipe.set_descriptor_output(None)
