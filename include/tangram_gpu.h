@@ -270,7 +270,6 @@ tg_status tg_pipeline_device_views(tg_pipeline* p, tg_pipeline_views* out);
 typedef struct {
   int64_t mask_fused_launches;
   int64_t mask_split_launches;
-  int64_t mask_band_launches;  /* one-pass band kernel (no raw bitmap) */
 } tg_pipeline_stats;
 tg_status tg_pipeline_get_stats(tg_pipeline* p, tg_pipeline_stats* out);
 

@@ -73,8 +73,7 @@ class tg_pipeline_views(C.Structure):
 
 
 class tg_pipeline_stats(C.Structure):
-    _fields_ = [("mask_fused_launches", C.c_int64), ("mask_split_launches", C.c_int64),
-                ("mask_band_launches", C.c_int64)]
+    _fields_ = [("mask_fused_launches", C.c_int64), ("mask_split_launches", C.c_int64)]
 
 
 class tg_workload_config(C.Structure):

@@ -684,8 +684,7 @@ class Pipeline:
         s = N.tg_pipeline_stats()
         check(N.lib().tg_pipeline_get_stats(self.handle, C.byref(s)))
         return {"mask_fused_launches": s.mask_fused_launches,
-                "mask_split_launches": s.mask_split_launches,
-                "mask_band_launches": s.mask_band_launches}
+                "mask_split_launches": s.mask_split_launches}
 
     def free_rects(self, frame: int):
         cap = 3 * self.zones + 4

@@ -80,7 +80,6 @@ struct tg_pipeline {
   int zones = 0, cells_x = 0, cells_y = 0, act_words = 0, mask_words = 0, job_cap = 0, nbands = 0;
   uint32_t *raw = nullptr, *cells = nullptr, *active = nullptr, *mask = nullptr;
   uint32_t* mask_sync = nullptr;  // fused K1/K1b launch: item counters + task queue
-  uint32_t* edges = nullptr;      // band kernel: the bands' published edge rows
   int32_t *n_rois = nullptr, *n_patches = nullptr, *n_placements = nullptr, *n_canvases = nullptr;
   tg_rect* rois = nullptr;
   tg_patch_meta* patches = nullptr;
@@ -746,7 +745,7 @@ tg_status tg_pipeline_params_default(int32_t width, int32_t height, tg_pipeline_
 void tg_pipeline_destroy(tg_pipeline* p) {
   if (!p) return;
   cudaSetDevice(p->ctx->device);
-  void* bufs[] = {p->raw, p->edges, p->mask_sync, p->cells, p->mask, p->n_rois, p->n_patches, p->n_placements,
+  void* bufs[] = {p->raw, p->mask_sync, p->cells, p->mask, p->n_rois, p->n_patches, p->n_placements,
                   p->n_canvases, p->rois, p->patches, p->admitted, p->placements,
                   p->canvas_base, p->jobs, p->canvas_jobs, p->ranges, p->gather_units,
                   p->id_state, p->look, p->psync};
@@ -804,7 +803,6 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
   const size_t sync_words = mask_sync_words(q.height, ctx->sms);
   if (!e) e = alloc(&p->mask_sync, sync_words + F * cy * p->act_words);
   if (!e) p->active = p->mask_sync + sync_words;
-  if (!e) e = alloc(&p->edges, band_edge_words(q.dilate_radius, ctx->sms));
   if (!e) e = alloc(&p->cells, F * cx * cy);
   if (!e && q.keep_mask) e = alloc(&p->mask, F * q.height * p->mask_words);
   if (!e) e = alloc(&p->n_rois, F);
@@ -868,26 +866,8 @@ tg_status tg_pipeline_stage_mask(tg_pipeline* p, int32_t n_frames, const uint8_t
     return fail(TG_ERR_INVALID_ARGUMENT, "n_frames must be in [0, max_frames]");
   if (n_frames > 0 && (!d_cur || !d_prev))
     return fail(TG_ERR_INVALID_ARGUMENT, "null frame pointer table");
-  // The band kernel (one pass, no raw bitmap) when every band fits on its own
-  // SM; else K1 + K1b in one cooperative launch; separate launches if the
-  // device cannot co-schedule one K1 CTA per SM (e.g. a shared GPU).
-  // TG_MASK_BAND=0 skips the band kernel (A/B probes).
-  static EnvInt env_band{"TG_MASK_BAND"};
-  if (env_band.get() != 0 && band_supported(p->p.width, p->p.height, p->ctx->sms)) {
-    const cudaError_t eb = launch_mask_band(
-        d_cur, d_prev, n_frames, p->p.width, p->p.height, p->p.pitch, p->p.threshold,
-        p->p.dilate_radius, p->cells, p->active, p->p.keep_mask ? p->mask : nullptr,
-        p->mask_sync, mask_sync_words(p->p.height, p->ctx->sms), p->edges, p->ctx->sms,
-        pick(p->ctx, stream));
-    if (eb == cudaSuccess) {
-      p->last_frames = n_frames;
-      if (n_frames > 0) ++p->stats.mask_band_launches;
-      return TG_OK;
-    }
-    if (eb != cudaErrorCooperativeLaunchTooLarge && eb != cudaErrorNotSupported)
-      return cuda_fail(eb, "launch_mask_band");
-    cudaGetLastError();
-  }
+  // K1 + K1b in one cooperative launch; separate launches if the device
+  // cannot co-schedule one K1 CTA per SM (e.g. a shared GPU).
   const cudaError_t e = launch_mask_fused(
       d_cur, d_prev, n_frames, p->p.width, p->p.height, p->p.pitch, p->p.threshold,
       p->p.dilate_radius, p->raw, p->cells, p->active, p->p.keep_mask ? p->mask : nullptr,

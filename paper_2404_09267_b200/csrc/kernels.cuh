@@ -21,18 +21,6 @@ cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const*
                               uint32_t* d_raw, uint32_t* d_cells, uint32_t* d_active,
                               uint32_t* d_mask, uint32_t* d_sync, int sms, cudaStream_t stream);
 
-// K1 band kernel (k_band.cu): mask + dilation + cells in one pass, no raw
-// bitmap.  Needs ceil(H / 16) <= sms (every band's CTA co-resident);
-// d_flags: flag_words u32 (>= sms) zeroed per launch -- when d_active follows
-// it directly one memset clears both; d_edges: band_edge_words(radius, sms).
-bool band_supported(int W, int H, int sms);
-size_t band_edge_words(int radius, int sms);
-cudaError_t launch_mask_band(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
-                             int n_frames, int W, int H, int pitch, int threshold, int radius,
-                             uint32_t* d_cells, uint32_t* d_active, uint32_t* d_mask,
-                             uint32_t* d_flags, size_t flag_words, uint32_t* d_edges, int sms,
-                             cudaStream_t stream);
-
 // ---- K2-K4 per-frame planner + frame-order prefix (k_plan.cu) --------------
 struct PlanArgs {
   int n_frames, W, H, X, Y, M, N;

@@ -53,7 +53,7 @@ def test_bench_cfg2_line():
     assert REQUIRED <= set(d)
     _check_roofline(d["roofline"])
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] == 12
-    assert d["mask_path"]["mask_band_launches"] > 0  # 4K: the one-pass band kernel
+    assert d["mask_path"]["mask_fused_launches"] > 0
 
 
 def test_bench_reference_arm_line():
