@@ -225,9 +225,27 @@ __device__ __forceinline__ uint32_t gt_bytes(uint32_t d, uint32_t t1) {
 
 // 4 pixels (12 bytes) of cur/prev -> 4 foreground bits (max_c |cur-prev| > T
 // <=> some channel's |cur-prev| > T).
+// TG_FG_MAX3=0 builds the round-1 planar-regroup form (per-byte threshold,
+// 6 PRMT + 2 LOP3 to OR each pixel's channels): 3 % slower K1.
+#ifndef TG_FG_MAX3
+#define TG_FG_MAX3 1
+#endif
 template <bool kLow>
 __device__ __forceinline__ uint32_t fg4(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t b0,
                                         uint32_t b1, uint32_t b2, uint32_t t1) {
+#if TG_FG_MAX3
+  // |cur - prev| per byte, then each pixel's three channel differences into
+  // the high bytes of 16-bit lanes (two pixels per word, one word per
+  // channel; the low bytes only break ties) and one VIMNMX3.U16x2 per two
+  // pixels: the 4 pixels' max difference, thresholded once.
+  const uint32_t d0 = __vabsdiffu4(a0, b0), d1 = __vabsdiffu4(a1, b1), d2 = __vabsdiffu4(a2, b2);
+  const uint32_t m01 = __vimax3_u16x2(__byte_perm(d0, d0, 0x3000), __byte_perm(d0, d1, 0x4010),
+                                      __byte_perm(d0, d1, 0x5020));
+  const uint32_t m23 = __vimax3_u16x2(__byte_perm(d1, d2, 0x5020), __byte_perm(d1, d2, 0x6030),
+                                      __byte_perm(d1, d2, 0x7040));
+  const uint32_t m = __byte_perm(m01, m23, 0x7531);
+  return ((gt_bytes<kLow>(m, t1) & 0x80808080u) * 0x00204081u) >> 28;
+#endif
   const uint32_t g0 = gt_bytes<kLow>(__vabsdiffu4(a0, b0), t1);
   const uint32_t g1 = gt_bytes<kLow>(__vabsdiffu4(a1, b1), t1);
   const uint32_t g2 = gt_bytes<kLow>(__vabsdiffu4(a2, b2), t1);
