@@ -391,6 +391,10 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
   uint8_t* slots = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(NS) * a.slot_bytes);
   uint64_t* empty = full + NS;
+  // frame whose diff a slot's row completes (-1: a chain start), written by
+  // the producer before it arms the slot: consumers never read the pointer
+  // tables
+  int* slot_f = reinterpret_cast<int*>(empty + NS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = a.rows_per_item * a.nparts;
   if (threadIdx.x == 0) {
@@ -438,6 +442,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
           if (!(used & bit) || mbar_test_wait(&empty[slot], (fills & bit) ? 0u : 1u)) {
             int out;
             const uint8_t* src = ch.next(a, &out) + off;
+            slot_f[slot] = out;
             mbar_arrive_expect_tx(&full[slot], bytes);
             bulk_g2s(slots + static_cast<size_t>(slot) * a.slot_bytes, src, bytes, &full[slot]);
             used |= bit;
@@ -471,25 +476,31 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
     const bool valid = col < a.part_words && w < a.nwords;
     uint32_t* out = a.raw + static_cast<size_t>(row) * a.nwords + w;
     const size_t fstride = static_cast<size_t>(a.H) * a.nwords;
-    Chain ch{it.f0, it.fend, true};
-    uint4 P[6] = {}, C[6] = {};
-    while (!ch.done()) {
-      int f;
-      ch.next(a, &f);
+    const uint32_t keep = w == a.nwords - 1 ? lastmask : 0xffffffffu;
+    // One stage: the next row of the chain into `cur`, diffed against `prv`
+    // (the previous stage's row) unless it starts the chain.  The item ends
+    // with frame fend-1 (a chain start never comes last); the two register
+    // sets alternate, so rows never move between registers.
+    auto stage = [&](uint4 (&cur)[6], const uint4 (&prv)[6]) -> int {
       const int slot = g * S + k;
       mbar_wait_sleep(&full[slot], (fpar >> k) & 1u);
       fpar ^= 1u << k;
-      if (in_slot) load96(C, slots + static_cast<size_t>(slot) * a.slot_bytes + 96 * col);
+      const int f = slot_f[slot];
+      if (in_slot) load96(cur, slots + static_cast<size_t>(slot) * a.slot_bytes + 96 * col);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
       if (++k == S) k = 0;
       if (f >= 0) {
-        uint32_t fw = fg_word<kLow>(C, P, t1);
-        if (w == a.nwords - 1) fw &= lastmask;
+        const uint32_t fw = fg_word<kLow>(cur, prv, t1) & keep;
         if (valid) out[static_cast<size_t>(f) * fstride] = fw;
       }
-#pragma unroll
-      for (int q = 0; q < 6; ++q) P[q] = C[q];
+      return f;
+    };
+    const int flast = it.fend - 1;
+    uint4 A[6], B[6];
+    for (;;) {
+      if (stage(A, B) == flast) break;
+      if (stage(B, A) == flast) break;
     }
     if (fused) {  // publish: this warp's raw words of the item are written
       __threadfence();
@@ -547,7 +558,8 @@ static cudaError_t plan_k1(MaskArgs& a, const uint8_t* const* d_cur, const uint8
   a.rows_per_item = kK1Groups / a.nparts;
   a.nrb = ceil_div(H, a.rows_per_item);
   a.slot_bytes = (a.part_words * 96 + 127) & ~127;
-  a.nslots = std::min(kK1MaxSlots, (kK1SmemBudget - 1024) / (kK1Groups * (a.slot_bytes + 16)));
+  // per slot: the row, full + empty barriers, the stage's frame
+  a.nslots = std::min(kK1MaxSlots, (kK1SmemBudget - 64) / (kK1Groups * (a.slot_bytes + 20)));
   a.nslots = std::max(2, std::min(a.nslots, env_or(g_env_slots, a.nslots)));
   // frame runs: enough items to balance the SMs
   int ntg = std::max(1, std::min(n_frames, ceil_div(8 * sms, a.nrb)));
@@ -556,7 +568,7 @@ static cudaError_t plan_k1(MaskArgs& a, const uint8_t* const* d_cur, const uint8
   a.ntg = ceil_div(n_frames, a.kf);
   a.total_items = a.ntg * a.nrb;
   a.raw = d_raw;
-  *smem = static_cast<size_t>(kK1Groups) * a.nslots * (a.slot_bytes + 16);
+  *smem = static_cast<size_t>(kK1Groups) * a.nslots * (a.slot_bytes + 20);
   if (*smem > static_cast<size_t>(kK1SmemBudget)) return cudaErrorInvalidConfiguration;
   const bool low = threshold <= 127;
   return low ? g_k1_smem[1].ensure(mask_fg_kernel<true>, static_cast<int>(*smem))
