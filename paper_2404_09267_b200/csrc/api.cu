@@ -798,7 +798,10 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
     return cudaMalloc(reinterpret_cast<void**>(ptr), std::max<size_t>(1, count) * sizeof(**ptr));
   };
   cudaError_t e = cudaSuccess;
-  if (!e) e = alloc(&p->raw, F * q.height * p->mask_words);
+  // F raw frames + one zero frame (K1b's rows for columns outside the frame)
+  if (!e) e = alloc(&p->raw, (F + 1) * q.height * p->mask_words);
+  if (!e) e = cudaMemset(p->raw + F * q.height * p->mask_words, 0,
+                         q.height * p->mask_words * sizeof(uint32_t));
   // K1 counters followed by the activity bits (p->active): one memset per launch
   const size_t sync_words = mask_sync_words(q.height, ctx->sms);
   if (!e) e = alloc(&p->mask_sync, sync_words + F * cy * p->act_words);
@@ -833,6 +836,10 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
   return TG_OK;
 }
 
+static const uint32_t* raw_zero(const tg_pipeline* p) {
+  return p->raw + static_cast<size_t>(p->p.max_frames) * p->p.height * p->mask_words;
+}
+
 tg_status tg_pipeline_stage_mask_fg(tg_pipeline* p, int32_t n_frames, const uint8_t* const* d_cur,
                                     const uint8_t* const* d_prev, void* stream) {
   tg_status s = use_device(p->ctx);
@@ -851,7 +858,8 @@ tg_status tg_pipeline_stage_mask_cells(tg_pipeline* p, int32_t n_frames, void* s
   if (s) return s;
   if (n_frames < 0 || n_frames > p->p.max_frames)
     return fail(TG_ERR_INVALID_ARGUMENT, "n_frames must be in [0, max_frames]");
-  TG_CUDA(launch_dilate_cells(p->raw, n_frames, p->p.width, p->p.height, p->p.dilate_radius,
+  TG_CUDA(launch_dilate_cells(p->raw, raw_zero(p), n_frames, p->p.width, p->p.height,
+                              p->p.dilate_radius,
                               p->cells, p->active, p->p.keep_mask ? p->mask : nullptr,
                               pick(p->ctx, stream)));
   p->last_frames = n_frames;
@@ -870,7 +878,8 @@ tg_status tg_pipeline_stage_mask(tg_pipeline* p, int32_t n_frames, const uint8_t
   // cannot co-schedule one K1 CTA per SM (e.g. a shared GPU).
   const cudaError_t e = launch_mask_fused(
       d_cur, d_prev, n_frames, p->p.width, p->p.height, p->p.pitch, p->p.threshold,
-      p->p.dilate_radius, p->raw, p->cells, p->active, p->p.keep_mask ? p->mask : nullptr,
+      p->p.dilate_radius, p->raw, raw_zero(p), p->cells, p->active,
+      p->p.keep_mask ? p->mask : nullptr,
       p->mask_sync, p->ctx->sms, pick(p->ctx, stream));
   if (e == cudaSuccess) {
     p->last_frames = n_frames;

@@ -70,6 +70,7 @@ constexpr int kK1MaxActWords = 16;      // K1b: act words per cell row (W <= 819
 // ---- K1b: dilation + cell summaries ---------------------------------------
 struct DilateArgs {
   const uint32_t* raw;
+  const uint32_t* zero;  // H * nwords zero words: the rows of columns outside the frame
   int H, W, nwords, cells_x, cells_y, act_words;
   uint32_t* cells;
   uint32_t* active;
@@ -83,12 +84,42 @@ __device__ __forceinline__ uint32_t pack_cell(int occ, uint32_t cols, uint32_t r
   return static_cast<uint32_t>(occ) | x0 << 9 | x1 << 13 | y0 << 17 | y1 << 21;
 }
 
+// One band's 16 output rows from the raw window: vertical OR over 2R+1 rows,
+// horizontal OR with the neighbour lanes' words, per-cell popcounts, column
+// and row masks.  kFull: all 16 rows inside the frame; kMask: also store the
+// dilated mask.
+template <int R, bool kFull, bool kMask>
+__device__ __forceinline__ void dilate_band(const DilateArgs& a, const uint32_t (&win)[kCell + 2 * R],
+                                            uint32_t keep, int nrow, uint32_t* mrow, int& occ,
+                                            int& occ_hi, uint32_t& cols, uint32_t& row_lo,
+                                            uint32_t& row_hi) {
+#pragma unroll
+  for (int ly = 0; ly < kCell; ++ly) {
+    uint32_t v = win[ly];
+#pragma unroll
+    for (int k = 1; k <= 2 * R; ++k) v |= win[ly + k];
+    const uint32_t vm = __shfl_up_sync(0xffffffffu, v, 1);
+    const uint32_t vp = __shfl_down_sync(0xffffffffu, v, 1);
+    uint32_t d = v;
+#pragma unroll
+    for (int k = 1; k <= R; ++k) d |= __funnelshift_r(v, vp, k) | __funnelshift_l(vm, v, k);
+    d &= (kFull || ly < nrow) ? keep : 0u;
+    if (kMask && keep && (kFull || ly < nrow)) mrow[static_cast<size_t>(ly) * a.nwords] = d;
+    occ += __popc(d);
+    occ_hi += __popc(d >> 16);
+    cols |= d;
+    if (d & 0xffffu) row_lo |= 1u << ly;
+    if (d > 0xffffu) row_hi |= 1u << ly;
+  }
+}
+
 // One warp: frame f, cell rows cy0 .. cy0+3, words [30*wi - 1, 30*wi + 31)
-// (lanes 1..30 own a word, lanes 0/31 are the neighbours).  kFused: raw rows
-// were written by other SMs during this launch -> L2 loads (ld.cg), activity
-// bits straight to global (zeroed before the launch); otherwise the CTA's
-// act_s collects them.
-template <int R, bool kFused>
+// (lanes 1..30 own a word, lanes 0/31 are the neighbours; a lane whose column
+// is outside the frame reads the zero page).  kFused: raw rows were written
+// by other SMs during this launch -> L2 loads (ld.cg), activity bits straight
+// to global (zeroed before the launch); otherwise the CTA's act_s collects
+// them.
+template <int R, bool kFused, bool kMask>
 __device__ __forceinline__ void dilate_strip(const DilateArgs& a, int f, int cy0, int wi, int lane,
                                              uint32_t (*act_s)[kK1MaxActWords]) {
   const int nb = min(kK1bBands, a.cells_y - cy0);
@@ -98,13 +129,11 @@ __device__ __forceinline__ void dilate_strip(const DilateArgs& a, int f, int cy0
   const bool owns = lane >= 1 && lane <= kK1GroupWords && col_ok;
   // bits this lane keeps: its own word, minus pixels past the frame edge
   const uint32_t keep = owns ? (w == a.nwords - 1 ? lastmask : 0xffffffffu) : 0u;
-  const int wc = min(max(w, 0), a.nwords - 1);  // clamped column: loads stay in bounds
-  const uint32_t cmask = col_ok ? 0xffffffffu : 0u;
-  const uint32_t* fr = a.raw + static_cast<size_t>(f) * a.H * a.nwords + wc;
+  const uint32_t* fr = col_ok ? a.raw + static_cast<size_t>(f) * a.H * a.nwords + w : a.zero;
   auto ld = [](const uint32_t* q) -> uint32_t { return kFused ? __ldcg(q) : __ldg(q); };
   // rows outside [0, H) read a clamped row and are masked to zero
   auto raw_row = [&](int yy) -> uint32_t {
-    const uint32_t m = (yy >= 0 && yy < a.H) ? cmask : 0u;
+    const uint32_t m = (yy >= 0 && yy < a.H) ? 0xffffffffu : 0u;
     return ld(fr + static_cast<size_t>(min(max(yy, 0), a.H - 1)) * a.nwords) & m;
   };
   // window of raw rows yb0 - R .. yb0 + 15 + R; consecutive bands share 2R rows
@@ -112,13 +141,13 @@ __device__ __forceinline__ void dilate_strip(const DilateArgs& a, int f, int cy0
   uint32_t win[kWin];
 #pragma unroll
   for (int i = 0; i < 2 * R; ++i) win[i] = raw_row(cy0 * kCell - R + i);
-  for (int bi = 0; bi < nb; ++bi) {
+  const uint32_t* q = fr + static_cast<size_t>(cy0 * kCell + R) * a.nwords;
+  for (int bi = 0; bi < nb; ++bi, q += kCell * a.nwords) {
     const int yb0 = (cy0 + bi) * kCell, cy = cy0 + bi;
     const bool interior = yb0 + kCell + R <= a.H;  // uniform: no row past the frame
     if (interior) {
-      const uint32_t* q = fr + static_cast<size_t>(yb0 + R) * a.nwords;
 #pragma unroll
-      for (int i = 2 * R; i < kWin; ++i) win[i] = ld(q + static_cast<size_t>(i - 2 * R) * a.nwords) & cmask;
+      for (int i = 2 * R; i < kWin; ++i) win[i] = ld(q + (i - 2 * R) * a.nwords);
     } else {
 #pragma unroll
       for (int i = 2 * R; i < kWin; ++i) win[i] = raw_row(yb0 - R + i);
@@ -128,7 +157,7 @@ __device__ __forceinline__ void dilate_strip(const DilateArgs& a, int f, int cy0
     uint32_t any = 0;
 #pragma unroll
     for (int i = 0; i < kWin; ++i) any |= win[i];
-    if (!a.mask_out && !__any_sync(0xffffffffu, any != 0)) {  // empty band tile: zero cells
+    if (!kMask && !__any_sync(0xffffffffu, any != 0)) {  // empty band tile: zero cells
       if (owns) {
         a.cells[cbase + 2 * w] = 0u;
         if (2 * w + 1 < a.cells_x) a.cells[cbase + 2 * w + 1] = 0u;
@@ -139,26 +168,11 @@ __device__ __forceinline__ void dilate_strip(const DilateArgs& a, int f, int cy0
     }
     int occ = 0, occ_hi = 0;
     uint32_t cols = 0, row_lo = 0, row_hi = 0;
-#pragma unroll
-    for (int ly = 0; ly < kCell; ++ly) {
-      uint32_t v = win[ly];
-#pragma unroll
-      for (int k = 1; k <= 2 * R; ++k) v |= win[ly + k];
-      const uint32_t vm = __shfl_up_sync(0xffffffffu, v, 1);
-      const uint32_t vp = __shfl_down_sync(0xffffffffu, v, 1);
-      uint32_t d = v;
-#pragma unroll
-      for (int k = 1; k <= R; ++k) d |= __funnelshift_r(v, vp, k) | __funnelshift_l(vm, v, k);
-      d &= ly < nrow ? keep : 0u;
-      if (a.mask_out && owns && ly < nrow)
-        a.mask_out[(static_cast<size_t>(f) * a.H + yb0 + ly) * a.nwords + w] = d;
-      const uint32_t dh = d >> 16;
-      occ += __popc(d);
-      occ_hi += __popc(dh);
-      cols |= d;
-      row_lo += min(d & 0xffffu, 1u) << ly;
-      row_hi += min(dh, 1u) << ly;
-    }
+    uint32_t* mrow = kMask ? a.mask_out + (static_cast<size_t>(f) * a.H + yb0) * a.nwords + w : nullptr;
+    if (nrow == kCell)
+      dilate_band<R, true, kMask>(a, win, keep, nrow, mrow, occ, occ_hi, cols, row_lo, row_hi);
+    else
+      dilate_band<R, false, kMask>(a, win, keep, nrow, mrow, occ, occ_hi, cols, row_lo, row_hi);
 #pragma unroll
     for (int i = 0; i < 2 * R; ++i) win[i] = win[kCell + i];
     if (owns) {
@@ -186,7 +200,10 @@ __global__ void __launch_bounds__(320) dilate_cells_kernel(const DilateArgs a) {
   const int nb = min(kK1bBands, a.cells_y - cy0);
   for (int i = threadIdx.x; i < kK1bBands * kK1MaxActWords; i += blockDim.x) (&act_s[0][0])[i] = 0;
   __syncthreads();
-  dilate_strip<R, false>(a, f, cy0, threadIdx.x >> 5, threadIdx.x & 31, act_s);
+  if (a.mask_out)
+    dilate_strip<R, false, true>(a, f, cy0, threadIdx.x >> 5, threadIdx.x & 31, act_s);
+  else
+    dilate_strip<R, false, false>(a, f, cy0, threadIdx.x >> 5, threadIdx.x & 31, act_s);
   __syncthreads();
   for (int i = threadIdx.x; i < nb * a.act_words; i += blockDim.x) {
     const int bi = i / a.act_words, aw = i - bi * a.act_words;
@@ -361,7 +378,10 @@ __device__ __forceinline__ void run_dilate_task(const MaskArgs& a, int t, int la
   switch (a.radius) {
 #define TG_DILATE_TASK(R) \
   case R:                 \
-    dilate_strip<R, true>(a.d, f, cy0, wi, lane, nullptr); \
+    if (a.d.mask_out)                                                          \
+      dilate_strip<R, true, true>(a.d, f, cy0, wi, lane, nullptr);             \
+    else                                                                       \
+      dilate_strip<R, true, false>(a.d, f, cy0, wi, lane, nullptr);            \
     break;
     TG_DILATE_TASK(0) TG_DILATE_TASK(1) TG_DILATE_TASK(2) TG_DILATE_TASK(3) TG_DILATE_TASK(4)
     TG_DILATE_TASK(5) TG_DILATE_TASK(6) TG_DILATE_TASK(7) TG_DILATE_TASK(8)
@@ -522,10 +542,12 @@ static int env_or(EnvInt& e, int dflt) {
   return v >= 0 ? v : dflt;
 }
 
-static DilateArgs dilate_args(const uint32_t* d_raw, int W, int H, uint32_t* d_cells,
+static DilateArgs dilate_args(const uint32_t* d_raw, const uint32_t* d_zero, int W, int H,
+                              uint32_t* d_cells,
                               uint32_t* d_active, uint32_t* d_mask) {
   DilateArgs d;
   d.raw = d_raw;
+  d.zero = d_zero;
   d.H = H;
   d.W = W;
   d.nwords = ceil_div(W, 32);
@@ -598,15 +620,16 @@ size_t mask_sync_words(int H, int sms) { return static_cast<size_t>(8) * sms + H
 
 cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                               int n_frames, int W, int H, int pitch, int threshold, int radius,
-                              uint32_t* d_raw, uint32_t* d_cells, uint32_t* d_active,
-                              uint32_t* d_mask, uint32_t* d_sync, int sms, cudaStream_t stream) {
+                              uint32_t* d_raw, const uint32_t* d_zero, uint32_t* d_cells,
+                              uint32_t* d_active, uint32_t* d_mask, uint32_t* d_sync, int sms,
+                              cudaStream_t stream) {
   if (n_frames <= 0) return cudaSuccess;
   if (radius < 0 || radius > kMaxRadius) return cudaErrorInvalidValue;
   MaskArgs a;
   size_t smem = 0;
   cudaError_t e = plan_k1(a, d_cur, d_prev, n_frames, W, H, pitch, threshold, d_raw, sms, &smem);
   if (e != cudaSuccess) return e;
-  a.d = dilate_args(d_raw, W, H, d_cells, d_active, d_mask);
+  a.d = dilate_args(d_raw, d_zero, W, H, d_cells, d_active, d_mask);
   if (a.d.act_words > kK1MaxActWords) return cudaErrorInvalidConfiguration;
   const size_t sync_words = mask_sync_words(H, sms);
   if (static_cast<size_t>(a.total_items) + 1 > sync_words) return cudaErrorInvalidConfiguration;
@@ -652,11 +675,11 @@ cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const*
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-cudaError_t launch_dilate_cells(const uint32_t* d_raw, int n_frames, int W, int H, int radius,
-                                uint32_t* d_cells, uint32_t* d_active, uint32_t* d_mask,
-                                cudaStream_t stream) {
+cudaError_t launch_dilate_cells(const uint32_t* d_raw, const uint32_t* d_zero, int n_frames,
+                                int W, int H, int radius, uint32_t* d_cells, uint32_t* d_active,
+                                uint32_t* d_mask, cudaStream_t stream) {
   if (n_frames <= 0) return cudaSuccess;
-  const DilateArgs d = dilate_args(d_raw, W, H, d_cells, d_active, d_mask);
+  const DilateArgs d = dilate_args(d_raw, d_zero, W, H, d_cells, d_active, d_mask);
   if (d.act_words > kK1MaxActWords) return cudaErrorInvalidConfiguration;
   const int dwarps = ceil_div(d.nwords, kK1GroupWords);
   const dim3 dg(n_frames * ceil_div(d.cells_y, kK1bBands)), db(dwarps * 32);

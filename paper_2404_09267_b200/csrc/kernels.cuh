@@ -9,17 +9,19 @@ namespace tg {
 cudaError_t launch_mask_fg(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                            int n_frames, int W, int H, int pitch, int threshold, uint32_t* d_raw,
                            int sms, cudaStream_t stream);
-cudaError_t launch_dilate_cells(const uint32_t* d_raw, int n_frames, int W, int H, int radius,
-                                uint32_t* d_cells, uint32_t* d_active, uint32_t* d_mask,
-                                cudaStream_t stream);
+// d_zero: H * ceil(W/32) zero words (what K1b reads for columns outside the frame)
+cudaError_t launch_dilate_cells(const uint32_t* d_raw, const uint32_t* d_zero, int n_frames,
+                                int W, int H, int radius, uint32_t* d_cells, uint32_t* d_active,
+                                uint32_t* d_mask, cudaStream_t stream);
 // K1 + K1b in one cooperative launch (K1b tasks run beside the stream);
 // d_sync: mask_sync_words(H, sms) u32 of scratch; when d_active follows it
 // directly (one allocation) a single memset clears both.
 size_t mask_sync_words(int H, int sms);
 cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                               int n_frames, int W, int H, int pitch, int threshold, int radius,
-                              uint32_t* d_raw, uint32_t* d_cells, uint32_t* d_active,
-                              uint32_t* d_mask, uint32_t* d_sync, int sms, cudaStream_t stream);
+                              uint32_t* d_raw, const uint32_t* d_zero, uint32_t* d_cells,
+                              uint32_t* d_active, uint32_t* d_mask, uint32_t* d_sync, int sms,
+                              cudaStream_t stream);
 
 // ---- K2-K4 per-frame planner + frame-order prefix (k_plan.cu) --------------
 struct PlanArgs {
