@@ -713,3 +713,41 @@ def test_cpp_dropin_per_frame_loop_matches_reference_build():
     assert ours.startswith("checksum ")
     if os.path.exists(os.path.join(cpp, "dropin_bench_ref")):
         assert ours == run("dropin_bench_ref")
+
+
+@pytest.mark.parametrize("radius", [0, 2])
+def test_mask_threshold_boundaries_random_bytes(ctx, radius):
+    """The per-pixel foreground test (max over channels of |cur - prev| > T,
+    K1's VIMNMX3 form and both SWAR threshold paths) against the oracle on
+    frames whose byte differences sit on and around every tested threshold
+    and the 7-bit boundary, for T across [0, 255]."""
+    from paper_2404_09267_b200 import _native as N
+    W, H, n = 640, 48, 3
+    rng = np.random.default_rng(7 + radius)
+    for T in (0, 1, 24, 25, 26, 126, 127, 128, 129, 200, 254, 255):
+        ring = A.FrameRing(ctx, W, H, n)
+        pitch = ring.pitch
+        base = rng.integers(0, 256, size=(H, pitch), dtype=np.int32)
+        frames = [base]
+        for _ in range(n):
+            d = rng.choice(np.array([0, 1, T - 1, T, T + 1, 127, 128, 255]), size=(H, pitch))
+            sign = rng.choice(np.array([-1, 1]), size=(H, pitch))
+            nxt = np.clip(frames[-1] + sign * d, 0, 255)
+            sparse = rng.random((H, pitch)) < 0.5  # half the bytes unchanged
+            frames.append(np.where(sparse, frames[-1], nxt))
+        frames = [f.astype(np.uint8) for f in frames]
+        for i, f in enumerate(frames):
+            ctx.upload(ring.slots[i], np.ascontiguousarray(f))
+        pipe = A.Pipeline(ctx, W, H, dilate_radius=radius, threshold=T, max_frames=n,
+                          keep_mask=1, max_canvases=64, pitch=pitch)
+        d_cur, d_prev = ring.tables()
+        A.check(N.lib().tg_pipeline_stage_mask(pipe.handle, n, d_cur, d_prev, None))
+        ctx.synchronize()
+        gm = pipe.mask(n)
+        cells = pipe.cells(n)
+        for i in range(n):
+            om = O.mask(frames[i + 1], frames[i], W, H, T, radius)
+            assert np.array_equal(gm[i], om), (T, radius, i)
+            assert np.array_equal(cells[i], O.cells(om, W, H)), (T, radius, i)
+        pipe.close()
+        ring.close()
