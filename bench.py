@@ -235,13 +235,17 @@ class Clocks:
                 "samples": len(sm)}
 
 
+NOMINAL_HBM_GBPS = 8000.0  # the north_star's "~8 TB/s" B200 HBM3e figure
+
+
 def roofline(kernel: str, bytes_per_launch: float, launch_ms: float, traffic, note: str) -> dict:
     peak, src = peaks()
     achieved = bytes_per_launch / (launch_ms / 1e3) / 1e9
     return {"bound": "hbm", "kernel": kernel, "achieved": round(achieved, 1), "peak": peak,
             "unit": "GB/s", "frac": round(achieved / peak, 4),
             "traffic": traffic, "algorithmic_bytes_per_launch": int(bytes_per_launch),
-            "launch_ms": round(launch_ms, 4), "peak_source": src, "bytes": note}
+            "launch_ms": round(launch_ms, 4), "peak_source": src, "bytes": note,
+            "frac_vs_nominal_8TBps": round(achieved / NOMINAL_HBM_GBPS, 4)}
 
 
 def path_record(unique_bytes: int, ms_step: float, b_run: int, stage_ms: dict, extra: dict) -> dict:
@@ -249,6 +253,7 @@ def path_record(unique_bytes: int, ms_step: float, b_run: int, stage_ms: dict, e
     gbps = unique_bytes / (ms_step / 1e3) / 1e9
     rec = {"unique_bytes_per_step": int(unique_bytes), "unique_GBps": round(gbps, 1),
            "unique_frac": round(gbps / peak, 4),
+           "unique_frac_vs_nominal_8TBps": round(gbps / NOMINAL_HBM_GBPS, 4),
            "unique_bytes_def": "frames read once each (cur chains, one background per camera) + "
                                "admitted patch pixels read + every canvas byte written",
            "B_run_model_bytes": int(b_run),
