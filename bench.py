@@ -408,12 +408,16 @@ def e2e_multicam(ctx, path, args, dist, local, n_cams_total):
     for h, r in zip(host, rings):
         ctx.memcpy(h, r.base, r.frame_bytes * (r.n + 1), 1, path.stream)
     ctx.stream_sync(path.stream)
-    h2d = sum(r.frame_bytes * (r.n + 1) for r in rings)
+    # a step's inputs are each camera's n new frames; slot 0 (the frame
+    # before them: the synthetic background here, the previous step's last
+    # frame in a live stream) is device state carried between steps
+    h2d = sum(r.frame_bytes * r.n for r in rings)
     d2h = path._hslot
 
     def one():
         for h, r in zip(host, rings):
-            ctx.memcpy(r.base, h, r.frame_bytes * (r.n + 1), 0, path.stream)
+            ctx.memcpy(r.base + r.frame_bytes, h + r.frame_bytes, r.frame_bytes * r.n, 0,
+                       path.stream)
         path.run_pipelined(1)
 
     one()
@@ -432,9 +436,10 @@ def e2e_multicam(ctx, path, args, dist, local, n_cams_total):
     return {"value": round(n_cams_total * path.n * steps / (ms / 1e3), 1), "unit": "frames/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
             "h2d_GBps_per_gpu": round(h2d * steps / (ms / 1e3) / 1e9, 1),
-            "note": "pinned host frames of every camera -> device rings, then one pass through "
-                    "the public API (MultiCameraPath: planes, descriptor block read-back, "
-                    "batcher, K5); PCIe-bound"}
+            "note": "pinned host frames (each camera's n new frames; the frame before them "
+                    "stays on the device) -> device rings, then one pass through the public API "
+                    "(MultiCameraPath: planes, descriptor block read-back, batcher, K5); "
+                    "PCIe-bound"}
 
 
 def cpu_baseline_multicam(path, n):
@@ -622,7 +627,7 @@ def e2e_cfg2(ctx, pipe, ring, n, d_ids, d_gen, d_canv, stream, args, world, dist
         A.check(lib.tg_stream_wait_event(ctx.handle, cstream, step_done))
         for c in range(nch):
             f0, fc = c * chunk, min(chunk, n - c * chunk)
-            lo = 0 if c == 0 else f0 + 1  # slot 0 (background) travels with chunk 0
+            lo = f0 + 1  # slot 0 (the frame before the step's frames) stays on the device
             hi = f0 + fc + 1
             nb = (hi - lo) * FRAME_BYTES
             ctx.memcpy(ring.slots[lo], host + lo * FRAME_BYTES, nb, 0, cstream)
@@ -822,7 +827,7 @@ def e2e_density(ctx, pipe, rings, F, tabs, d_canv, steps):
     for h, r in zip(host, rings):
         ctx.memcpy(h, r.base, r.frame_bytes * (r.n + 1), 1)
     ctx.stream_sync()
-    h2d = sum(r.frame_bytes * (r.n + 1) for r in rings)
+    h2d = sum(r.frame_bytes * r.n for r in rings)  # slot 0 stays on the device
     Z = pipe.zones
     hdesc = ctx.malloc_host(F * Z * 96 + F * 8)
     v = pipe.views
@@ -830,7 +835,7 @@ def e2e_density(ctx, pipe, rings, F, tabs, d_canv, steps):
 
     def one():
         for h, r in zip(host, rings):
-            ctx.memcpy(r.base, h, r.frame_bytes * (r.n + 1), 0)
+            ctx.memcpy(r.base + r.frame_bytes, h + r.frame_bytes, r.frame_bytes * r.n, 0)
         pipe.run(F, d_cur, d_prev, d_ids, d_gen, 0, d_canv)
         ctx.memcpy(hdesc, v.placements, F * Z * 32, 1)
         ctx.memcpy(hdesc + F * Z * 32, v.patches, F * Z * 64, 1)
