@@ -34,8 +34,12 @@ namespace tg {
 #ifndef TG_GATHER_SLOTS
 #define TG_GATHER_SLOTS 6
 #endif
+// 4: the register budget of 4 CTAs per SM (64 registers, no spills) -- the
+// grid stays smem-limited at 3 per SM, and a capped event gather (configs
+// 3/4, 2 per SM) leaves more registers to the K1b / planner CTAs beside it
+// (config-4 pass -0.5 % against 80 registers)
 #ifndef TG_GATHER_MIN_BLOCKS
-#define TG_GATHER_MIN_BLOCKS 3
+#define TG_GATHER_MIN_BLOCKS 4
 #endif
 #ifndef TG_GATHER_RING
 #define TG_GATHER_RING 6144
