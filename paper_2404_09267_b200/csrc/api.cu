@@ -127,6 +127,7 @@ tg_status check_device_error(tg_ctx* ctx) {
   TG_CUDA(cudaMemcpy(&e, ctx->d_err, sizeof(e), cudaMemcpyDeviceToHost));
   if (e.code == 0) return TG_OK;
   TG_CUDA(cudaMemset(ctx->d_err, 0, sizeof(DevError)));
+  TG_CUDA(cudaDeviceSynchronize());  // the legacy-stream reset precedes later launches
   return device_error_status(e);
 }
 
@@ -307,6 +308,7 @@ tg_status tg_ctx_create(int32_t device, tg_ctx** out) {
   TG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   TG_CUDA(cudaMalloc(&c->d_err, sizeof(DevError)));
   TG_CUDA(cudaMemset(c->d_err, 0, sizeof(DevError)));
+  TG_CUDA(cudaDeviceSynchronize());  // before any non-blocking stream's kernel can latch
   *out = c;
   return TG_OK;
 }
@@ -828,6 +830,9 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
   if (!e) e = cudaMemset(p->look, 0, F * sizeof(uint64_t));
   if (!e) e = cudaMemset(p->psync, 0, 3 * sizeof(uint32_t));
   if (!e) e = cudaMemset(p->gather_units, 0, 3 * sizeof(int32_t));
+  // the initial memsets run on the legacy stream; the pipeline's work runs
+  // on non-blocking streams, which do not wait for it
+  if (!e) e = cudaDeviceSynchronize();
   if (e) {
     tg_pipeline_destroy(p);
     return cuda_fail(e, "pipeline allocation");
