@@ -215,12 +215,17 @@ struct Carver {
   }
 };
 
-tg_status zone_grid_check(int width, int height, tg_partition_config cfg) {
-  // partition.hpp:70-73
+// partition.hpp:70-73.  `device_limit`: the fused per-frame planner keeps a
+// frame's zones in shared memory (kMaxZones); the drop-in partition takes
+// any grid, like the reference.
+tg_status zone_grid_check(int width, int height, tg_partition_config cfg, bool device_limit) {
   if (cfg.zones_x < 1 || cfg.zones_y < 1 || cfg.zones_x > width || cfg.zones_y > height)
     return fail(TG_ERR_INVALID_ARGUMENT, "zone grid finer than frame");
-  if (cfg.zones_x * cfg.zones_y > kMaxZones)
-    return fail(TG_ERR_INVALID_ARGUMENT, "zone grid exceeds the device limit (%d zones)", kMaxZones);
+  if (device_limit && cfg.zones_x * cfg.zones_y > kMaxZones)
+    return fail(TG_ERR_INVALID_ARGUMENT, "zone grid exceeds the pipeline limit (%d zones)",
+                kMaxZones);
+  if (static_cast<long long>(cfg.zones_x) * cfg.zones_y > (1 << 24))
+    return fail(TG_ERR_INVALID_ARGUMENT, "zone grid too large");
   return TG_OK;
 }
 
@@ -583,7 +588,7 @@ tg_status tg_partition(tg_ctx* ctx, const tg_frame_spec* frame, tg_partition_con
                        int32_t* n_patches) {
   tg_status s = use_device(ctx);
   if (s) return s;
-  if ((s = zone_grid_check(frame->width, frame->height, cfg))) return s;
+  if ((s = zone_grid_check(frame->width, frame->height, cfg, false))) return s;
   const int nz = cfg.zones_x * cfg.zones_y;
   Carver cv;
   const size_t o_f = cv.take<tg_frame_spec>(1), o_off = cv.take<int32_t>(2),
@@ -770,7 +775,7 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
     return fail(TG_ERR_INVALID_ARGUMENT, "threshold must be in [0, 255]");
   if (q.dilate_radius < 0 || q.dilate_radius > kMaxRadius)
     return fail(TG_ERR_INVALID_ARGUMENT, "dilate radius must be in [0, %d]", kMaxRadius);
-  if ((s = zone_grid_check(q.width, q.height, q.partition))) return s;
+  if ((s = zone_grid_check(q.width, q.height, q.partition, true))) return s;
   if (q.canvas.width < 1 || q.canvas.height < 1 || q.canvas.width > 65535 ||
       q.canvas.height > 65535)
     return fail(TG_ERR_INVALID_ARGUMENT, "canvas dimensions must be in [1, 65535]");

@@ -379,28 +379,57 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
 
 // ---- drop-in / batched rect-level kernels ---------------------------------
 // One block per frame: partition() of host-supplied RoIs.
+// Zones are accumulated kMaxZones at a time (any grid, like the reference's
+// partition): each chunk's non-empty zones become patches in zone order,
+// numbered after the previous chunks'.
 __global__ void __launch_bounds__(256) partition_batch_kernel(const PartitionBatchArgs a) {
   __shared__ ZoneAcc zacc;
   __shared__ tg_patch_meta sp[kMaxZones];
+  __shared__ int s_base;
   const int f = blockIdx.x, tid = threadIdx.x, nz = a.X * a.Y;
   const tg_frame_spec fs = a.frames[f];
   const int r0 = a.roi_offsets[f], r1 = a.roi_offsets[f + 1];
-  zone_acc_init(zacc, nz, tid, blockDim.x);
-  __syncthreads();
-  partition_accumulate(a.rois + r0, r1 - r0, fs.width, fs.height, a.X, a.Y, zacc, a.err, f,
-                       a.zone_of ? a.zone_of + r0 : nullptr, tid, blockDim.x);
-  __threadfence_system();  // zone_of may be host-mapped: visible before n_patches
-  __syncthreads();
+  const tg_rect* rois = a.rois + r0;
+  if (tid == 0) s_base = 0;
+  for (int zc = 0; zc < nz; zc += kMaxZones) {
+    const int cn = min(kMaxZones, nz - zc);
+    zone_acc_init(zacc, cn, tid, blockDim.x);
+    __syncthreads();
+    for (int i = tid; i < r1 - r0; i += blockDim.x) {
+      const tg_rect r = rois[i];
+      const int bz = best_zone(r, fs.width, fs.height, a.X, a.Y);
+      if (zc == 0) {
+        if (a.zone_of) a.zone_of[r0 + i] = bz;
+        // with zone_of the caller reports the FIRST bad index itself (the
+        // reference throws at the lowest one, partition.hpp:106-108)
+        else if (bz < 0) raise_error(a.err, TG_ERR_INVALID_ARGUMENT, kErrRoiOutside, i, f);
+      }
+      const int zi = bz - zc;
+      if (bz < zc || zi >= cn) continue;  // outside the frame, or another chunk's zone
+      atomicMin(&zacc.x0[zi], r.x);
+      atomicMin(&zacc.y0[zi], r.y);
+      atomicMax(&zacc.x1[zi], r.x + r.w);
+      atomicMax(&zacc.y1[zi], r.y + r.h);
+      atomicAdd(&zacc.cnt[zi], 1);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const int base = s_base;
+      const int np = partition_emit(zacc, cn, fs.frame_id, fs.generation_time_us, fs.slo_us,
+                                    a.bpp, a.first_ids[f] + static_cast<uint64_t>(base), sp, tid);
+      __syncwarp();
+      for (int j = tid; j < np; j += 32) a.patches[static_cast<size_t>(f) * nz + base + j] = sp[j];
+      __syncwarp();
+      if (tid == 0) s_base = base + np;
+    }
+    __syncthreads();
+  }
   if (tid >= 32) return;
-  const int np = partition_emit(zacc, nz, fs.frame_id, fs.generation_time_us, fs.slo_us, a.bpp,
-                                a.first_ids[f], sp, tid);
+  __threadfence_system();  // zone_of / patches may be host-mapped: visible before n_patches
   __syncwarp();
-  for (int j = tid; j < np; j += 32) a.patches[static_cast<size_t>(f) * nz + j] = sp[j];
   // n_patches is written last: the blocking drop-in waits on it in mapped
   // host memory instead of synchronizing the stream
-  __threadfence_system();
-  __syncwarp();
-  if (tid == 0) a.n_patches[f] = np;
+  if (tid == 0) a.n_patches[f] = s_base;
 }
 
 // One warp per queue; the free set ends in the caller's workspace.  A short

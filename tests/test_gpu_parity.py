@@ -80,6 +80,26 @@ def test_partition_dropin_random_vs_reference_port(ctx):
         assert patch_tuples([got])[0] == oracle_patch_tuples([want])[0]
 
 
+def test_partition_dropin_any_zone_grid(ctx):
+    """The drop-in partition takes any zone grid, like the reference (the
+    device accumulates zones 64 at a time): grids past 64 zones, against the
+    port and the reference build."""
+    rng = O.Rng(O.derive_seed(9, "partition-big-grids"))
+    lib = "ref" if O.have_ref() else "port"
+    for it, (zx, zy) in enumerate([(13, 5), (8, 9), (20, 20), (64, 2), (100, 30), (3, 200)]):
+        W, H = max(zx, 1920), max(zy, 1080)
+        n = rng.uniform_int(0, 120)
+        rois = []
+        for _ in range(n):
+            w, h = rng.uniform_int(1, W // 3), rng.uniform_int(1, H // 3)
+            rois.append((rng.uniform_int(0, W - w), rng.uniform_int(0, H - h), w, h))
+        got = A.partition(A.FrameSpec(it, W, H, 1000 * it, 5000), A.PartitionConfig(zx, zy), rois,
+                          1.5, 7 * it, ctx=ctx)
+        want = O.partition(it, W, H, 1000 * it, 5000, zx, zy, rois, 1.5, 7 * it, lib=lib)
+        assert len(got) > 0 or n == 0
+        assert patch_tuples([got])[0] == oracle_patch_tuples([want])[0], (zx, zy)
+
+
 def _stitch_tuples(res):
     pl = sorted([(p.patch_id, p.canvas_index, p.position.x, p.position.y, p.position.w,
                   p.position.h) for c in res.canvases for p in c.placements])
@@ -468,7 +488,7 @@ def test_pipeline_argument_validation(ctx):
         (dict(W=640, H=64, threshold=256), "threshold"),
         (dict(W=640, H=64, dilate_radius=9), "dilate radius"),
         (dict(W=640, H=32, zones=(1, 40)), "zone grid finer than frame"),
-        (dict(W=640, H=64, zones=(13, 5)), "device limit"),
+        (dict(W=640, H=64, zones=(13, 5)), "pipeline limit"),
         (dict(W=640, H=64, canvas=(0, 1024)), "canvas dimensions"),
         (dict(W=640, H=64, max_frames=0), "capacities"),
         (dict(W=8192, H=2064), "more than 65535"),
