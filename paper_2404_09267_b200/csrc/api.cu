@@ -221,9 +221,9 @@ struct Carver {
 tg_status zone_grid_check(int width, int height, tg_partition_config cfg, bool device_limit) {
   if (cfg.zones_x < 1 || cfg.zones_y < 1 || cfg.zones_x > width || cfg.zones_y > height)
     return fail(TG_ERR_INVALID_ARGUMENT, "zone grid finer than frame");
-  if (device_limit && cfg.zones_x * cfg.zones_y > kMaxZones)
+  if (device_limit && cfg.zones_x * cfg.zones_y > kMaxPlanZones)
     return fail(TG_ERR_INVALID_ARGUMENT, "zone grid exceeds the pipeline limit (%d zones)",
-                kMaxZones);
+                kMaxPlanZones);
   if (static_cast<long long>(cfg.zones_x) * cfg.zones_y > (1 << 24))
     return fail(TG_ERR_INVALID_ARGUMENT, "zone grid too large");
   return TG_OK;
@@ -785,7 +785,8 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
   if (static_cast<long long>(cx) * cy > 65535 ||
       static_cast<long long>(ceil_div(cx, 32)) * cy * 16 > 65536)  // 16-bit CCL run slots
     return fail(TG_ERR_INVALID_ARGUMENT, "frame has more than 65535 %dx%d cells", kCell, kCell);
-  if (plan_smem_bytes(cx, cy, q.max_rois_per_frame) > 200 * 1024)
+  if (plan_smem_bytes(cx, cy, q.max_rois_per_frame,
+                      q.partition.zones_x * q.partition.zones_y) > 200 * 1024)
     return fail(TG_ERR_INVALID_ARGUMENT, "max_rois_per_frame too large for this frame size");
   // patch and canvas prefixes travel in 23-bit look-back fields
   if (static_cast<long long>(q.max_frames) * q.partition.zones_x * q.partition.zones_y >= (1 << 23))

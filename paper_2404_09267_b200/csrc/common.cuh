@@ -11,7 +11,8 @@
 namespace tg {
 
 constexpr int kCell = TG_CELL_SIZE;   // 16x16-pixel patch-grid cells
-constexpr int kMaxZones = 64;         // X*Y supported by the device partitioner
+constexpr int kMaxZones = 64;         // zones per partitioner chunk / fast planner variant
+constexpr int kMaxPlanZones = 256;    // X*Y supported by the fused per-frame planner
 constexpr int kMaxRadius = 8;         // dilation radius bound (K1b register window)
 
 // Device-side error latch (first error wins), read back at sync points.

@@ -138,24 +138,27 @@ __device__ void plan_totals(const PlanArgs& a, uint64_t first_id, uint64_t total
 
 // K3/K4 working set; aliases the K2 (CCL) region of dynamic smem once the
 // RoI boxes are out, so three planner CTAs fit on an SM.
+template <int Z>
 struct PlanTail {
-  tg_patch_meta spatch[kMaxZones];
-  FreeRect freel[2 * kMaxZones + 2];
-  StitchOut souts[kMaxZones];
-  Job sjobs[3 * kMaxZones];
+  tg_patch_meta spatch[Z];
+  FreeRect freel[2 * Z + 2];
+  StitchOut souts[Z];
+  Job sjobs[3 * Z];
 };
 
 #ifdef TG_PLAN_PHASES
 __device__ unsigned long long g_plan_phase[16];
 #endif
 
+// Z: zones per frame at most (kMaxZones, or kMaxPlanZones for finer grids)
+template <int Z>
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   extern __shared__ __align__(16) uint8_t dsm[];
-  __shared__ ZoneAcc zacc;
-  __shared__ int adm_w[kMaxZones], adm_h[kMaxZones], adm_idx[kMaxZones];
+  __shared__ ZoneAccT<Z> zacc;
+  __shared__ int adm_w[Z], adm_h[Z], adm_idx[Z];
   __shared__ int warp_tmp[32];
   __shared__ int s_nrois;
-  PlanTail& T = *reinterpret_cast<PlanTail*>(dsm);
+  PlanTail<Z>& T = *reinterpret_cast<PlanTail<Z>*>(dsm);
   tg_patch_meta* spatch = T.spatch;
   FreeRect* freel = T.freel;
   StitchOut* souts = T.souts;
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
 
   // ---- K4: stitch plan (Alg. 2 solver) -------------------------------------
   int nfree = 0;
-  const int nc = na ? bssf_stitch(adm_w, adm_h, nullptr, na, a.M, a.N, freel, 2 * kMaxZones + 2,
+  const int nc = na ? bssf_stitch(adm_w, adm_h, nullptr, na, a.M, a.N, freel, 2 * Z + 2,
                                   souts, &nfree, a.err, f, lane)
                     : 0;
   __syncwarp();
@@ -260,9 +263,9 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   const int ncv = nc < 0 ? 0 : nc;
   look_publish(a, f, s_epoch, static_cast<uint64_t>(np), static_cast<uint64_t>(ncv), lane);
   // Gather jobs (frame-local): placements and free rects grouped by canvas,
-  // sorted by x; lane c keeps canvases c and c + 32's (first job, count)
-  // for their ranges (a frame has at most zones <= 64 canvases).
-  uint32_t my_rng[2] = {0u, 0u};  // first job | count << 16
+  // sorted by x; lane c keeps canvases c, c + 32, ...: (first job, count)
+  // for their ranges (a frame has at most Z canvases).
+  uint32_t my_rng[Z / 32] = {};  // first job | count << 16
   if (ncv > 0) {
     Job* fj = a.jobs + static_cast<size_t>(f) * a.job_cap;
     uint32_t* fcj = a.canvas_jobs + static_cast<size_t>(f) * nz;
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     if (f == a.n_frames - 1) plan_totals(a, s_first, ex_p + np, cb + ncv);
   }
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < Z / 32; ++h) {
     const int c = lane + 32 * h;
     if (c < ncv && cb + c < a.max_canvases)
       a.ranges[cb + c] = make_uint2(static_cast<uint32_t>(f) * a.job_cap + (my_rng[h] & 0xffffu),
@@ -499,22 +502,32 @@ __global__ void __launch_bounds__(128) stitch_batch_kernel(const StitchBatchArgs
 }
 
 // ---- launchers --------------------------------------------------------------
-size_t plan_smem_bytes(int cells_x, int cells_y, int max_rois) {
+size_t plan_smem_bytes(int cells_x, int cells_y, int max_rois, int zones) {
   const int aw = ceil_div(cells_x, 32);
   const size_t ncw = static_cast<size_t>(cells_y) * aw;
   const size_t ccl = ncw * 4 * 2 + (ncw + 1) * 4 + static_cast<size_t>(max_rois) * 16 +
                      ncw * kHeadsPerWord * 2 + 16;
-  return ccl > sizeof(PlanTail) ? ccl : sizeof(PlanTail);
+  const size_t tail = zones <= kMaxZones ? sizeof(PlanTail<kMaxZones>)
+                                         : sizeof(PlanTail<kMaxPlanZones>);
+  return ccl > tail ? ccl : tail;
+}
+
+template <int Z>
+static cudaError_t launch_plan_t(const PlanArgs& a, size_t smem, cudaStream_t stream) {
+  static SmemOptIn opt_in;
+  cudaError_t e = opt_in.ensure(plan_kernel<Z>, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  plan_kernel<Z><<<a.n_frames > 0 ? a.n_frames : 1, kPlanThreads, smem, stream>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
   if (a.n_frames < 0) return cudaErrorInvalidValue;
-  static SmemOptIn opt_in;
-  const size_t smem = plan_smem_bytes(a.cells_x, a.cells_y, a.max_rois);
-  cudaError_t e = opt_in.ensure(plan_kernel, static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  plan_kernel<<<a.n_frames > 0 ? a.n_frames : 1, kPlanThreads, smem, stream>>>(a);
-  return cudaGetLastError();
+  const int nz = a.X * a.Y;
+  if (nz > kMaxPlanZones) return cudaErrorInvalidValue;
+  const size_t smem = plan_smem_bytes(a.cells_x, a.cells_y, a.max_rois, nz);
+  return nz <= kMaxZones ? launch_plan_t<kMaxZones>(a, smem, stream)
+                         : launch_plan_t<kMaxPlanZones>(a, smem, stream);
 }
 
 

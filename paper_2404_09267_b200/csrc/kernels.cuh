@@ -92,7 +92,7 @@ struct StitchBatchArgs {
 // free sets) in shared memory.
 constexpr int kStitchStage = 128;
 
-size_t plan_smem_bytes(int cells_x, int cells_y, int max_rois);
+size_t plan_smem_bytes(int cells_x, int cells_y, int max_rois, int zones);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
 cudaError_t launch_partition_batch(const PartitionBatchArgs& a, cudaStream_t stream);
 cudaError_t launch_stitch_batch(const StitchBatchArgs& a, cudaStream_t stream);

@@ -56,12 +56,15 @@ __device__ __forceinline__ int best_zone(const tg_rect& r, int W, int H, int X, 
   return bz;
 }
 
-// Per-zone enclosing-rect accumulators in shared memory.
-struct ZoneAcc {
-  int x0[kMaxZones], y0[kMaxZones], x1[kMaxZones], y1[kMaxZones], cnt[kMaxZones];
+// Per-zone enclosing-rect accumulators in shared memory (Z zones at most).
+template <int Z>
+struct ZoneAccT {
+  int x0[Z], y0[Z], x1[Z], y1[Z], cnt[Z];
 };
+using ZoneAcc = ZoneAccT<kMaxZones>;
 
-__device__ __forceinline__ void zone_acc_init(ZoneAcc& z, int nz, int tid, int nthreads) {
+template <class ZA>
+__device__ __forceinline__ void zone_acc_init(ZA& z, int nz, int tid, int nthreads) {
   for (int i = tid; i < nz; i += nthreads) {
     z.x0[i] = INT_MAX;
     z.y0[i] = INT_MAX;
@@ -73,9 +76,9 @@ __device__ __forceinline__ void zone_acc_init(ZoneAcc& z, int nz, int tid, int n
 
 // Block-cooperative assignment of n RoIs into the zone accumulators.
 // Returns nothing; an RoI outside the frame latches kErrRoiOutside.
-template <class RectAt>
+template <class RectAt, class ZA>
 __device__ __forceinline__ void partition_accumulate_at(RectAt rect_at, int n, int W, int H,
-                                                        int X, int Y, ZoneAcc& z, DevError* err,
+                                                        int X, int Y, ZA& z, DevError* err,
                                                         int frame, int* zone_of, int tid,
                                                         int nthreads) {
   for (int i = tid; i < n; i += nthreads) {
@@ -106,7 +109,8 @@ __device__ __forceinline__ void partition_accumulate(const tg_rect* rois, int n,
 
 // One warp: one patch per non-empty zone in zone order (partition.hpp:
 // 125-141).  patch_id = first_id + rank; returns the patch count.
-__device__ __forceinline__ int partition_emit(const ZoneAcc& z, int nz, uint64_t frame_id,
+template <class ZA>
+__device__ __forceinline__ int partition_emit(const ZA& z, int nz, uint64_t frame_id,
                                               int64_t gen_us, int64_t slo_us, double bpp,
                                               uint64_t first_id, tg_patch_meta* out, int lane) {
   int base = 0;

@@ -388,6 +388,9 @@ def test_round_trip_fixture(ctx):
     dict(W=640, H=360, n=5, threshold=200),            # the T >= 128 SWAR path
     dict(W=1280, H=720, n=4, zones=(1, 1)),
     dict(W=1280, H=720, n=4, zones=(8, 8)),
+    dict(W=1280, H=720, n=4, zones=(10, 9)),            # past 64 zones: the 256-zone planner
+    dict(W=1920, H=1088, n=3, zones=(16, 16), trace_kw=dict(roi_proportion_mean=0.3,
+                                                            roi_count_max=40)),
     dict(W=1280, H=720, n=4, zones=(3, 5), canvas=(300, 200)),
     dict(W=640, H=352, n=3, pitch=640 * 3 + 64),       # padded rows
     dict(W=8192, H=48, n=3),                           # 4 K1 parts per row, 2 rows per item
@@ -488,7 +491,7 @@ def test_pipeline_argument_validation(ctx):
         (dict(W=640, H=64, threshold=256), "threshold"),
         (dict(W=640, H=64, dilate_radius=9), "dilate radius"),
         (dict(W=640, H=32, zones=(1, 40)), "zone grid finer than frame"),
-        (dict(W=640, H=64, zones=(13, 5)), "pipeline limit"),
+        (dict(W=640, H=64, zones=(20, 13)), "pipeline limit"),
         (dict(W=640, H=64, canvas=(0, 1024)), "canvas dimensions"),
         (dict(W=640, H=64, max_frames=0), "capacities"),
         (dict(W=8192, H=2064), "more than 65535"),
