@@ -392,7 +392,7 @@ __device__ __forceinline__ void run_dilate_task(const MaskArgs& a, int t, int la
 }
 
 // Drains the queue, waiting for each claimed task's items.
-__device__ void run_dilate_tasks(const MaskArgs& a, int lane) {
+__device__ __forceinline__ void run_dilate_tasks(const MaskArgs& a, int lane) {
   for (;;) {
     int t = 0;
     if (lane == 0) t = static_cast<int>(atomicAdd(a.task_next, 1u));
