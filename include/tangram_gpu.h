@@ -118,8 +118,10 @@ tg_status tg_device_sm_count(tg_ctx* ctx, int32_t* sms);
  * canvas gathers' persistent grid (tg_stitch_gather, tg_batcher_gather*;
  * 0 = SMs x the occupancy limit): below that, the next pass's K1b and
  * planner CTAs co-run with the event gather of configs 3/4 instead of
- * queueing behind it. */
-typedef enum { TG_OPT_GATHER_GRID = 1 } tg_option;
+ * queueing behind it.  TG_OPT_GATHER_BAND sets the canvas rows per
+ * (canvas, band) work unit of those gathers (0 = automatic: 64 rows, up to
+ * 512 for plans of many canvases). */
+typedef enum { TG_OPT_GATHER_GRID = 1, TG_OPT_GATHER_BAND = 2 } tg_option;
 tg_status tg_ctx_set_option(tg_ctx* ctx, int32_t option, int64_t value);
 
 /* ---- memory / streams / events (plumbing for callers without a CUDA

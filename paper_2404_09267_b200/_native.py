@@ -20,6 +20,7 @@ TG_ERR_CUDA = 4
 TG_ERR_NO_DEVICE = 5
 TG_ERR_COMM = 6
 TG_OPT_GATHER_GRID = 1
+TG_OPT_GATHER_BAND = 2
 
 
 class tg_rect(C.Structure):

@@ -72,6 +72,7 @@ struct tg_ctx {
   int32_t g_units_h[3] = {0, 0, 0};
   size_t g_job_cap = 0, g_range_cap = 0;
   int32_t gather_grid = 0;  // TG_OPT_GATHER_GRID (0: SMs x the occupancy limit)
+  int32_t gather_band = 0;  // TG_OPT_GATHER_BAND (0: gather_band())
 };
 
 struct tg_pipeline {
@@ -265,7 +266,9 @@ tg_status tg_internal_run_gather(tg_ctx* ctx, const void* jobs, int32_t n_jobs, 
     TG_CUDA(cudaMalloc(&ctx->g_ranges, ctx->g_range_cap * sizeof(uint2)));
   }
   if (!ctx->g_units) TG_CUDA(cudaMalloc(&ctx->g_units, 3 * sizeof(int32_t)));
-  const int nbands = gather_bands(spec.height);
+  const int band =
+      ctx->gather_band > 0 ? ctx->gather_band : gather_band(n_canvases, spec.height, ctx->sms);
+  const int nbands = gather_bands(spec.height, band);
   ctx->g_units_h[0] = n_canvases * nbands;
   ctx->g_units_h[1] = 0;  // K5's unit claim counter
   ctx->g_units_h[2] = 0;  // K5's finished-CTA counter
@@ -280,6 +283,7 @@ tg_status tg_internal_run_gather(tg_ctx* ctx, const void* jobs, int32_t n_jobs, 
   g.M = spec.width;
   g.N = spec.height;
   g.nbands = nbands;
+  g.band = band;
   g.jobs = ctx->g_jobs;
   g.ranges = ctx->g_ranges;
   g.units = ctx->g_units;
@@ -347,6 +351,10 @@ tg_status tg_ctx_set_option(tg_ctx* ctx, int32_t option, int64_t value) {
     case TG_OPT_GATHER_GRID:
       if (value < 0 || value > (1 << 20)) return fail(TG_ERR_INVALID_ARGUMENT, "gather grid out of range");
       ctx->gather_grid = static_cast<int32_t>(value);
+      return TG_OK;
+    case TG_OPT_GATHER_BAND:
+      if (value < 0 || value > (1 << 16)) return fail(TG_ERR_INVALID_ARGUMENT, "gather band out of range");
+      ctx->gather_band = static_cast<int32_t>(value);
       return TG_OK;
     default:
       return fail(TG_ERR_INVALID_ARGUMENT, "unknown context option %d", option);
@@ -800,7 +808,7 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
   p->act_words = ceil_div(cx, 32);
   p->mask_words = ceil_div(q.width, 32);
   p->job_cap = 3 * p->zones;
-  p->nbands = gather_bands(q.canvas.height);
+  p->nbands = gather_bands(q.canvas.height, kGatherDefaultBand);
   const size_t F = q.max_frames, Z = p->zones;
   auto alloc = [&](auto** ptr, size_t count) -> cudaError_t {
     return cudaMalloc(reinterpret_cast<void**>(ptr), std::max<size_t>(1, count) * sizeof(**ptr));
@@ -978,6 +986,7 @@ tg_status tg_pipeline_stage_gather(tg_pipeline* p, int32_t n_frames, const uint8
   g.M = p->p.canvas.width;
   g.N = p->p.canvas.height;
   g.nbands = p->nbands;
+  g.band = kGatherDefaultBand;
   g.jobs = p->jobs;
   g.ranges = p->ranges;
   g.units = p->gather_units;

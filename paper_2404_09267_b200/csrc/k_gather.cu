@@ -4,11 +4,12 @@
 // Every canvas is exactly tiled by its placements plus its final guillotine
 // free rects: each canvas row is a left-to-right
 // sequence of intervals, each either a patch's source row or zeros.  A
-// persistent grid claims (canvas, 64-row band) units from a device counter
+// persistent grid claims (canvas, band of rows) units from a device counter
 // -- their count is what the planner left in device memory (no host
 // round trip between planning and gathering); dynamic claiming keeps CTAs
 // that drew light, zero-fill bands busy, so the grid drains together (static
-// round robin: 0.82 ms vs 0.66 ms per 300 4K frames).  Warp w of a block
+// round robin: 0.82 ms vs 0.66 ms per 300 4K frames); bands are 64 rows, or
+// up to 512 for long explicit plans (gather_band).  Warp w of a block
 // owns rows b0 + w, b0 + w + 8, ... of the band, split into 3 KB destination
 // segments ("items").
 //
@@ -44,9 +45,6 @@ namespace tg {
 #ifndef TG_GATHER_RING
 #define TG_GATHER_RING 6144
 #endif
-#ifndef TG_GATHER_BAND
-#define TG_GATHER_BAND 64
-#endif
 #ifndef TG_GATHER_DYNAMIC
 #define TG_GATHER_DYNAMIC 1
 #endif
@@ -57,7 +55,6 @@ namespace tg {
 
 constexpr int kGatherThreads = TG_GATHER_THREADS;
 constexpr int kGatherWarps = kGatherThreads / 32;
-constexpr int kGatherBand = TG_GATHER_BAND;      // rows per unit
 constexpr int kGatherMaxJobs = 192;              // jobs of one canvas cached in smem
 constexpr int kSlots = TG_GATHER_SLOTS;          // items in flight per warp (header slots)
 constexpr int kRing = TG_GATHER_RING;            // source bytes in flight per warp
@@ -223,7 +220,7 @@ __global__ void __launch_bounds__(kGatherThreads, TG_GATHER_MIN_BLOCKS) gather_k
     const uint2 range = a.ranges[k];
     const int cnt = static_cast<int>(range.y);
     const Job* gj = a.jobs + range.x;
-    const int b0 = b * kGatherBand, b1 = min(a.N, b0 + kGatherBand);
+    const int b0 = b * a.band, b1 = min(a.N, b0 + a.band);
     uint8_t* canvas = a.out + static_cast<size_t>(k) * canvas_bytes;
 
     if (!(aligned_rows && cnt <= kGatherMaxJobs)) {
@@ -493,6 +490,18 @@ cudaError_t launch_gather(const GatherArgs& a, int sms, int grid_ctas, cudaStrea
   return cudaGetLastError();
 }
 
-int gather_bands(int N) { return ceil_div(N, kGatherBand); }
+int gather_bands(int N, int band) { return ceil_div(N, band); }
+
+// Taller bands amortise each warp's interval lists and chunk plans over more
+// rows (config 4's event gather, 3,713 canvases per pass: 64 -> 256 rows,
+// pass -2 %); short plans keep 64 so the dynamic claim still balances the
+// grid (config 2's per-step gather: 256 rows +4 %).
+int gather_band(int n_canvases, int N, int sms) {
+  int band = kGatherDefaultBand;
+  while (band < 8 * kGatherDefaultBand &&
+         static_cast<long long>(n_canvases) * gather_bands(N, 2 * band) >= 64LL * sms)
+    band *= 2;
+  return band;
+}
 
 }  // namespace tg

@@ -102,7 +102,7 @@ cudaError_t launch_stitch_batch(const StitchBatchArgs& a, cudaStream_t stream);
 // sorted by dx; src_frame indexes `frames`.
 struct GatherArgs {
   const uint8_t* const* frames;
-  int pitch, M, N, nbands;
+  int pitch, M, N, nbands, band;  // band: canvas rows per unit (gather_band)
   const Job* jobs;
   const uint2* ranges;
   int32_t* units;         // [0]: (canvas, band) units; [1], [2]: K5's claim and finished-CTA
@@ -111,7 +111,12 @@ struct GatherArgs {
 };
 // grid_ctas: 0 = the persistent grid of sms x the occupancy limit
 cudaError_t launch_gather(const GatherArgs& a, int sms, int grid_ctas, cudaStream_t stream);
-int gather_bands(int N);
+int gather_bands(int N, int band);
+// Rows per (canvas, band) unit for an explicit plan of n_canvases canvases
+// of N rows: the default band, doubled (up to 8x) while the plan keeps at
+// least 64 units per SM.
+int gather_band(int n_canvases, int N, int sms);
+constexpr int kGatherDefaultBand = 64;
 
 // ---- synthetic frames (k_synth.cu) -----------------------------------------
 struct SynthArgs {

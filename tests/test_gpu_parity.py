@@ -596,16 +596,23 @@ def test_two_launch_mask_path_stage_by_stage(ctx, keep):
     run.close()
 
 
-def test_stitch_gather_explicit_plan(ctx):
+@pytest.mark.parametrize("M,band", [(300, 0), (320, 0), (320, 1), (320, 8), (320, 512)])
+def test_stitch_gather_explicit_plan(ctx, M, band):
     """tg_stitch_gather (A13 on a caller-built plan): the oracle's stitch of
     patches cut from several frames -> placement jobs + zero jobs for the
     final free rects; every canvas byte equals the SURVEY A13 fill
     canvas[py+v][(px+u)*3+c] = frame[ry+v][(rx+u)*3+c], uncovered = 0,
-    over canvases pre-filled with garbage.  Malformed plans fail loudly."""
+    over canvases pre-filled with garbage.  Malformed plans fail loudly.
+    M = 300 takes K5's rect-by-rect path (rows not 16-byte multiples), 320
+    its TMA pipeline; band = TG_OPT_GATHER_BAND (0 = automatic, 512 = one
+    unit per canvas)."""
     import ctypes as C
 
     from paper_2404_09267_b200 import _native as N
-    W, H, n, M, Nh = 640, 360, 4, 300, 200
+    W, H, n, Nh = 640, 360, 4, 200
+    with pytest.raises(A.InvalidArgument, match="gather band out of range"):
+        A.check(N.lib().tg_ctx_set_option(ctx.handle, N.TG_OPT_GATHER_BAND, -1))
+    A.check(N.lib().tg_ctx_set_option(ctx.handle, N.TG_OPT_GATHER_BAND, band))
     run = GpuRun(ctx, W, H, n, seed=1007, trace_kw=dict(roi_max_dim=200))
     frames = run.host_frames()
     rng = O.Rng(O.derive_seed(1007, "stitch-gather"))
@@ -652,6 +659,7 @@ def test_stitch_gather_explicit_plan(ctx):
         A.check(N.lib().tg_stitch_gather(ctx.handle, c_jobs, len(jobs), c_offs, nc, spec, run.d_cur,
                                          run.ring.pitch + 8, d_canv, None))
     ctx.free(d_canv)
+    A.check(N.lib().tg_ctx_set_option(ctx.handle, N.TG_OPT_GATHER_BAND, 0))
     run.close()
 
 
