@@ -49,6 +49,11 @@ namespace tg {
 #define TG_GATHER_DYNAMIC 1
 #endif
 
+// explicit plans: units per SM below which bands stay at 64 rows (gather_band)
+#ifndef TG_GATHER_UNITS_PER_SM
+#define TG_GATHER_UNITS_PER_SM 64LL
+#endif
+
 #ifndef TG_GATHER_THREADS
 #define TG_GATHER_THREADS 256
 #endif
@@ -499,7 +504,7 @@ int gather_bands(int N, int band) { return ceil_div(N, band); }
 int gather_band(int n_canvases, int N, int sms) {
   int band = kGatherDefaultBand;
   while (band < 8 * kGatherDefaultBand &&
-         static_cast<long long>(n_canvases) * gather_bands(N, 2 * band) >= 64LL * sms)
+         static_cast<long long>(n_canvases) * gather_bands(N, 2 * band) >= TG_GATHER_UNITS_PER_SM * sms)
     band *= 2;
   return band;
 }
