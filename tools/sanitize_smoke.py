@@ -40,6 +40,14 @@ _, n_ev, n_canv = path.step()
 ctx.synchronize()
 print("batcher", n_ev, "events", n_canv, "canvases")
 path.close()
+A.check(N.lib().tg_ctx_set_option(ctx.handle, N.TG_OPT_GATHER_BAND, 256))  # tall units
+path = MC.MultiCameraPath(ctx, [0, 1], 640, 368, 4, [(1, 60.0, 3.0), (2, 85.0, 4.0)],
+                          bandwidth_mbps=40.0, trace_kw=dict(roi_max_dim=200))
+_, n_ev, n_canv = path.step()
+ctx.synchronize()
+print("batcher band 256", n_ev, "events", n_canv, "canvases")
+path.close()
+A.check(N.lib().tg_ctx_set_option(ctx.handle, N.TG_OPT_GATHER_BAND, 0))
 comm = A.Comm.nccl(ctx, A.Comm.unique_id(), 0, 1)  # device descriptor all-gather
 path = MC.MultiCameraPath(ctx, [0, 1], 640, 368, 4, [(1, 60.0, 3.0), (2, 85.0, 4.0)],
                           bandwidth_mbps=40.0, trace_kw=dict(roi_max_dim=200), comm=comm)
