@@ -53,6 +53,16 @@
 namespace tg {
 
 
+// Fused launch: the frame lines are streamed with evict_first (bit 0) and the
+// raw words stored with evict_last (bit 1), so more of the raw rows the K1b
+// tasks read back are still in L2 (300 4K frames: DRAM reads 7.86 -> 7.79
+// GB, config-2 step -0.4 %).  K1b tasks trailing the stream front by 8-frame
+// progress blocks (a publisher warp per CTA, a stream-order task table) on
+// top of this: 7.75 GB and no faster.
+#ifndef TG_K1_L2HINT
+#define TG_K1_L2HINT 3
+#endif
+
 constexpr int kK1MaxPartWords = 64;     // 32-pixel words per unit (one per consumer lane)
 constexpr int kK1Group = 2;             // warps per consumer group
 constexpr int kK1Groups = 8;            // consumer groups (units per item)
@@ -464,7 +474,13 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
             const uint8_t* src = ch.next(a, &out) + off;
             slot_f[slot] = out;
             mbar_arrive_expect_tx(&full[slot], bytes);
-            bulk_g2s(slots + static_cast<size_t>(slot) * a.slot_bytes, src, bytes, &full[slot]);
+#if TG_K1_L2HINT & 1
+            if (fused)
+              bulk_g2s_hint(slots + static_cast<size_t>(slot) * a.slot_bytes, src, bytes,
+                            &full[slot], l2_evict_first());
+            else
+#endif
+              bulk_g2s(slots + static_cast<size_t>(slot) * a.slot_bytes, src, bytes, &full[slot]);
             used |= bit;
             fills ^= bit;
             if (++k == S) k = 0;
@@ -512,7 +528,16 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
       if (++k == S) k = 0;
       if (f >= 0) {
         const uint32_t fw = fg_word<kLow>(cur, prv, t1) & keep;
+#if TG_K1_L2HINT & 2
+        if (valid) {
+          if (fused)
+            st_hint(out + static_cast<size_t>(f) * fstride, fw, l2_evict_last());
+          else
+            out[static_cast<size_t>(f) * fstride] = fw;
+        }
+#else
         if (valid) out[static_cast<size_t>(f) * fstride] = fw;
+#endif
       }
       return f;
     };
