@@ -116,7 +116,12 @@ int gather_bands(int N, int band);
 // of N rows: the default band, doubled (up to 8x) while the plan keeps at
 // least 64 units per SM.
 int gather_band(int n_canvases, int N, int sms);
-constexpr int kGatherDefaultBand = 64;
+// per-frame pipeline gathers (config 2 K5: 0.667 ms at 64 rows, 0.678 at
+// 128, 0.739 at 32)
+#ifndef TG_GATHER_DEFAULT_BAND
+#define TG_GATHER_DEFAULT_BAND 64
+#endif
+constexpr int kGatherDefaultBand = TG_GATHER_DEFAULT_BAND;
 
 // ---- synthetic frames (k_synth.cu) -----------------------------------------
 struct SynthArgs {
