@@ -187,6 +187,25 @@ def ncu_traffic(name: str, units: int):
         return None
 
 
+def ncu_step_dram(name: str, units: int, ms_step: float):
+    """Every kernel's DRAM bytes per step from a committed ncu launch list
+    (profiles/), over this run's step time; None unless the run is the
+    profiled workload (same frame reads per step)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            d = json.load(f)
+        if d.get("frame_reads_per_launch") != units or "dram_bytes_per_step" not in d:
+            return None
+    except Exception:
+        return None
+    b = d["dram_bytes_per_step"]
+    gbps = b / (ms_step / 1e3) / 1e9
+    return {"bytes_per_step": int(b), "GBps": round(gbps, 1), "frac": round(gbps / peaks()[0], 4),
+            "def": "DRAM bytes of all the step's kernels (ncu dram__bytes_read + write, "
+                   "committed launch list) over the step time: how busy HBM is across the "
+                   "overlapped stages", "source": d.get("source")}
+
+
 class Clocks:
     """nvidia-smi sampler running during the timed region."""
 
@@ -357,7 +376,9 @@ def run_multicam(args):
                             {"events": path._nev, "canvases": n_canv,
                              "patches_admitted": int(len(pats)),
                              "canvas_efficiency_mean": round(patch_bytes / max(1, canvas_bytes), 4),
-                             "rank": rank}),
+                             "rank": rank,
+                             "dram_ncu": ncu_step_dram("r02_k1_cfg4_traffic.json", F_local + len(cams),
+                                                        ms_step)}),
         "clocks": clk,
         "gpu_launches": 4 * K,  # K1, K1b, planner (+descriptors), K5 per step
         "mask_path": {"k1": "mask_fg_kernel on every SM (cooperative-free, one CTA per SM)",
@@ -547,7 +568,8 @@ def measure_cfg2(args, rank, world, local, dist, ctx, secondary=False):
                        "gather": round(gat, 4)},
                       {"rois": int(res["n_rois"].sum()), "patches": int(res["n_patches"].sum()),
                        "admitted": int(res["admitted"].sum()), "canvases": ncanv,
-                       "canvas_efficiency_mean": round(adm_bytes / max(1, ncanv * CANVAS_BYTES), 4)})
+                       "canvas_efficiency_mean": round(adm_bytes / max(1, ncanv * CANVAS_BYTES), 4),
+                       "dram_ncu": ncu_step_dram("k1_traffic.json", n + 1, ms_step)})
     workload = ("BASELINE configs[1]: synthetic 3840x2160 RGB camera per GPU, 300 frames, moderate "
                 "RoI density (roi_proportion_mean=0.10, roi_max_dim=480), 4x4 zones, 1024x1024 "
                 "canvases")

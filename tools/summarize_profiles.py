@@ -6,8 +6,9 @@ Reads gpurun_out/<tag>_launches.csv (ncu --metrics gpu__time_duration.sum,
 dram__bytes_read.sum,dram__bytes_write.sum launch list of a short bench run,
 tools/gpu/r02_profile.sh) and gpurun_out/<tag>_prof_<kernel>.ncu-rep (one
 --set full capture per hot kernel); writes profiles/<tag>_launches.csv,
-profiles/<tag>_summary.md and the K1 traffic record bench.py reads for
-roofline.traffic (DRAM bytes of one mask_fg launch per frame read).
+profiles/<tag>_summary.md and the traffic record bench.py reads for
+roofline.traffic (DRAM bytes of one mask_fg launch per frame read) and
+path.dram (every kernel's DRAM bytes per step).
 """
 from __future__ import annotations
 
@@ -83,6 +84,7 @@ def main(tag, reads, traffic_json, title):
              "|---|---|---|---|---|---|"]
     k1 = None
     total = 0.0
+    step_bytes = 0.0  # every kernel's mean DRAM bytes per launch (one launch per step each)
     for name, ms in per.items():
         if name.startswith("synth"):
             continue
@@ -90,6 +92,7 @@ def main(tag, reads, traffic_json, title):
         rd = sum(m["dram__bytes_read.sum"] for m in ms) / len(ms)
         wr = sum(m["dram__bytes_write.sum"] for m in ms) / len(ms)
         total += t
+        step_bytes += rd + wr
         lines.append(f"| {name} | {len(ms)} | {t:.4f} | {rd/1e9:.3f} | {wr/1e9:.3f} | "
                      f"{(rd+wr)/t/1e6:.0f} |")
         if name.startswith("mask_fg_kernel"):
@@ -124,6 +127,9 @@ def main(tag, reads, traffic_json, title):
         json.dump({"kernel": "mask_fg_kernel", "frame_reads_per_launch": reads,
                    "dram_bytes_per_launch": traffic, "dram_bytes_per_frame": traffic / reads,
                    "algorithmic_bytes_per_launch": reads * FRAME_BYTES,
+                   "dram_bytes_per_step": step_bytes,
+                   "dram_bytes_per_step_def": "sum over the step's kernels (one launch each) of "
+                                              "the mean dram__bytes_read + dram__bytes_write",
                    "source": f"profiles/{tag}_launches.csv"},
                   open(os.path.join(ROOT, traffic_json), "w"), indent=1)
     print("\n".join(lines))
