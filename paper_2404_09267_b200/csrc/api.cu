@@ -815,7 +815,10 @@ tg_status tg_pipeline_create(tg_ctx* ctx, const tg_pipeline_params* params, tg_p
   };
   cudaError_t e = cudaSuccess;
   // F raw frames + one zero frame (K1b's rows for columns outside the frame)
-  if (!e) e = alloc(&p->raw, (F + 1) * q.height * p->mask_words);
+  // ... then, split launches, the sparse bitmap's per-row word flags
+  // (kernels.cuh: raw_flag_words)
+  if (!e) e = alloc(&p->raw, (F + 1) * q.height * p->mask_words +
+                                 F * q.height * raw_flag_words(q.width));
   if (!e) e = cudaMemset(p->raw + F * q.height * p->mask_words, 0,
                          q.height * p->mask_words * sizeof(uint32_t));
   // K1 counters followed by the activity bits (p->active): one memset per launch
@@ -859,6 +862,12 @@ static const uint32_t* raw_zero(const tg_pipeline* p) {
   return p->raw + static_cast<size_t>(p->p.max_frames) * p->p.height * p->mask_words;
 }
 
+// the split launches' word flags (null: dense raw bitmap, kernels.cuh)
+static uint32_t* raw_flags(const tg_pipeline* p) {
+  if (!raw_flag_words(p->p.width)) return nullptr;
+  return p->raw + static_cast<size_t>(p->p.max_frames + 1) * p->p.height * p->mask_words;
+}
+
 tg_status tg_pipeline_stage_mask_fg(tg_pipeline* p, int32_t n_frames, const uint8_t* const* d_cur,
                                     const uint8_t* const* d_prev, void* stream) {
   tg_status s = use_device(p->ctx);
@@ -868,7 +877,8 @@ tg_status tg_pipeline_stage_mask_fg(tg_pipeline* p, int32_t n_frames, const uint
   if (n_frames > 0 && (!d_cur || !d_prev))
     return fail(TG_ERR_INVALID_ARGUMENT, "null frame pointer table");
   TG_CUDA(launch_mask_fg(d_cur, d_prev, n_frames, p->p.width, p->p.height, p->p.pitch,
-                         p->p.threshold, p->raw, p->ctx->sms, pick(p->ctx, stream)));
+                         p->p.threshold, p->raw, raw_flags(p), p->ctx->sms,
+                         pick(p->ctx, stream)));
   return TG_OK;
 }
 
@@ -877,7 +887,7 @@ tg_status tg_pipeline_stage_mask_cells(tg_pipeline* p, int32_t n_frames, void* s
   if (s) return s;
   if (n_frames < 0 || n_frames > p->p.max_frames)
     return fail(TG_ERR_INVALID_ARGUMENT, "n_frames must be in [0, max_frames]");
-  TG_CUDA(launch_dilate_cells(p->raw, raw_zero(p), n_frames, p->p.width, p->p.height,
+  TG_CUDA(launch_dilate_cells(p->raw, raw_zero(p), raw_flags(p), n_frames, p->p.width, p->p.height,
                               p->p.dilate_radius,
                               p->cells, p->active, p->p.keep_mask ? p->mask : nullptr,
                               pick(p->ctx, stream)));
@@ -897,7 +907,7 @@ tg_status tg_pipeline_stage_mask(tg_pipeline* p, int32_t n_frames, const uint8_t
   // cannot co-schedule one K1 CTA per SM (e.g. a shared GPU).
   const cudaError_t e = launch_mask_fused(
       d_cur, d_prev, n_frames, p->p.width, p->p.height, p->p.pitch, p->p.threshold,
-      p->p.dilate_radius, p->raw, raw_zero(p), p->cells, p->active,
+      p->p.dilate_radius, p->raw, raw_zero(p), raw_flags(p), p->cells, p->active,
       p->p.keep_mask ? p->mask : nullptr,
       p->mask_sync, p->ctx->sms, pick(p->ctx, stream));
   if (e == cudaSuccess) {

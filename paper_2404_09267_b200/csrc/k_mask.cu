@@ -44,7 +44,14 @@
 // 1.49 ms -- K1b on the streaming SMs slows the stream more than it hides;
 // L2 evict_first on the frame stream + evict_last on the raw words cut DRAM
 // reads by 0.14 GB but not time; a sparse raw bitmap (only non-zero words
-// written, plus per-row ballot masks) saved K1 15 us but cost K1b 60 us.
+// written, plus per-row ballot masks) saved K1 15 us but cost K1b 60 us in
+// the fused launch (round 1).  Round 2's form (TG_K1_SPARSE, kernels.cuh):
+// K1 stores only the 32-byte sectors holding a foreground bit plus one flag
+// word per 32 raw words per row (parts 32-word aligned, so a consumer warp's
+// ballot is one flag word), K1b loads a band's flags first, then only the
+// flagged words -- config-4 pass 11.43 -> 11.29 ms, config 3 8.74 -> 8.63
+// ms (split launches: the raw bitmap goes through DRAM), and with
+// TG_K1_SPARSE_FUSED the config-2 step 1.959 -> 1.935 ms (same boxes).
 #include <algorithm>
 #include <cstdlib>
 
@@ -81,7 +88,8 @@ constexpr int kK1MaxActWords = 16;      // K1b: act words per cell row (W <= 819
 struct DilateArgs {
   const uint32_t* raw;
   const uint32_t* zero;  // H * nwords zero words: the rows of columns outside the frame
-  int H, W, nwords, cells_x, cells_y, act_words;
+  const uint32_t* flags;  // split launches, sparse bitmap: [F][H][fwords] word flags
+  int H, W, nwords, fwords, cells_x, cells_y, act_words;
   uint32_t* cells;
   uint32_t* active;
   uint32_t* mask_out;
@@ -129,7 +137,7 @@ __device__ __forceinline__ void dilate_band(const DilateArgs& a, const uint32_t 
 // by other SMs during this launch -> L2 loads (ld.cg), activity bits straight
 // to global (zeroed before the launch); otherwise the CTA's act_s collects
 // them.
-template <int R, bool kFused, bool kMask>
+template <int R, bool kFused, bool kMask, bool kSparse = false>
 __device__ __forceinline__ void dilate_strip(const DilateArgs& a, int f, int cy0, int wi, int lane,
                                              uint32_t (*act_s)[kK1MaxActWords]) {
   const int nb = min(kK1bBands, a.cells_y - cy0);
@@ -141,10 +149,18 @@ __device__ __forceinline__ void dilate_strip(const DilateArgs& a, int f, int cy0
   const uint32_t keep = owns ? (w == a.nwords - 1 ? lastmask : 0xffffffffu) : 0u;
   const uint32_t* fr = col_ok ? a.raw + static_cast<size_t>(f) * a.H * a.nwords + w : a.zero;
   auto ld = [](const uint32_t* q) -> uint32_t { return kFused ? __ldcg(q) : __ldg(q); };
+  // sparse bitmap: a word is loaded only if its row's flag bit is set (the
+  // zero page stands in for the flags of columns outside the frame)
+  const uint32_t* fl = kSparse ? (col_ok ? a.flags + static_cast<size_t>(f) * a.H * a.fwords + (w >> 5)
+                                         : a.zero)
+                               : nullptr;
+  const uint32_t wbit = 1u << (w & 31);
   // rows outside [0, H) read a clamped row and are masked to zero
   auto raw_row = [&](int yy) -> uint32_t {
     const uint32_t m = (yy >= 0 && yy < a.H) ? 0xffffffffu : 0u;
-    return ld(fr + static_cast<size_t>(min(max(yy, 0), a.H - 1)) * a.nwords) & m;
+    const int yc = min(max(yy, 0), a.H - 1);
+    if (kSparse && !(ld(fl + static_cast<size_t>(yc) * a.fwords) & wbit)) return 0u;
+    return ld(fr + static_cast<size_t>(yc) * a.nwords) & m;
   };
   // window of raw rows yb0 - R .. yb0 + 15 + R; consecutive bands share 2R rows
   constexpr int kWin = kCell + 2 * R;
@@ -152,10 +168,18 @@ __device__ __forceinline__ void dilate_strip(const DilateArgs& a, int f, int cy0
 #pragma unroll
   for (int i = 0; i < 2 * R; ++i) win[i] = raw_row(cy0 * kCell - R + i);
   const uint32_t* q = fr + static_cast<size_t>(cy0 * kCell + R) * a.nwords;
-  for (int bi = 0; bi < nb; ++bi, q += kCell * a.nwords) {
+  const uint32_t* fq = kSparse ? fl + static_cast<size_t>(cy0 * kCell + R) * a.fwords : nullptr;
+  for (int bi = 0; bi < nb; ++bi, q += kCell * a.nwords, fq += kSparse ? kCell * a.fwords : 0) {
     const int yb0 = (cy0 + bi) * kCell, cy = cy0 + bi;
     const bool interior = yb0 + kCell + R <= a.H;  // uniform: no row past the frame
-    if (interior) {
+    if (kSparse && interior) {  // all flags first, then only the flagged words
+      uint32_t fb[kCell];
+#pragma unroll
+      for (int i = 0; i < kCell; ++i) fb[i] = ld(fq + i * a.fwords);
+#pragma unroll
+      for (int i = 2 * R; i < kWin; ++i)
+        win[i] = (fb[i - 2 * R] & wbit) ? ld(q + (i - 2 * R) * a.nwords) : 0u;
+    } else if (interior) {
 #pragma unroll
       for (int i = 2 * R; i < kWin; ++i) win[i] = ld(q + (i - 2 * R) * a.nwords);
     } else {
@@ -202,7 +226,7 @@ __device__ __forceinline__ void dilate_strip(const DilateArgs& a, int f, int cy0
   }
 }
 
-template <int R>  // dilation radius
+template <int R, bool kSparse>  // dilation radius, sparse raw bitmap
 __global__ void __launch_bounds__(320) dilate_cells_kernel(const DilateArgs a) {  // W <= 8192: <= 9 warps
   __shared__ uint32_t act_s[kK1bBands][kK1MaxActWords];
   const int strips = ceil_div(a.cells_y, kK1bBands);
@@ -211,9 +235,9 @@ __global__ void __launch_bounds__(320) dilate_cells_kernel(const DilateArgs a) {
   for (int i = threadIdx.x; i < kK1bBands * kK1MaxActWords; i += blockDim.x) (&act_s[0][0])[i] = 0;
   __syncthreads();
   if (a.mask_out)
-    dilate_strip<R, false, true>(a, f, cy0, threadIdx.x >> 5, threadIdx.x & 31, act_s);
+    dilate_strip<R, false, true, kSparse>(a, f, cy0, threadIdx.x >> 5, threadIdx.x & 31, act_s);
   else
-    dilate_strip<R, false, false>(a, f, cy0, threadIdx.x >> 5, threadIdx.x & 31, act_s);
+    dilate_strip<R, false, false, kSparse>(a, f, cy0, threadIdx.x >> 5, threadIdx.x & 31, act_s);
   __syncthreads();
   for (int i = threadIdx.x; i < nb * a.act_words; i += blockDim.x) {
     const int bi = i / a.act_words, aw = i - bi * a.act_words;
@@ -234,6 +258,8 @@ struct MaskArgs {
   int nslots;         // ring slots per group
   int slot_bytes;
   uint32_t* raw;      // [F][H][nwords] raw foreground bits
+  uint32_t* flags;    // split launch, sparse bitmap: [F][H][fwords] word flags (else null)
+  int fwords;
   // fused launch only (item_done == nullptr otherwise)
   uint32_t* item_done;  // [total_items] warps done per item (zeroed)
   uint32_t* task_next;  // K1b task queue head (zeroed)
@@ -380,6 +406,15 @@ __device__ __forceinline__ void wait_dilate_task(const MaskArgs& a, int t, int l
   }
 }
 
+// TG_K1_SPARSE_FUSED: the fused launch on the sparse bitmap too (K1 stores
+// keep evict_last, K1b tasks read flags + flagged words through L2):
+// config-2 step 1.959 -> 1.935 ms (same box), fused mask stage 1.250 ->
+// 1.229 ms.
+#ifndef TG_K1_SPARSE_FUSED
+#define TG_K1_SPARSE_FUSED 1
+#endif
+constexpr bool kFusedSparse = TG_K1_SPARSE && TG_K1_SPARSE_FUSED;
+
 __device__ __forceinline__ void run_dilate_task(const MaskArgs& a, int t, int lane) {
   __syncwarp();
   __threadfence();
@@ -389,9 +424,9 @@ __device__ __forceinline__ void run_dilate_task(const MaskArgs& a, int t, int la
 #define TG_DILATE_TASK(R) \
   case R:                 \
     if (a.d.mask_out)                                                          \
-      dilate_strip<R, true, true>(a.d, f, cy0, wi, lane, nullptr);             \
+      dilate_strip<R, true, true, kFusedSparse>(a.d, f, cy0, wi, lane, nullptr); \
     else                                                                       \
-      dilate_strip<R, true, false>(a.d, f, cy0, wi, lane, nullptr);            \
+      dilate_strip<R, true, false, kFusedSparse>(a.d, f, cy0, wi, lane, nullptr); \
     break;
     TG_DILATE_TASK(0) TG_DILATE_TASK(1) TG_DILATE_TASK(2) TG_DILATE_TASK(3) TG_DILATE_TASK(4)
     TG_DILATE_TASK(5) TG_DILATE_TASK(6) TG_DILATE_TASK(7) TG_DILATE_TASK(8)
@@ -513,6 +548,11 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
     uint32_t* out = a.raw + static_cast<size_t>(row) * a.nwords + w;
     const size_t fstride = static_cast<size_t>(a.H) * a.nwords;
     const uint32_t keep = w == a.nwords - 1 ? lastmask : 0xffffffffu;
+    // sparse: parts are 32-word aligned, so this warp's 32 words are one flag word
+    const bool sparse = a.flags != nullptr;
+    const int wbase = part * a.part_words + (warp - g * kK1Group) * 32;
+    const bool fseg = (warp - g * kK1Group) * 32 < a.part_words && wbase < a.nwords;
+    const int seg = wbase >> 5;
     // One stage: the next row of the chain into `cur`, diffed against `prv`
     // (the previous stage's row) unless it starts the chain.  The item ends
     // with frame fend-1 (a chain start never comes last); the two register
@@ -528,6 +568,21 @@ __global__ void __launch_bounds__(kK1Threads, 1) mask_fg_kernel(const MaskArgs a
       if (++k == S) k = 0;
       if (f >= 0) {
         const uint32_t fw = fg_word<kLow>(cur, prv, t1) & keep;
+#if TG_K1_SPARSE
+        if (sparse) {  // whole 8-word sectors holding a foreground bit + the row's flag word
+          const uint32_t b = __ballot_sync(0xffffffffu, valid && fw != 0u);
+          if (valid && ((b >> (lane & 24)) & 0xffu)) {
+#if TG_K1_L2HINT & 2
+            if (fused)
+              st_hint(out + static_cast<size_t>(f) * fstride, fw, l2_evict_last());
+            else
+#endif
+              out[static_cast<size_t>(f) * fstride] = fw;
+          }
+          if (lane == 0 && fseg) a.flags[(static_cast<size_t>(f) * a.H + row) * a.fwords + seg] = b;
+          return f;
+        }
+#endif
 #if TG_K1_L2HINT & 2
         if (valid) {
           if (fused)
@@ -573,6 +628,8 @@ static DilateArgs dilate_args(const uint32_t* d_raw, const uint32_t* d_zero, int
   DilateArgs d;
   d.raw = d_raw;
   d.zero = d_zero;
+  d.flags = nullptr;
+  d.fwords = 0;
   d.H = H;
   d.W = W;
   d.nwords = ceil_div(W, 32);
@@ -588,7 +645,7 @@ static DilateArgs dilate_args(const uint32_t* d_raw, const uint32_t* d_zero, int
 // K1 work decomposition (items, ring slots) for one launch.
 static cudaError_t plan_k1(MaskArgs& a, const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                            int n_frames, int W, int H, int pitch, int threshold, uint32_t* d_raw,
-                           int sms, size_t* smem) {
+                           int sms, size_t* smem, uint32_t* d_flags = nullptr) {
   a = MaskArgs{};
   a.cur = d_cur;
   a.prev = d_prev;
@@ -602,6 +659,12 @@ static cudaError_t plan_k1(MaskArgs& a, const uint8_t* const* d_cur, const uint8
   a.nparts = ceil_div(a.nwords, kK1MaxPartWords);
   if (a.nparts > kK1Groups) return cudaErrorInvalidConfiguration;  // W > 16384
   a.part_words = ceil_div(a.nwords, a.nparts);
+  if (d_flags) {  // sparse bitmap: 32-word aligned parts (one flag word per consumer warp)
+    a.part_words = ceil_div(a.part_words, 32) * 32;
+    a.nparts = ceil_div(a.nwords, a.part_words);
+    a.flags = d_flags;
+    a.fwords = ceil_div(a.nwords, 32);
+  }
   a.rows_per_item = kK1Groups / a.nparts;
   a.nrb = ceil_div(H, a.rows_per_item);
   a.slot_bytes = (a.part_words * 96 + 127) & ~127;
@@ -624,11 +687,12 @@ static cudaError_t plan_k1(MaskArgs& a, const uint8_t* const* d_cur, const uint8
 
 cudaError_t launch_mask_fg(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                            int n_frames, int W, int H, int pitch, int threshold, uint32_t* d_raw,
-                           int sms, cudaStream_t stream) {
+                           uint32_t* d_flags, int sms, cudaStream_t stream) {
   if (n_frames <= 0) return cudaSuccess;
   MaskArgs a;
   size_t smem = 0;
-  cudaError_t e = plan_k1(a, d_cur, d_prev, n_frames, W, H, pitch, threshold, d_raw, sms, &smem);
+  cudaError_t e =
+      plan_k1(a, d_cur, d_prev, n_frames, W, H, pitch, threshold, d_raw, sms, &smem, d_flags);
   if (e != cudaSuccess) return e;
   int grid = std::min(a.total_items, sms);
   grid = std::max(1, std::min(a.total_items, env_or(g_env_grid, grid)));
@@ -645,16 +709,20 @@ size_t mask_sync_words(int H, int sms) { return static_cast<size_t>(8) * sms + H
 
 cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                               int n_frames, int W, int H, int pitch, int threshold, int radius,
-                              uint32_t* d_raw, const uint32_t* d_zero, uint32_t* d_cells,
-                              uint32_t* d_active, uint32_t* d_mask, uint32_t* d_sync, int sms,
-                              cudaStream_t stream) {
+                              uint32_t* d_raw, const uint32_t* d_zero, uint32_t* d_flags,
+                              uint32_t* d_cells, uint32_t* d_active, uint32_t* d_mask,
+                              uint32_t* d_sync, int sms, cudaStream_t stream) {
   if (n_frames <= 0) return cudaSuccess;
   if (radius < 0 || radius > kMaxRadius) return cudaErrorInvalidValue;
+  if (!kFusedSparse) d_flags = nullptr;
   MaskArgs a;
   size_t smem = 0;
-  cudaError_t e = plan_k1(a, d_cur, d_prev, n_frames, W, H, pitch, threshold, d_raw, sms, &smem);
+  cudaError_t e =
+      plan_k1(a, d_cur, d_prev, n_frames, W, H, pitch, threshold, d_raw, sms, &smem, d_flags);
   if (e != cudaSuccess) return e;
   a.d = dilate_args(d_raw, d_zero, W, H, d_cells, d_active, d_mask);
+  a.d.flags = d_flags;
+  a.d.fwords = a.fwords;
   if (a.d.act_words > kK1MaxActWords) return cudaErrorInvalidConfiguration;
   const size_t sync_words = mask_sync_words(H, sms);
   if (static_cast<size_t>(a.total_items) + 1 > sync_words) return cudaErrorInvalidConfiguration;
@@ -700,18 +768,24 @@ cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const*
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-cudaError_t launch_dilate_cells(const uint32_t* d_raw, const uint32_t* d_zero, int n_frames,
+cudaError_t launch_dilate_cells(const uint32_t* d_raw, const uint32_t* d_zero,
+                                const uint32_t* d_flags, int n_frames,
                                 int W, int H, int radius, uint32_t* d_cells, uint32_t* d_active,
                                 uint32_t* d_mask, cudaStream_t stream) {
   if (n_frames <= 0) return cudaSuccess;
-  const DilateArgs d = dilate_args(d_raw, d_zero, W, H, d_cells, d_active, d_mask);
+  DilateArgs d = dilate_args(d_raw, d_zero, W, H, d_cells, d_active, d_mask);
+  d.flags = d_flags;
+  d.fwords = ceil_div(d.nwords, 32);
   if (d.act_words > kK1MaxActWords) return cudaErrorInvalidConfiguration;
   const int dwarps = ceil_div(d.nwords, kK1GroupWords);
   const dim3 dg(n_frames * ceil_div(d.cells_y, kK1bBands)), db(dwarps * 32);
   switch (radius) {
 #define TG_DILATE_CASE(R) \
   case R:                 \
-    dilate_cells_kernel<R><<<dg, db, 0, stream>>>(d); \
+    if (d_flags)          \
+      dilate_cells_kernel<R, TG_K1_SPARSE != 0><<<dg, db, 0, stream>>>(d); \
+    else                  \
+      dilate_cells_kernel<R, false><<<dg, db, 0, stream>>>(d); \
     break;
     TG_DILATE_CASE(0) TG_DILATE_CASE(1) TG_DILATE_CASE(2) TG_DILATE_CASE(3) TG_DILATE_CASE(4)
     TG_DILATE_CASE(5) TG_DILATE_CASE(6) TG_DILATE_CASE(7) TG_DILATE_CASE(8)

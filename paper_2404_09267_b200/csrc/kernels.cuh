@@ -6,11 +6,21 @@
 namespace tg {
 
 // ---- K1 (k_mask.cu) --------------------------------------------------------
+// Split launches (K1, then K1b): with TG_K1_SPARSE the raw bitmap is sparse --
+// K1 stores only the 32-byte sectors (8 words) that hold a foreground bit and
+// one flag word per 32 raw words per row (bit i: word i is non-zero), K1b
+// loads only flagged words; the unstored words keep stale bits nobody reads.
+// d_flags: n_frames * H * raw_flag_words(W) words (null: dense bitmap).
+#ifndef TG_K1_SPARSE
+#define TG_K1_SPARSE 1
+#endif
+inline int raw_flag_words(int W) { return TG_K1_SPARSE ? (W + 1023) / 1024 : 0; }
 cudaError_t launch_mask_fg(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                            int n_frames, int W, int H, int pitch, int threshold, uint32_t* d_raw,
-                           int sms, cudaStream_t stream);
+                           uint32_t* d_flags, int sms, cudaStream_t stream);
 // d_zero: H * ceil(W/32) zero words (what K1b reads for columns outside the frame)
-cudaError_t launch_dilate_cells(const uint32_t* d_raw, const uint32_t* d_zero, int n_frames,
+cudaError_t launch_dilate_cells(const uint32_t* d_raw, const uint32_t* d_zero,
+                                const uint32_t* d_flags, int n_frames,
                                 int W, int H, int radius, uint32_t* d_cells, uint32_t* d_active,
                                 uint32_t* d_mask, cudaStream_t stream);
 // K1 + K1b in one cooperative launch (K1b tasks run beside the stream);
@@ -19,9 +29,9 @@ cudaError_t launch_dilate_cells(const uint32_t* d_raw, const uint32_t* d_zero, i
 size_t mask_sync_words(int H, int sms);
 cudaError_t launch_mask_fused(const uint8_t* const* d_cur, const uint8_t* const* d_prev,
                               int n_frames, int W, int H, int pitch, int threshold, int radius,
-                              uint32_t* d_raw, const uint32_t* d_zero, uint32_t* d_cells,
-                              uint32_t* d_active, uint32_t* d_mask, uint32_t* d_sync, int sms,
-                              cudaStream_t stream);
+                              uint32_t* d_raw, const uint32_t* d_zero, uint32_t* d_flags,
+                              uint32_t* d_cells, uint32_t* d_active, uint32_t* d_mask,
+                              uint32_t* d_sync, int sms, cudaStream_t stream);
 
 // ---- K2-K4 per-frame planner + frame-order prefix (k_plan.cu) --------------
 struct PlanArgs {

@@ -596,6 +596,48 @@ def test_two_launch_mask_path_stage_by_stage(ctx, keep):
     run.close()
 
 
+@pytest.mark.parametrize("case", [
+    dict(W=208, H=100, n=4, radius=2),                 # W % 32 == 16, H % 16 != 0
+    dict(W=96, H=64, n=6, radius=3),
+    dict(W=640, H=360, n=5, radius=0),
+    dict(W=640, H=360, n=5, radius=8),
+    dict(W=640, H=360, n=5, threshold=0),              # every noisy byte is foreground
+    dict(W=1000, H=77, n=4, pitch=3008),               # 32 words: one 32-word part
+    dict(W=8192, H=48, n=3),                           # 4 K1 parts per row
+    dict(W=2080, H=70, n=5),                           # 65 words: parts of 64 + 1 (sparse)
+    dict(W=5008, H=40, n=3),
+    dict(W=16, H=8, n=4),                              # half a word
+    dict(W=32, H=3000, n=2),                           # tall
+    dict(W=3840, H=2160, n=3),                         # 4K: parts of 64 + 56 words (sparse)
+])
+@pytest.mark.parametrize("keep", [True, False])
+def test_two_launch_mask_path_over_stale_bitmap(ctx, case, keep):
+    """The split K1 / K1b launches (configs 3/4 run them; with TG_K1_SPARSE
+    K1 stores only the raw sectors holding foreground plus per-row word
+    flags) at edge geometries, over a raw bitmap a first pass on other,
+    dense frames left full of stale bits: bit-exact vs the oracle."""
+    from paper_2404_09267_b200 import _native as N
+    lib = N.lib()
+    case = dict(case)
+    W, H, n = case.pop("W"), case.pop("H"), case.pop("n")
+    run = GpuRun(ctx, W, H, n, seed=7, trace_kw=dict(roi_max_dim=min(480, W, H)),
+                 keep_mask=keep, **case)
+    junk = GpuRun(ctx, W, H, n, seed=99, pitch=run.ring.pitch,
+                  trace_kw=dict(roi_proportion_mean=0.59, roi_max_dim=min(W, H), roi_count_max=30))
+    h = run.pipe.handle
+    A.check(lib.tg_pipeline_stage_mask_fg(h, n, junk.d_cur, junk.d_prev, None))
+    A.check(lib.tg_pipeline_stage_mask_cells(h, n, None))
+    A.check(lib.tg_pipeline_stage_mask_fg(h, n, run.d_cur, run.d_prev, None))
+    A.check(lib.tg_pipeline_stage_mask_cells(h, n, None))
+    A.check(lib.tg_pipeline_stage_plan(h, n, run.d_ids, run.d_gen, run.first_patch_id, None))
+    A.check(lib.tg_pipeline_stage_gather(h, n, run.d_cur, run.d_canvases, None))
+    run.ctx.stream_sync()
+    run.res = run.pipe.results(n)
+    _compare_full(run, run.res, run.oracle())
+    junk.close()
+    run.close()
+
+
 @pytest.mark.parametrize("M,band", [(300, 0), (320, 0), (320, 1), (320, 8), (320, 512)])
 def test_stitch_gather_explicit_plan(ctx, M, band):
     """tg_stitch_gather (A13 on a caller-built plan): the oracle's stitch of

@@ -41,9 +41,17 @@ def launches(path):
     return d
 
 
+def page(rep, name):
+    """One report page as CSV text: from the .ncu-rep, or from the
+    <rep>.<page>.csv the box exported (reports too large to copy back)."""
+    if os.path.exists(rep):
+        return subprocess.run(["ncu", "-i", rep, "--page", name, "--csv"], capture_output=True,
+                              text=True).stdout
+    return open(f"{rep[:-len('.ncu-rep')]}.{name}.csv").read()
+
+
 def details(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True,
-                         text=True).stdout
+    out = page(rep, "details")
     rows = list(csv.reader(out.splitlines()))
     h = rows[0]
     mi, vi, ui = h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
@@ -51,8 +59,7 @@ def details(rep):
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    out = page(rep, "raw")
     rows = list(csv.reader(out.splitlines()))
     return dict(zip(rows[0], rows[2]))
 
@@ -105,7 +112,7 @@ def main(tag, reads, traffic_json, title):
                   f"{(k1['read']+k1['write'])/alg:.3f}x the algorithmic bytes.", ""]
     for kern in KERNELS:
         rep = os.path.join(OUT, f"{tag}_prof_{kern}.ncu-rep")
-        if not os.path.exists(rep):
+        if not (os.path.exists(rep) or os.path.exists(rep[:-len(".ncu-rep")] + ".raw.csv")):
             continue
         det, r = details(rep), raw(rep)
         lines.append(f"## {kern} (ncu --set full)")
