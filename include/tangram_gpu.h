@@ -226,7 +226,9 @@ tg_status tg_pipeline_run(tg_pipeline* p, int32_t n_frames, const uint8_t* const
 
 /* The same stages one by one (parity tests, profiling).  stage_mask =
  * stage_mask_fg (K1: raw foreground bitmap) + stage_mask_cells (K1b:
- * dilation + cell summaries). */
+ * dilation + cell summaries).  The raw bitmap is sparse (only the 32-byte
+ * sectors holding foreground are stored, plus per-row word flags), so a
+ * stage_mask_cells reads the bitmap of the pipeline's last stage_mask_fg. */
 tg_status tg_pipeline_stage_mask(tg_pipeline* p, int32_t n_frames, const uint8_t* const* d_cur,
                                  const uint8_t* const* d_prev, void* stream);
 tg_status tg_pipeline_stage_mask_fg(tg_pipeline* p, int32_t n_frames, const uint8_t* const* d_cur,

@@ -602,7 +602,7 @@ def test_two_launch_mask_path_stage_by_stage(ctx, keep):
     dict(W=640, H=360, n=5, radius=0),
     dict(W=640, H=360, n=5, radius=8),
     dict(W=640, H=360, n=5, threshold=0),              # every noisy byte is foreground
-    dict(W=1000, H=77, n=4, pitch=3008),               # 32 words: one 32-word part
+    dict(W=992, H=77, n=4),                            # 31 words: one 32-word part
     dict(W=8192, H=48, n=3),                           # 4 K1 parts per row
     dict(W=2080, H=70, n=5),                           # 65 words: parts of 64 + 1 (sparse)
     dict(W=5008, H=40, n=3),
